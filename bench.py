@@ -1,0 +1,431 @@
+"""Benchmark: forward + adjoint PISO steps on the 3D turbulent channel.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c4|c5|c2|c1] [--no-cpu-baseline]
+
+Metric (BASELINE.json): Mcell-steps/s of forward+adjoint PISO on the 3D
+channel; one "step" = one taped ``piso_step`` plus its ``backward_step``
+(FULL gradient path) for a fixed cotangent, on the C4 workload
+make_channel((256, 192, 256), ratio=1.03) + reichardt_init(Re_tau=180,
+perturbation 0.1, seed 0), dt = 0.3 (2 pi/256) / max|u0|, tol 1e-8, fp64,
+per-step wall forcing.  The state advances, warm starts are on (the
+reference's run_rollout setting), inputs (>10 GB working set) exceed L2.
+
+Multi-GPU (torchrun, N>1): every rank advances its own C4 replica (weak
+scaling, no data-path collective); value = all ranks' cell-steps / max-over-
+ranks device time.
+
+--impl reference runs the reference's own CPU implementation (pisoflow,
+built unmodified into oracle/_ref by oracle/build_ref.py) on rank 0, one
+single-threaded process per host core up to 8, each advancing a bounded
+sample of the workload (the same channel recipe at 64x48x64 cells).
+"""
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Mcell-steps/s fwd+adjoint PISO, 3D channel"
+UNIT = "Mcell-steps/s"
+
+CONFIGS = {
+    # name: (shape, ratio, cfl factor, description)
+    "c4": ((256, 192, 256), 1.03, 0.3,
+           "C4 channel 256x192x256 Re_tau=180, fwd+adjoint"),
+    "c5": ((64, 48, 64), 1.095, 0.5,
+           "C5 channel 64x48x64 Re_tau=180 (per sample), fwd+adjoint"),
+    "slab8": ((128, 96, 128), 1.03, 0.3,
+              "C4 per-GPU slab proxy 128x96x128, fwd+adjoint"),
+}
+SAMPLE_SHAPE = (64, 48, 64)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-iters", type=int, default=20)
+    ap.add_argument("--tol", type=float, default=1e-8)
+    ap.add_argument("--reference-worker", action="store_true",
+                    help=argparse.SUPPRESS)
+    ap.add_argument("--worker-steps", type=int, default=1,
+                    help=argparse.SUPPRESS)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# reference CPU arm
+
+
+def reference_worker(args):
+    """One single-threaded reference process: build the sample channel with
+    the reference's own API, take `worker-steps` fwd+adjoint steps, print
+    cell-steps and seconds (domain build excluded)."""
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS",
+              "PISOFLOW_THREADS"):
+        os.environ[k] = "1"
+    from oracle import build_ref
+    sys.path.insert(0, build_ref.ref_path())
+    import numpy as np
+    from pisoflow import adjoint, kernels, mesh, piso
+    shape = SAMPLE_SHAPE
+    dom = mesh.make_channel(shape, ratio=CONFIGS["c4"][1])
+    state, nu, u_tau = piso.reichardt_init(dom, 180.0, perturbation=0.1,
+                                           seed=0)
+    dt = CONFIGS["c4"][2] * (2 * np.pi / shape[0]) / np.abs(state.u).max()
+    rng = np.random.default_rng(0)
+    w = rng.standard_normal((dom.n, 3))
+    ws = piso.PisoWorkspace(dom)
+    t0 = time.perf_counter()
+    iters = []
+    for _ in range(args.worker_steps):
+        src = piso.wall_forcing_source(dom, state.u, nu)
+        cfg = piso.StepConfig(dt=dt, nu=nu, source=src, tol=args.tol)
+        tape = piso.StepTape()
+        state, dg = piso.piso_step(dom, state, cfg, ws, tape)
+        g = adjoint.backward_step(dom, tape,
+                                  adjoint.GradState(u=w, p=np.zeros(dom.n)),
+                                  tol=args.tol)
+        iters.append((dg.momentum_iterations, dg.pressure_iterations,
+                      g.solve_iterations))
+    sec = time.perf_counter() - t0
+    print(json.dumps({"cell_steps": dom.n * args.worker_steps,
+                      "seconds": sec, "lane": kernels.LANE,
+                      "iterations": iters}))
+
+
+def run_reference_sample(procs, steps, tol):
+    """Run `procs` concurrent reference workers; aggregate Mcell-steps/s."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--reference-worker",
+           "--worker-steps", str(steps), "--tol", str(tol)]
+    t0 = time.perf_counter()
+    ps = [subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                           text=True, cwd=ROOT) for _ in range(procs)]
+    outs = []
+    for p in ps:
+        o, e = p.communicate(timeout=1800)
+        if p.returncode != 0:
+            raise RuntimeError(f"reference worker failed: {e[-2000:]}")
+        outs.append(json.loads(o.strip().splitlines()[-1]))
+    wall = time.perf_counter() - t0
+    cells = sum(o["cell_steps"] for o in outs)
+    slowest = max(o["seconds"] for o in outs)
+    return {"value": cells / slowest / 1e6, "seconds": slowest,
+            "cell_steps": cells, "procs": procs, "lane": outs[0]["lane"],
+            "iterations": outs[0]["iterations"], "wall": wall}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    procs = max(1, min(os.cpu_count() or 1, 8))
+    steps = max(1, args.steps)
+    try:
+        from oracle import build_ref
+        if not build_ref.build():
+            raise RuntimeError("oracle/_ref missing")
+        # warm-up: W single steps are not timed; the sample already excludes
+        # domain construction
+        r = run_reference_sample(procs, steps, args.tol)
+    except Exception as exc:  # the oracle always exists; report why not
+        print(json.dumps({"impl": "reference", "unavailable": str(exc)[:300]}))
+        return
+    sample = (f"reference pisoflow (lane {r['lane']}) on channel "
+              f"{'x'.join(map(str, SAMPLE_SHAPE))} (same recipe as C4, "
+              f"1/64 of its cells), {steps} fwd+adjoint step(s) per process, "
+              f"{procs} concurrent single-threaded processes")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": r["value"],
+        "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * r["seconds"] / steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, sample=True),
+        "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": procs,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "reference_iterations": r["iterations"],
+    }
+    print(json.dumps(line))
+
+
+def workload_config(args, sample=False):
+    shape, ratio, cfl, desc = CONFIGS[args.config]
+    return {"workload": desc, "grid": list(shape),
+            "cells": int(math.prod(shape)), "wall_ratio": ratio,
+            "dt_rule": f"{cfl}*(2pi/{shape[0]})/max|u0|", "tol": args.tol,
+            "gradient_path": "full",
+            "parallelism": ("replicas" if args.gpus > 1 else "single"),
+            "l2": "inputs larger than L2 (no flush needed)",
+            "reference_sample": list(SAMPLE_SHAPE) if sample else None}
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,"
+             "clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
+                    "samples": 0}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() in ("active", "1"):
+                    reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def build_workload(args, dev):
+    import numpy as np
+    import torch
+    from paper_2505_16992_b200 import channel, mesh
+    shape, ratio, cfl, _ = CONFIGS[args.config]
+    dom = mesh.make_channel(shape, ratio=ratio)
+    state, nu, u_tau = channel.reichardt_init(dom, 180.0, perturbation=0.1,
+                                              seed=0, device=dev)
+    dt = cfl * (2 * np.pi / shape[0]) / float(state.u.abs().max())
+    forcing = channel.WallForcing(dom, dev)
+    g = torch.Generator(device="cpu").manual_seed(0)
+    w = torch.randn((dom.n, 3), generator=g, dtype=torch.float64).to(dev)
+    return dom, state, nu, dt, forcing, w
+
+
+def main():
+    args = parse()
+    if args.reference_worker:
+        return reference_worker(args)
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2505_16992_b200 import _lib, adjoint, piso
+
+    dom, state0, nu, dt, forcing, w = build_workload(args, dev)
+    plan = dom.device_plan(dev)
+    cot = adjoint.GradState(u=w, p=torch.zeros(dom.n, dtype=torch.float64,
+                                               device=dev))
+    ws = piso.PisoWorkspace(dom)
+    stats = {"mom": 0, "p": 0, "adj": 0, "steps": 0}
+
+    def step(state):
+        cfg = piso.StepConfig(dt=dt, nu=nu, source=forcing(state.u, nu),
+                              tol=args.tol)
+        tape = piso.StepTape()
+        new, dg = piso.piso_step(dom, state, cfg, ws, tape)
+        g = adjoint.backward_step(dom, tape, cot, tol=args.tol)
+        stats["mom"] += dg.momentum_iterations
+        stats["p"] += dg.pressure_iterations
+        stats["adj"] += g.solve_iterations
+        stats["steps"] += 1
+        return new, g
+
+    state = state0
+    for _ in range(args.warmup):
+        state, _ = step(state)
+    for k in stats:
+        stats[k] = 0
+
+    lib = _lib.load()
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    l0 = lib.pf_launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        state, grad = step(state)
+    e1.record()
+    torch.cuda.synchronize()
+    launches = lib.pf_launch_count() - l0
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * dom.n * args.steps / (ms / 1e3) / 1e6
+    it_per_step = {k: stats[k] / max(stats["steps"], 1)
+                   for k in ("mom", "p", "adj")}
+
+    # end to end through the public API with host buffers
+    u_host = state.u.detach().cpu().pin_memory()
+    out_u = torch.empty_like(u_host).pin_memory()
+    out_g = torch.empty_like(u_host).pin_memory()
+    bc_host = [b.detach().cpu() for b in state.bc]
+    h2d = u_host.numel() * 8 + sum(b.numel() * 8 for b in bc_host)
+    d2h = 2 * out_u.numel() * 8
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record()
+    for _ in range(args.steps):
+        st = piso.FlowState(u=u_host.to(dev, non_blocking=True),
+                            p=state.p, bc=[b.to(dev) for b in bc_host],
+                            t=state.t, step=state.step)
+        new, g = step(st)
+        out_u.copy_(new.u, non_blocking=True)
+        out_g.copy_(g.u, non_blocking=True)
+    e3.record()
+    torch.cuda.synchronize()
+    ms_e2e = e2.elapsed_time(e3)
+    if world > 1:
+        t = torch.tensor([ms_e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    e2e_value = world * dom.n * args.steps / (ms_e2e / 1e3) / 1e6
+
+    # roofline of the dominant kernel (CG SpMV) on this step's operator
+    import ctypes
+    from paper_2505_16992_b200 import piso as P
+    c = P.assemble_momentum(dom, state.u, nu, dt)
+    k = torch.empty_like(c)
+    _lib.call("pf_assemble_pressure", plan.handle, _lib.ptr(c), 0,
+              _lib.ptr(k), plan.stream)
+    b = torch.randn(dom.n, dtype=torch.float64, device=dev)
+    ms3 = (ctypes.c_double * 3)()
+    _lib.call("pf_cg_profile", plan.handle, _lib.ptr(k), _lib.ptr(b),
+              args.profile_iters, _lib.ptr(plan.workspace), ms3, plan.stream)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    n = dom.n
+    spmv_bytes = 40 * n          # (d+2) s: 3 face coefficients + x + y
+    iter_bytes = 136 * n         # SURVEY §8 d fused Jacobi-PCG iteration
+    spmv_gbs = spmv_bytes / (ms3[0] * 1e-3) / 1e9
+    iter_ms = ms3[0] + ms3[1] + ms3[2]
+    iter_gbs = iter_bytes / (iter_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic_spmv.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.config)
+        except (OSError, ValueError):
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            r = run_reference_sample(1, 1, args.tol)
+            cpu = {"value": r["value"], "unit": UNIT, "cores": 1,
+                   "kind": "reference",
+                   "sample": (f"reference pisoflow (lane {r['lane']}) on "
+                              f"channel {'x'.join(map(str, SAMPLE_SHAPE))} "
+                              "(same recipe, 1/64 of C4 cells), 1 fwd+adjoint"
+                              f" step, {r['seconds']:.1f} s"),
+                   "iterations": r["iterations"]}
+        except Exception as exc:
+            cpu = {"value": None, "unit": UNIT, "cores": 1,
+                   "kind": "reference", "sample": f"failed: {exc}"[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reichardt_init seed 0, random cotangent)",
+            "config": workload_config(args),
+            "roofline": {"bound": "hbm", "kernel": "k_cg_spmv (PCG SpMV + p.Ap)",
+                         "achieved": spmv_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": spmv_gbs / peak, "traffic": traffic,
+                         "peak_source": peak_src,
+                         "bytes_per_cell": 40, "ms_per_launch": ms3[0],
+                         "cg_iteration": {"bytes_per_cell": 136,
+                                          "ms": iter_ms,
+                                          "achieved_gbs": iter_gbs,
+                                          "frac": iter_gbs / peak,
+                                          "ms_per_kernel": list(ms3)}},
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches),
+            "iterations_per_step": it_per_step,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,274 @@
+/*
+ * pisob200.h -- C ABI of the B200-native differentiable PISO step.
+ *
+ * Drop-in boundary for the hot path of the reference `pisoflow`
+ * (/root/reference/pkg/src/pisoflow, abbreviated S/ below): the forward
+ * PISO step `piso.piso_step` (S/piso.py:561-654), its discrete adjoint
+ * `adjoint.backward_step` (S/adjoint.py:412-506) and the Krylov solvers they
+ * run (`linalg.cg_solve` S/linalg.py:258-273, `linalg.bicgstab_solve`
+ * S/linalg.py:276-281, both through `_run_with_fallback` S/linalg.py:215-255).
+ *
+ * Conventions
+ *  - Every pointer is a DEVICE pointer (cudaMalloc / torch allocation) unless
+ *    the parameter name ends in `_host`.  The library never allocates device
+ *    memory: outputs and scratch are passed in by the caller (torch owns every
+ *    buffer).  Scratch sizes come from pf_workspace_bytes().
+ *  - `stream` is a cudaStream_t passed as void*; all work is stream ordered.
+ *    Solver entry points synchronise `stream` to read convergence status.
+ *  - Scalar fields are length n.  Vector fields are structure-of-arrays
+ *    (d, n): component c of cell i lives at v[c * n + i].  The Python layer
+ *    presents them as the reference's (n, d) arrays through transposed views.
+ *  - Stencils (matrices on the cell-adjacency pattern, the reference's CSR
+ *    `data` arrays, S/mesh.py:323-346) are stored as (2d + 1, n): row 0 is the
+ *    diagonal, row 1 + f the coefficient coupling cell i to its neighbour
+ *    across face f = 2 * axis + side (0 where the face is a boundary).
+ *  - Boundary faces (S/mesh.py:348-380) are flattened in the reference's
+ *    `domain.bfaces` order into m "boundary entries"; boundary velocities are
+ *    (d, m) SoA.
+ *  - Return value: 0 on success, a PF_ERR_* code otherwise; the message is
+ *    available from pf_last_error().  A non-converged solve is NOT an error
+ *    code: it is reported through pf_solver_report.converged == 0 (the Python
+ *    layer maps it to linalg.SolverError with the reference's stage label).
+ *  - Deterministic: no floating-point atomics; every reduction is a fixed
+ *    order tree, so repeated calls are bitwise identical (the contract of
+ *    T/test_adjoint.py:394-406).
+ */
+#ifndef PISOB200_H
+#define PISOB200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PF_API __attribute__((visibility("default")))
+#else
+#define PF_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PF_OK 0
+#define PF_ERR_ARG 1
+#define PF_ERR_CUDA 2
+#define PF_ERR_UNSUPPORTED 3
+
+#define PF_TOPO_GATHER 0 /* multi-block: packed neighbour table          */
+#define PF_TOPO_BOX 1    /* single block: neighbours by index arithmetic */
+
+#define PF_BKIND_DIRICHLET 0
+#define PF_BKIND_OUTFLOW 1
+
+/* Static, immutable mesh description (replaces the arrays of
+ * mesh.Domain, S/mesh.py:166-469).  All arrays are device pointers. */
+typedef struct pf_plan_desc {
+  int32_t dim;  /* 2 or 3 */
+  int32_t topo; /* PF_TOPO_* */
+  int64_t n;    /* number of cells */
+  /* PF_TOPO_BOX: block shape (C order, last axis fastest), periodicity per
+   * axis, and the first boundary-entry index of face (a, s) (-1 if periodic) */
+  int64_t box_shape[3];
+  int32_t box_periodic[3];
+  int64_t box_face_offset[6];
+  /* PF_TOPO_GATHER: (2d, n) packed neighbour table.  v >= 0: neighbour
+   * cell (bits 0-25), its axis seen across the face (bits 26-27; the
+   * reference's nbr_ax[a, s, i, a]) and orientation flip (bit 28;
+   * nbr_sign[a, s, i, a] == -1).  v < 0: boundary entry ~v. */
+  const int32_t *nbr;
+  /* cell metrics (S/mesh.py:111-119, 247-268) */
+  const double *jac;        /* (n)         J = det(dx/dxi)            */
+  const double *tmat;       /* (d*d, n)    T[a][j] at row a*d + j      */
+  const double *alpha_diag; /* (d, n)      alpha[a][a]                 */
+  /* boundary entries (S/mesh.py:348-380) */
+  int64_t m;
+  const int32_t *bcell;  /* (m) adjacent cell                         */
+  const int32_t *bface;  /* (m) face f = 2a + s | kind << 4           */
+  const double *bjac;    /* (m) face J                                */
+  const double *bt;      /* (d, m) face T[a][j], a = face axis        */
+  const double *balpha;  /* (m) face alpha[a][a]                      */
+} pf_plan_desc;
+
+typedef struct pf_plan pf_plan;
+
+/* Outcome of one linear solve (replaces linalg.SolverReport,
+ * S/linalg.py:29-35). */
+typedef struct pf_solver_report {
+  int32_t converged;
+  int32_t iterations;
+  double residual; /* true residual / |b| when converged */
+  int32_t fallback_used;
+  int32_t breakdown; /* 1 if the Krylov recurrence broke down */
+} pf_solver_report;
+
+PF_API const char *pf_last_error(void);
+PF_API int pf_version(void);
+/* number of kernels this library has launched in the process (for the
+ * benchmark's gpu_launches accounting) */
+PF_API unsigned long long pf_launch_count(void);
+
+PF_API int pf_plan_create(const pf_plan_desc *desc, pf_plan **out);
+PF_API int pf_plan_destroy(pf_plan *plan);
+/* bytes of device scratch the solvers and reductions need for this plan */
+PF_API int64_t pf_workspace_bytes(const pf_plan *plan);
+
+/* ---- forward building blocks (S/piso.py) --------------------------------- */
+
+/* U^a = J (T u)_a  -- piso.contravariant_flux, S/piso.py:123-125 */
+PF_API int pf_contravariant_flux(const pf_plan *plan, const double *u, double *flux,
+                          void *stream);
+
+/* C = advection-diffusion stencil -- piso.assemble_momentum,
+ * S/piso.py:293-319.  `flux_scratch` is (d, n). */
+PF_API int pf_assemble_momentum(const pf_plan *plan, const double *u_n, double nu,
+                         double dt, double *flux_scratch, double *c_out,
+                         void *stream);
+
+/* rhs = u_n/dt + S + boundary terms -- piso.momentum_rhs, S/piso.py:356-372
+ * (orthogonal faces; the lagged non-orthogonal flux is zero there).
+ * `source` is (d, n), or a (d) vector when source_is_uniform != 0. */
+PF_API int pf_momentum_rhs(const pf_plan *plan, const double *u_n, const double *bc,
+                    const double *source, int32_t source_is_uniform,
+                    double nu, double dt, double *rhs_out, void *stream);
+
+/* K = -P stencil -- piso.assemble_pressure, S/piso.py:395-412; K's diagonal
+ * is the sum of the face coefficients, its off-diagonals the negated face
+ * means.  `c` is the momentum stencil (its row 0, A, is read) or, when
+ * c_is_a_inv != 0, the (n) vector A^-1 itself. */
+PF_API int pf_assemble_pressure(const pf_plan *plan, const double *c,
+                                int32_t c_is_a_inv, double *k_out,
+                                void *stream);
+
+/* h = A^-1 (rhs - H u) -- corrector h stage, S/piso.py:608-612 */
+PF_API int pf_h_stage(const pf_plan *plan, const double *c, const double *u_cur,
+               const double *rhs, double *h_out, void *stream);
+
+/* b = divergence_rhs(h, bc), S/piso.py:415-428 (flux_scratch (d, n)) */
+PF_API int pf_divergence_rhs(const pf_plan *plan, const double *h, const double *bc,
+                      double *flux_scratch, double *b_out, void *stream);
+
+/* u = h - A^-1 T^t wide_grad(p, mirror) -- piso.correct_velocity,
+ * S/piso.py:452-455 with wide_grad S/piso.py:172-209 */
+PF_API int pf_correct_velocity(const pf_plan *plan, const double *h, const double *p,
+                        const double *c, double *u_out, void *stream);
+
+/* max |divergence_rhs(u, bc) / J| -- StepDiagnostics.div_wide_max,
+ * S/piso.py:458-460, 635-636.  Result written to *out_host. */
+PF_API int pf_divergence_max(const pf_plan *plan, const double *u, const double *bc,
+                      double *flux_scratch, void *workspace, double *out_host,
+                      void *stream);
+
+/* y = A x (transpose != 0: y = A^t x) for a stencil A, ncomp right-hand
+ * sides of length n each -- SystemPattern.matvec, S/linalg.py:80-83 and
+ * _kernels_c.matvec S/_kernels_c.pyx:45-63 */
+PF_API int pf_stencil_matvec(const pf_plan *plan, const double *a, int32_t transpose,
+                      int32_t ncomp, const double *x, double *y, void *stream);
+
+/* ---- solvers (S/linalg.py) ---------------------------------------------- */
+
+/* Zero-mean (optional) Jacobi-preconditioned CG on stencil `a`, with the
+ * reference's semantics: b projected to zero mean, relative tolerance,
+ * true-residual verification <= 10 tol_abs, unpreconditioned retry from zero
+ * with 2*maxiter on failure -- cg_solve / _cg_core / _run_with_fallback,
+ * S/linalg.py:136-170, 215-273.  The right-hand side is b_scale * b.  x holds
+ * the warm start on entry (has_x0 != 0; zero otherwise) and the solution on
+ * exit. */
+PF_API int pf_cg_solve(const pf_plan *plan, const double *a, const double *b,
+                       double b_scale, double *x, int32_t has_x0, double tol,
+                       int32_t maxiter, int32_t zero_mean, int32_t precond,
+                       void *workspace, pf_solver_report *report_host,
+                       void *stream);
+
+/* ncomp independent Jacobi-preconditioned BiCGStab solves sharing matrix `a`
+ * (transpose != 0 solves with A^t) -- bicgstab_solve / _bicgstab_core,
+ * S/linalg.py:173-212, 276-281; the predictor loop S/piso.py:583-590 and the
+ * adjoint momentum solve S/adjoint.py:369-380.  One report per component. */
+PF_API int pf_bicgstab_solve(const pf_plan *plan, const double *a, int32_t transpose,
+                      int32_t ncomp, const double *b, double *x,
+                      int32_t has_x0, double tol, int32_t maxiter,
+                      int32_t precond, void *workspace,
+                      pf_solver_report *reports_host, void *stream);
+
+/* Live timing of the CG iteration kernels on operator `a` (tol = 0, so the
+ * recurrence never stops): ms_host[0..2] = average ms per launch of the
+ * SpMV + p.Ap kernel, the x/r update + reductions kernel and the direction
+ * update kernel over `iters` iterations, timed with CUDA events on
+ * `stream`.  Used by bench.py for the roofline figure. */
+PF_API int pf_cg_profile(const pf_plan *plan, const double *a,
+                         const double *b, int32_t iters, void *workspace,
+                         double *ms_host, void *stream);
+
+/* ---- adjoint stage kernels (S/adjoint.py) --------------------------------- */
+
+/* backward_correct_velocity, S/adjoint.py:78-91: dA += (cu . T^t g)/A^2,
+ * cot_p = wide_grad_adjoint(-A^-1 T cu) (+ extra_cot_p if non-null). */
+PF_API int pf_bwd_correct_velocity(const pf_plan *plan, const double *p,
+                            const double *c, const double *cu, double *da,
+                            double *cot_p, const double *extra_cot_p,
+                            void *workspace, void *stream);
+
+/* dKf[f][i] += y_i (p_nb - p_i): face cotangents of the pressure stencil from
+ * one adjoint pressure solve -- outer_on_pattern(y, p) S/adjoint.py:113
+ * folded with the diagonal as backward_pressure_matrix consumes it. */
+PF_API int pf_bwd_pressure_outer(const pf_plan *plan, const double *y,
+                          const double *p, double *dkf, void *stream);
+
+/* dA += backward_pressure_matrix(a_inv, dP), S/adjoint.py:116-134 */
+PF_API int pf_bwd_pressure_matrix(const pf_plan *plan, const double *c,
+                           const double *dkf, double *da, void *stream);
+
+/* _adj_divergence_rhs, S/adjoint.py:137-153, for the cotangent cot_scale*cot_b:
+ * g_h += J T^t g_flux(cot_b),
+ * dbc += N J_f cot_b T_f[a,:] */
+PF_API int pf_adj_divergence_rhs(const pf_plan *plan, const double *cot_b,
+                                 double cot_scale, double *g_h, double *dbc,
+                                 void *stream);
+
+/* h-stage adjoint, S/adjoint.py:477-487: dA -= A^-1 g_h.h; g_rhs += A^-1 g_h;
+ * dC_off += outer(-A^-1 g_h, u_hin); cu = (C^t - A)(-A^-1 g_h). */
+PF_API int pf_bwd_h_stage(const pf_plan *plan, const double *c, const double *g_h,
+                   const double *h, const double *u_hin, double *da,
+                   double *g_rhs, double *dc, double *cu_out, void *workspace,
+                   void *stream);
+
+/* dC += outer(-y, u_star) on the pattern (diagonal included) -- the matrix
+ * cotangent of the momentum solve, S/adjoint.py:380 */
+PF_API int pf_bwd_momentum_outer(const pf_plan *plan, const double *y,
+                          const double *u_star, double *dc, void *stream);
+
+/* _adj_momentum_rhs, S/adjoint.py:236-268 (orthogonal faces):
+ * du_n += cot/dt, dbc += ..., *dnu_dev += sum(...).  dnu_dev is a device
+ * double accumulated in stream order. */
+PF_API int pf_adj_momentum_rhs(const pf_plan *plan, const double *cot_rhs,
+                        const double *bc, double nu, double dt, double *du_n,
+                        double *dbc, double *dnu_dev, void *workspace,
+                        void *stream);
+
+/* _adj_assemble_momentum, S/adjoint.py:307-340: du_n += J T^t g_flux(dC),
+ * *dnu_dev += viscous part. */
+PF_API int pf_adj_assemble_momentum(const pf_plan *plan, const double *dc,
+                             double nu, double *du_n, double *dnu_dev,
+                             void *workspace, void *stream);
+
+/* ---- boundary preprocessing (S/piso.py:467-509) --------------------------- */
+
+/* advective_outflow_update: relax outflow faces towards the adjacent cells
+ * and rescale for zero net boundary flux.  bc_inout (d, m) is updated in
+ * place; the scale factor is written to *scale_host. */
+PF_API int pf_advective_outflow_update(const pf_plan *plan, const double *u,
+                                double *bc_inout, double dt, void *workspace,
+                                double *scale_host, void *stream);
+
+/* generic deterministic reductions used by the host layer */
+PF_API int pf_reduce_sum(const pf_plan *plan, const double *x, int64_t len,
+                  void *workspace, double *out_host, void *stream);
+PF_API int pf_reduce_dot(const pf_plan *plan, const double *x, const double *y,
+                  int64_t len, void *workspace, double *out_host,
+                  void *stream);
+PF_API int pf_reduce_maxabs(const pf_plan *plan, const double *x, int64_t len,
+                     void *workspace, double *out_host, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PISOB200_H */

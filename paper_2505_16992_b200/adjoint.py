@@ -1,0 +1,286 @@
+"""Discrete adjoint of the PISO step on device (mirror of S/adjoint.py).
+
+``backward_step`` / ``backward_rollout`` keep the reference's signatures,
+gradient-path gating (``GradientPath``), stage labels and ``GradState``
+(S/adjoint.py:28-66, 412-539).  Every stage is a kernel of
+``libpisob200.so``; transposes are gathers over the neighbour relation, so
+the result is bitwise reproducible.
+
+Stage map (orthogonal grids):
+
+=============================  ===========================  ==========================
+reverse of                     reference                    kernel entry
+=============================  ===========================  ==========================
+correct_velocity               S/adjoint.py:78-91           pf_bwd_correct_velocity
+pressure solve (adjoint CG)    S/adjoint.py:94-113          pf_cg_solve + pf_bwd_pressure_outer
+pressure assembly              S/adjoint.py:116-134         pf_bwd_pressure_matrix
+divergence_rhs                 S/adjoint.py:137-153         pf_adj_divergence_rhs
+h stage                        S/adjoint.py:477-487         pf_bwd_h_stage
+momentum solve (adjoint BiCG)  S/adjoint.py:369-380         pf_bicgstab_solve(A^t) + pf_bwd_momentum_outer
+momentum_rhs                   S/adjoint.py:236-268         pf_adj_momentum_rhs
+assemble_momentum              S/adjoint.py:307-340         pf_adj_assemble_momentum
+=============================  ===========================  ==========================
+"""
+
+from dataclasses import dataclass, field
+from enum import Enum
+
+import numpy as np
+import torch
+
+from . import _lib
+from .linalg import bicgstab_solve, cg_solve
+from .piso import F64, bc_views, scalar_field, soa
+
+
+class GradientPath(Enum):
+    FULL = "full"
+    ADV_ONLY = "adv_only"
+    P_ONLY = "p_only"
+    NONE = "none"
+
+    @classmethod
+    def parse(cls, name):
+        for p in cls:
+            if p.value == str(name).strip().lower():
+                return p
+        raise ValueError(f"unknown gradient path {name!r}; choose from "
+                         + ", ".join(p.value for p in cls))
+
+    @property
+    def pressure_solve(self):
+        return self in (GradientPath.FULL, GradientPath.P_ONLY)
+
+    @property
+    def advection_solve(self):
+        return self in (GradientPath.FULL, GradientPath.ADV_ONLY)
+
+
+@dataclass
+class GradState:
+    """Cotangents shaped like the state fields (S/adjoint.py:51-66)."""
+    u: object
+    p: object
+    nu: float = 0.0
+    source: object = None
+    bc: list = None
+    solve_iterations: int = 0
+
+    @classmethod
+    def zeros(cls, domain, device=None):
+        dev = torch.device("cuda", torch.cuda.current_device()) \
+            if device is None else torch.device(device)
+        n, d = domain.n, domain.dim
+        plan = domain.device_plan(dev)
+        bc = torch.zeros((d, plan.m), dtype=F64, device=dev) if plan.m \
+            else None
+        return cls(u=torch.zeros((d, n), dtype=F64, device=dev).t(),
+                   p=torch.zeros(n, dtype=F64, device=dev), nu=0.0,
+                   source=torch.zeros((d, n), dtype=F64, device=dev).t(),
+                   bc=bc_views(plan, bc))
+
+
+def backward_step(domain, tape, cot, path=GradientPath.FULL, tol=None,
+                  maxiter=None):
+    """Chain the backward kernels through one recorded step
+    (S/adjoint.py:412-506)."""
+    if tape is None or tape.u_n is None:
+        raise ValueError("backward_step needs a recorded tape")
+    if isinstance(path, str):
+        path = GradientPath.parse(path)
+    dev = tape.c_data.device
+    plan = domain.device_plan(dev)
+    n, d = domain.n, domain.dim
+    hs = plan.stream
+    C, K = tape.c_data, tape.k_data
+    n_corr = len(tape.correctors)
+    reports = []
+
+    dC = torch.zeros((2 * d + 1, n), dtype=F64, device=dev)
+    dA = dC[0]                       # dC[diag] += dA (S/adjoint.py:492)
+    dKf = torch.zeros((2 * d, n), dtype=F64, device=dev)
+    g_rhs = torch.zeros((d, n), dtype=F64, device=dev)
+    dbc = torch.zeros((d, plan.m), dtype=F64, device=dev) if plan.m else None
+    dnu = torch.zeros(1, dtype=F64, device=dev)
+
+    cu = soa(cot.u, n, d, dev).clone()
+    cp_out = None if cot.p is None else scalar_field(cot.p, n, dev)
+    cot_p = torch.empty(n, dtype=F64, device=dev)
+    cu_next = torch.empty((d, n), dtype=F64, device=dev)
+    pressure_done = False
+
+    for m in reversed(range(n_corr)):
+        corr = tape.correctors[m]
+        p_m = corr.p_iters[-1]
+        _lib.call("pf_bwd_correct_velocity", plan.handle, _lib.ptr(p_m),
+                  _lib.ptr(C), _lib.ptr(cu), _lib.ptr(dA), _lib.ptr(cot_p),
+                  _lib.ptr(cp_out if m == n_corr - 1 else None),
+                  _lib.ptr(plan.workspace), hs)
+        g_h = cu                     # dh = cu; the divergence adjoint adds
+        # only the last outer iterate carries a cotangent on orthogonal grids
+        # (the lagged-cross adjoint that would feed earlier ones is zero)
+        it = len(corr.p_iters) - 1
+        if path.pressure_solve:
+            y, rep = cg_solve(plan, K, cot_p, tol=tol, maxiter=maxiter,
+                              zero_mean=True, stage="adjoint_pressure")
+            reports.append(rep)
+            _lib.call("pf_bwd_pressure_outer", plan.handle, _lib.ptr(y),
+                      _lib.ptr(corr.p_iters[it]), _lib.ptr(dKf), hs)
+            pressure_done = True
+            # forward solved (-P) p = proj(-b): db = -y
+            _lib.call("pf_adj_divergence_rhs", plan.handle, _lib.ptr(y),
+                      -1.0, _lib.ptr(g_h), _lib.ptr(dbc), hs)
+        _lib.call("pf_bwd_h_stage", plan.handle, _lib.ptr(C), _lib.ptr(g_h),
+                  _lib.ptr(soa(corr.h, n, d, dev)),
+                  _lib.ptr(soa(corr.u_hin, n, d, dev)), _lib.ptr(dA),
+                  _lib.ptr(g_rhs), _lib.ptr(dC), _lib.ptr(cu_next),
+                  _lib.ptr(plan.workspace), hs)
+        cu, cu_next = cu_next, cu
+
+    if pressure_done:
+        _lib.call("pf_bwd_pressure_matrix", plan.handle, _lib.ptr(C),
+                  _lib.ptr(dKf), _lib.ptr(dA), hs)
+
+    # predictor (S/adjoint.py:343-405); only the last outer iterate is fed
+    grhs = g_rhs
+    if path.advection_solve:
+        y, reps = bicgstab_solve(plan, C, cu, tol=tol, maxiter=maxiter,
+                                 transpose=True,
+                                 stages=[f"adjoint_momentum[{c}]"
+                                         for c in range(d)])
+        reports.extend(reps)
+        u_star = soa(tape.mom_iters[-1], n, d, dev)
+        _lib.call("pf_bwd_momentum_outer", plan.handle, _lib.ptr(y),
+                  _lib.ptr(u_star), _lib.ptr(dC), hs)
+        grhs = y.add_(g_rhs)
+    du_n = torch.zeros((d, n), dtype=F64, device=dev)
+    bcd = getattr(tape, "_bc_dm", None)
+    if bcd is None and plan.m:
+        from .piso import bc_soa
+        bcd = bc_soa(plan, tape.bc, d)
+    _lib.call("pf_adj_momentum_rhs", plan.handle, _lib.ptr(grhs),
+              _lib.ptr(bcd), float(tape.nu), float(tape.dt), _lib.ptr(du_n),
+              _lib.ptr(dbc), _lib.ptr(dnu), _lib.ptr(plan.workspace), hs)
+    _lib.call("pf_adj_assemble_momentum", plan.handle, _lib.ptr(dC),
+              float(tape.nu), _lib.ptr(du_n), _lib.ptr(dnu),
+              _lib.ptr(plan.workspace), hs)
+    iters = sum(r.iterations for r in reports)
+    return GradState(u=du_n.t(), p=torch.zeros(n, dtype=F64, device=dev),
+                     nu=float(dnu.item()), source=grhs.t(),
+                     bc=bc_views(plan, dbc), solve_iterations=iters)
+
+
+def backward_rollout(domain, tapes, cots, path=GradientPath.FULL, tol=None,
+                     maxiter=None):
+    """Reverse chain over recorded steps (S/adjoint.py:509-539): u is the
+    cotangent of the initial velocity; nu, source and bc accumulate."""
+    if len(tapes) != len(cots):
+        raise ValueError("need one cotangent slot per recorded step")
+    n, d = domain.n, domain.dim
+    dev = tapes[-1].c_data.device if tapes else None
+    total = GradState.zeros(domain, dev)
+    src = total.source.t()           # (d, n) storage
+    bc_total = [b for b in total.bc]
+    cu = torch.zeros((d, n), dtype=F64, device=dev)
+    for k in reversed(range(len(tapes))):
+        ck = cots[k]
+        if ck is not None:
+            cu = cu + soa(ck.u, n, d, dev)
+            cp = ck.p
+        else:
+            cp = None
+        g = backward_step(domain, tapes[k], GradState(u=cu.t(), p=cp),
+                          path=path, tol=tol, maxiter=maxiter)
+        total.nu += g.nu
+        src += g.source.t()
+        for i in range(len(bc_total)):
+            bc_total[i] += g.bc[i]
+        total.solve_iterations += g.solve_iterations
+        cu = soa(g.u, n, d, dev)
+    total.u = cu.t()
+    return total
+
+
+# ---------------------------------------------------------------------------
+# finite-difference verification harness (S/adjoint.py:546-624)
+
+
+@dataclass
+class GradcheckEntry:
+    stage: str
+    name: str
+    max_rel_err: float
+    passed: bool
+
+
+@dataclass
+class GradcheckReport:
+    entries: list = field(default_factory=list)
+    threshold: float = 1e-4
+
+    @property
+    def passed(self):
+        return all(e.passed for e in self.entries)
+
+    @property
+    def max_rel_err(self):
+        return max((e.max_rel_err for e in self.entries), default=0.0)
+
+    def text(self):
+        return "\n".join(
+            f"stage={e.stage} input={e.name} max_rel_err={e.max_rel_err:.3e} "
+            f"pass={1 if e.passed else 0}" for e in self.entries)
+
+
+def _to_np(x):
+    if torch.is_tensor(x):
+        return x.detach().cpu().numpy()
+    return np.asarray(x, dtype=np.float64)
+
+
+def gradcheck(fn, inputs, eps=None, mode="central", threshold=1e-4,
+              stage="map"):
+    """Central (or forward) finite differences against the analytic
+    gradient; relative error floored at 10% of the largest magnitude per
+    input (the reference's acceptance metric)."""
+    names = list(inputs)
+    is_scalar = {k: np.ndim(_to_np(inputs[k])) == 0 for k in names}
+    work = {k: np.array(np.atleast_1d(_to_np(inputs[k])), dtype=np.float64)
+            for k in names}
+
+    def evaluate():
+        args = {k: (float(work[k][0]) if is_scalar[k] else work[k].copy())
+                for k in names}
+        return float(fn(args)[0])
+
+    loss0, grads = fn(inputs)
+    rep = GradcheckReport(threshold=threshold)
+    base_eps = float(np.cbrt(np.finfo(np.float64).eps))
+    for k in names:
+        g_an = np.atleast_1d(_to_np(grads[k])).astype(np.float64)
+        flat = work[k].reshape(-1)
+        g_fd = np.zeros(flat.size)
+        for j in range(flat.size):
+            h = eps if eps is not None else base_eps * max(1.0, abs(flat[j]))
+            keep = flat[j]
+            flat[j] = keep + h
+            up = evaluate()
+            if mode == "central":
+                flat[j] = keep - h
+                g_fd[j] = (up - evaluate()) / (2.0 * h)
+            else:
+                g_fd[j] = (up - loss0) / h
+            flat[j] = keep
+        g_fd = g_fd.reshape(g_an.shape)
+        if not (np.isfinite(g_an).all() and np.isfinite(g_fd).all()):
+            rep.entries.append(GradcheckEntry(stage, k, float("inf"), False))
+            continue
+        scale = max(np.abs(g_an).max(), np.abs(g_fd).max(), 1e-12)
+        err = np.abs(g_an - g_fd) / np.maximum(np.abs(g_fd), 0.1 * scale)
+        worst = float(err.max()) if err.size else 0.0
+        rep.entries.append(GradcheckEntry(stage, k, worst, worst <= threshold))
+    return rep
+
+
+__all__ = ["GradientPath", "GradState", "backward_step", "backward_rollout",
+           "GradcheckEntry", "GradcheckReport", "gradcheck"]

@@ -1,0 +1,374 @@
+// common.cuh -- plan view, mesh topologies, deterministic reductions.
+//
+// Everything here is device-side plumbing shared by the forward, solver and
+// adjoint translation units.  The cell-adjacency semantics follow the
+// reference mesh (S/mesh.py:294-321): for cell i and face f = 2a + s the
+// neighbour is nbr[a, s, i] (or a boundary face), the neighbour's axis seen
+// across the face is nbr_ax[a, s, i, a] and its orientation nbr_sign.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cfloat>
+#include <cmath>
+#include <string>
+
+#include "../../include/pisob200.h"
+
+namespace pf {
+
+constexpr int kBlock = 256;      // threads per CTA for streaming kernels
+constexpr int kMaxRedBlocks = 1184;  // 148 SMs x 8 resident CTAs
+constexpr int kMaxK = 8;         // values per fused reduction
+
+void set_error(const std::string &msg);
+int cuda_check(cudaError_t e, const char *what);
+#define PF_CUDA(call)                                          \
+  do {                                                         \
+    int _rc = ::pf::cuda_check((call), #call);                 \
+    if (_rc) return _rc;                                       \
+  } while (0)
+#define PF_LAUNCH_CHECK(what) PF_CUDA(cudaGetLastError())
+
+// Every kernel launch of the library goes through launch(), which counts it
+// (pf_launch_count) -- the bench reports how many of OUR kernels ran.
+extern unsigned long long g_launches;
+template <typename... KArgs, typename... Args>
+inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block,
+                   cudaStream_t stream, Args... args) {
+  ++g_launches;
+  kernel<<<grid, block, 0, stream>>>(args...);
+}
+
+// Host-side plan: the immutable device description plus derived launch
+// parameters.
+struct Plan {
+  pf_plan_desc d;
+  int num_sms;
+  int red_blocks;  // grid of reduction kernels
+};
+
+// ---------------------------------------------------------------------------
+// face lookup
+
+struct Face {
+  int32_t nb;    // neighbour cell, -1 for a boundary face
+  int32_t ax;    // neighbour's axis for my face axis (perm[a])
+  int32_t neg;   // orientation flip of that axis (sign == -1)
+  int32_t bidx;  // boundary entry when nb < 0
+};
+
+// back face of the neighbour pointing at me: axis perm[a], side flipped
+// unless the orientation is reversed (S/mesh.py:393-397)
+__device__ __forceinline__ int back_face(const Face &fc, int s) {
+  const int rs = fc.neg ? s : 1 - s;
+  return 2 * fc.ax + rs;
+}
+
+struct GatherTopo {
+  const int32_t *nbr;
+  int64_t n;
+  struct Cell {
+    int32_t i;
+  };
+  __device__ __forceinline__ Cell cell(int32_t i) const { return Cell{i}; }
+  __device__ __forceinline__ Face face(const Cell &c, int f) const {
+    const int32_t v = __ldg(nbr + (int64_t)f * n + c.i);
+    Face r;
+    if (v >= 0) {
+      r.nb = v & 0x03FFFFFF;
+      r.ax = (v >> 26) & 3;
+      r.neg = (v >> 28) & 1;
+      r.bidx = -1;
+    } else {
+      r.nb = -1;
+      r.ax = f >> 1;
+      r.neg = 0;
+      r.bidx = ~v;
+    }
+    return r;
+  }
+};
+
+template <int D>
+struct BoxTopo {
+  int32_t shape[3];
+  int32_t stride[3];
+  int32_t periodic[3];
+  int32_t face_off[6];
+  struct Cell {
+    int32_t i;
+    int32_t x[3];
+  };
+  __device__ __forceinline__ Cell cell(int32_t i) const {
+    Cell c;
+    c.i = i;
+    int32_t rem = i;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      c.x[a] = rem / stride[a];
+      rem -= c.x[a] * stride[a];
+    }
+    return c;
+  }
+  __device__ __forceinline__ Face face(const Cell &c, int f) const {
+    const int a = f >> 1, s = f & 1;
+    Face r;
+    r.ax = a;
+    r.neg = 0;
+    r.bidx = -1;
+    const int xa = c.x[a];
+    if (s) {
+      if (xa + 1 < shape[a]) {
+        r.nb = c.i + stride[a];
+      } else if (periodic[a]) {
+        r.nb = c.i - (shape[a] - 1) * stride[a];
+      } else {
+        r.nb = -1;
+      }
+    } else {
+      if (xa > 0) {
+        r.nb = c.i - stride[a];
+      } else if (periodic[a]) {
+        r.nb = c.i + (shape[a] - 1) * stride[a];
+      } else {
+        r.nb = -1;
+      }
+    }
+    if (r.nb < 0) {
+      // boundary entries are the face's cells in C order of the other axes
+      int32_t idx = 0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        if (k == a) continue;
+        idx = idx * shape[k] + c.x[k];
+      }
+      r.bidx = face_off[f] + idx;
+    }
+    return r;
+  }
+};
+
+// Device view of the plan (passed by value into kernels).
+template <int D, class Topo>
+struct View {
+  static constexpr int kDim = D;
+  using Cell = typename Topo::Cell;
+  Topo topo;
+  int32_t n;
+  int32_t m;
+  const double *__restrict__ jac;
+  const double *__restrict__ tmat;   // (D*D, n)
+  const double *__restrict__ alpha;  // (D, n)
+  const int32_t *__restrict__ bcell;
+  const int32_t *__restrict__ bface;
+  const double *__restrict__ bjac;
+  const double *__restrict__ bt;  // (D, m)
+  const double *__restrict__ balpha;
+
+  __device__ __forceinline__ double T(int a, int j, int32_t i) const {
+    return __ldg(tmat + (int64_t)(a * D + j) * n + i);
+  }
+  __device__ __forceinline__ double A(int a, int32_t i) const {
+    return __ldg(alpha + (int64_t)a * n + i);
+  }
+  __device__ __forceinline__ double J(int32_t i) const {
+    return __ldg(jac + i);
+  }
+  // contravariant flux component a of a (D, n) SoA velocity at cell i
+  __device__ __forceinline__ double flux(const double *__restrict__ u, int a,
+                                         int32_t i) const {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) acc += T(a, j, i) * u[(int64_t)j * n + i];
+    return J(i) * acc;
+  }
+  // boundary face flux U_f = J_f T_f[a,:] . ub  (S/piso.py:128-131)
+  __device__ __forceinline__ double bflux(const double *__restrict__ bc,
+                                          int32_t e) const {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+      acc += __ldg(bt + (int64_t)j * m + e) * bc[(int64_t)j * m + e];
+    return __ldg(bjac + e) * acc;
+  }
+};
+
+template <int D, class Topo>
+View<D, Topo> make_view(const Plan &p, const Topo &topo) {
+  View<D, Topo> v;
+  v.topo = topo;
+  v.n = (int32_t)p.d.n;
+  v.m = (int32_t)p.d.m;
+  v.jac = p.d.jac;
+  v.tmat = p.d.tmat;
+  v.alpha = p.d.alpha_diag;
+  v.bcell = p.d.bcell;
+  v.bface = p.d.bface;
+  v.bjac = p.d.bjac;
+  v.bt = p.d.bt;
+  v.balpha = p.d.balpha;
+  return v;
+}
+
+template <int D>
+BoxTopo<D> make_box(const Plan &p) {
+  BoxTopo<D> t;
+  int32_t st = 1;
+  for (int a = D - 1; a >= 0; --a) {
+    t.shape[a] = (int32_t)p.d.box_shape[a];
+    t.stride[a] = st;
+    st *= t.shape[a];
+    t.periodic[a] = p.d.box_periodic[a];
+  }
+  for (int a = D; a < 3; ++a) {
+    t.shape[a] = 1;
+    t.stride[a] = 1;
+    t.periodic[a] = 0;
+  }
+  for (int f = 0; f < 6; ++f) t.face_off[f] = (int32_t)p.d.box_face_offset[f];
+  return t;
+}
+
+// Calls fn(View<D, Topo>) with the plan's dimension and topology resolved at
+// compile time.
+template <class Fn>
+int dispatch(const Plan &p, Fn &&fn) {
+  if (p.d.topo == PF_TOPO_BOX) {
+    if (p.d.dim == 2) return fn(make_view<2>(p, make_box<2>(p)));
+    if (p.d.dim == 3) return fn(make_view<3>(p, make_box<3>(p)));
+  } else {
+    GatherTopo g{p.d.nbr, p.d.n};
+    if (p.d.dim == 2) return fn(make_view<2>(p, g));
+    if (p.d.dim == 3) return fn(make_view<3>(p, g));
+  }
+  set_error("unsupported plan dimension/topology");
+  return PF_ERR_ARG;
+}
+
+inline int grid_for(int64_t work, int block = kBlock) {
+  int64_t g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// ---------------------------------------------------------------------------
+// deterministic reductions: warp shuffle tree -> per-warp smem -> per-block
+// partials -> the last block to finish (ticket counter) folds the partials in
+// fixed order and runs a finaliser.  No floating-point atomics anywhere.
+
+template <int K>
+__device__ __forceinline__ void warp_sum(double (&v)[K]) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      v[k] += __shfl_down_sync(0xffffffffu, v[k], off);
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void warp_max(double (&v)[K]) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      v[k] = fmax(v[k], __shfl_down_sync(0xffffffffu, v[k], off));
+  }
+}
+
+// Block-wide reduction; the result is valid in thread 0.
+template <int K, bool kMax = false>
+__device__ __forceinline__ void block_reduce(double (&v)[K]) {
+  __shared__ double sm[kBlock / 32][K];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (kMax) warp_max<K>(v); else warp_sum<K>(v);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) sm[w][k] = v[k];
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      v[k] = lane < nw ? sm[lane][k] : (kMax ? -DBL_MAX : 0.0);
+    if (kMax) warp_max<K>(v); else warp_sum<K>(v);
+  }
+  __syncthreads();
+}
+
+// Reduce K values over the whole grid; thread 0 of the last block gets the
+// totals in `tot` and returns true.  partials: gridDim.x * K doubles,
+// counter: one zero-initialised unsigned (reset here for the next use).
+template <int K, bool kMax = false>
+__device__ __forceinline__ bool grid_reduce(double (&v)[K], double *partials,
+                                            unsigned *counter,
+                                            double (&tot)[K]) {
+  __shared__ bool is_last;
+  block_reduce<K, kMax>(v);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) partials[(int64_t)blockIdx.x * K + k] = v[k];
+    __threadfence();
+    const unsigned t = atomicAdd(counter, 1u);
+    is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return false;
+  __threadfence();
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = kMax ? -DBL_MAX : 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const double x = __ldcg(partials + (int64_t)b * K + k);
+      acc[k] = kMax ? fmax(acc[k], x) : acc[k] + x;
+    }
+  }
+  block_reduce<K, kMax>(acc);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) tot[k] = acc[k];
+    *counter = 0u;
+    return true;
+  }
+  return false;
+}
+
+// Workspace layout shared by all entry points (bytes, 256-aligned):
+//   [0, 4096)                 : counters (unsigned) + small scalar block
+//   partials                  : kMaxRedBlocks * kMaxK doubles
+//   solver scalars            : 4096 doubles
+//   solver vectors            : nvec * (3 * n) doubles
+struct Workspace {
+  unsigned *counters;   // 64 counters
+  double *scalars;      // 448 doubles of small scratch (host-visible copies)
+  double *partials;     // kMaxRedBlocks * kMaxK
+  double *solver;       // 4096 doubles for solver state
+  double *vecs;         // vector scratch
+  int64_t vec_len;      // doubles available in vecs
+};
+constexpr int64_t kWsHeader = 4096;
+constexpr int64_t kWsSolver = 4096;
+constexpr int kWsVectors = 12;  // vectors of length d*n the solvers may use
+
+inline Workspace carve(void *base, int64_t n, int dim) {
+  char *b = static_cast<char *>(base);
+  Workspace w;
+  w.counters = reinterpret_cast<unsigned *>(b);
+  w.scalars = reinterpret_cast<double *>(b + 512);
+  w.partials = reinterpret_cast<double *>(b + kWsHeader);
+  w.solver = w.partials + (int64_t)kMaxRedBlocks * kMaxK;
+  w.vecs = w.solver + kWsSolver;
+  w.vec_len = (int64_t)kWsVectors * dim * n;
+  return w;
+}
+inline int64_t workspace_bytes(int64_t n, int dim) {
+  return kWsHeader + 8 * ((int64_t)kMaxRedBlocks * kMaxK + kWsSolver +
+                          (int64_t)kWsVectors * dim * n);
+}
+
+}  // namespace pf

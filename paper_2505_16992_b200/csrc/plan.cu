@@ -1,0 +1,97 @@
+// plan.cu -- plan lifetime, error reporting, workspace sizing.
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace pf {
+
+static thread_local std::string g_last_error;
+unsigned long long g_launches = 0;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+int cuda_check(cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return PF_OK;
+  char buf[512];
+  snprintf(buf, sizeof(buf), "CUDA error %d (%s) in %s", (int)e,
+           cudaGetErrorString(e), what);
+  set_error(buf);
+  return PF_ERR_CUDA;
+}
+
+}  // namespace pf
+
+using namespace pf;
+
+extern "C" const char *pf_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int pf_version(void) { return 1; }
+
+extern "C" unsigned long long pf_launch_count(void) { return g_launches; }
+
+extern "C" int pf_plan_create(const pf_plan_desc *desc, pf_plan **out) {
+  if (!desc || !out) {
+    set_error("pf_plan_create: null argument");
+    return PF_ERR_ARG;
+  }
+  const pf_plan_desc &d = *desc;
+  if (d.dim != 2 && d.dim != 3) {
+    set_error("pf_plan_create: dim must be 2 or 3");
+    return PF_ERR_ARG;
+  }
+  if (d.n <= 0 || d.n >= (1LL << 26)) {
+    set_error("pf_plan_create: cell count out of range (1 .. 2^26-1)");
+    return PF_ERR_ARG;
+  }
+  if (!d.jac || !d.tmat || !d.alpha_diag) {
+    set_error("pf_plan_create: missing metrics");
+    return PF_ERR_ARG;
+  }
+  if (d.m > 0 && (!d.bcell || !d.bface || !d.bjac || !d.bt || !d.balpha)) {
+    set_error("pf_plan_create: missing boundary arrays");
+    return PF_ERR_ARG;
+  }
+  if (d.topo == PF_TOPO_GATHER) {
+    if (!d.nbr) {
+      set_error("pf_plan_create: gather topology needs a neighbour table");
+      return PF_ERR_ARG;
+    }
+  } else if (d.topo == PF_TOPO_BOX) {
+    int64_t cnt = 1;
+    for (int a = 0; a < d.dim; ++a) {
+      if (d.box_shape[a] < 1) {
+        set_error("pf_plan_create: bad box shape");
+        return PF_ERR_ARG;
+      }
+      cnt *= d.box_shape[a];
+    }
+    if (cnt != d.n) {
+      set_error("pf_plan_create: box shape does not match n");
+      return PF_ERR_ARG;
+    }
+  } else {
+    set_error("pf_plan_create: unknown topology");
+    return PF_ERR_ARG;
+  }
+  int dev = 0, sms = 148;
+  PF_CUDA(cudaGetDevice(&dev));
+  PF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  Plan *p = new Plan;
+  p->d = d;
+  p->num_sms = sms;
+  p->red_blocks = sms * 8 < kMaxRedBlocks ? sms * 8 : kMaxRedBlocks;
+  *out = reinterpret_cast<pf_plan *>(p);
+  return PF_OK;
+}
+
+extern "C" int pf_plan_destroy(pf_plan *plan) {
+  delete reinterpret_cast<Plan *>(plan);
+  return PF_OK;
+}
+
+extern "C" int64_t pf_workspace_bytes(const pf_plan *plan) {
+  if (!plan) return -1;
+  const Plan &p = *reinterpret_cast<const Plan *>(plan);
+  return workspace_bytes(p.d.n, p.d.dim);
+}

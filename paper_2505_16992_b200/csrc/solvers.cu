@@ -1,0 +1,980 @@
+// solvers.cu -- device-resident Krylov solvers with the reference semantics.
+//
+// CG with zero-mean projection (S/linalg.py:136-170) and BiCGStab
+// (S/linalg.py:173-212) behind the verification/fallback wrapper
+// (S/linalg.py:215-255).  The preconditioner is Jacobi (ILU(0), the
+// reference's choice, is a sequential triangular solve with ~2(nx+ny+nz)
+// dependent wavefronts and no place on a 148-SM GPU, SURVEY.md §7 hard part
+// 1); results agree with the reference to solver tolerance, iteration counts
+// differ and are reported.
+//
+// Every iteration is a short chain of fused streaming kernels; each fused
+// reduction finishes in the last CTA to arrive, which also evaluates the
+// recurrence scalars (alpha, beta, omega, convergence) into a device-side
+// state block.  The host only polls that block every few iterations, so the
+// GPU never waits on a host round trip per iteration.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace pf {
+
+struct CompState {
+  double bnorm, tol_abs, res, rho, rho_new, alpha, omega, beta;
+  double zbar, rz, xmean, true_res, bmean, rmean, tol, pad1;
+  int32_t iter, maxiter, done, converged, fail, zero_rhs, pending, active;
+  int32_t project_x, pad2[7];
+};
+
+struct SolverState {
+  CompState c[3];
+  int32_t all_done, ncomp, precond, zero_mean;
+  int32_t pad[12];
+};
+
+static_assert(sizeof(SolverState) <= 8 * kWsSolver, "solver state too big");
+
+__device__ __forceinline__ bool finite(double x) { return isfinite(x); }
+
+// ---------------------------------------------------------------------------
+// stencil application  y_i = sum_j A_ij x_j  (transposed: A_ji)
+
+template <class V, bool kTrans>
+__device__ __forceinline__ double apply_row(const V &v, int32_t i,
+                                            const Face (&fc)[2 * V::kDim],
+                                            const double *__restrict__ a,
+                                            const double *__restrict__ x) {
+  constexpr int D = V::kDim;
+  const int64_t n = v.n;
+  double acc = a[i] * x[i];
+#pragma unroll
+  for (int f = 0; f < 2 * D; ++f) {
+    if (fc[f].nb < 0) continue;
+    const double coef =
+        kTrans ? a[(int64_t)(1 + back_face(fc[f], f & 1)) * n + fc[f].nb]
+               : a[(int64_t)(1 + f) * n + i];
+    acc += coef * x[fc[f].nb];
+  }
+  return acc;
+}
+
+template <class V>
+__device__ __forceinline__ void load_faces(const V &v, int32_t i,
+                                           Face (&fc)[2 * V::kDim]) {
+  const auto cell = v.topo.cell(i);
+#pragma unroll
+  for (int f = 0; f < 2 * V::kDim; ++f) fc[f] = v.topo.face(cell, f);
+}
+
+__device__ __forceinline__ double prec(int precond, const double *__restrict__ a,
+                                       int32_t i, double r) {
+  return precond ? r / a[i] : r;
+}
+
+#define GRID_LOOP(i, n)                                                  \
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (n);       \
+       i += gridDim.x * blockDim.x)
+
+// ===========================================================================
+// CG
+
+__global__ void k_cg_reset(SolverState *st, int maxiter, int precond,
+                           int zero_mean, double tol, int fresh) {
+  CompState &c = st->c[0];
+  if (fresh) {
+    c.bnorm = 0.0;
+    c.bmean = 0.0;
+    c.zero_rhs = 0;
+  }
+  c.tol = tol;
+  c.iter = 0;
+  c.maxiter = maxiter;
+  c.done = c.zero_rhs;
+  c.converged = c.zero_rhs;
+  c.fail = 0;
+  c.project_x = 0;
+  c.res = 0.0;
+  c.true_res = 0.0;
+  c.active = 1;
+  st->all_done = c.done;
+  st->ncomp = 1;
+  st->precond = precond;
+  st->zero_mean = zero_mean;
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_cg_bsum(const double *__restrict__ b, double bs, int32_t n,
+              SolverState *st, double *partials, unsigned *counter) {
+  double acc[1] = {0.0};
+  GRID_LOOP(i, n) acc[0] += bs * b[i];
+  double tot[1];
+  if (grid_reduce<1>(acc, partials, counter, tot))
+    st->c[0].bmean = st->zero_mean ? tot[0] / n : 0.0;
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_cg_bproj(const double *__restrict__ b, double bs,
+               double *__restrict__ bp, int32_t n, SolverState *st,
+               double *partials, unsigned *counter) {
+  const double mean = st->c[0].bmean;
+  double acc[1] = {0.0};
+  GRID_LOOP(i, n) {
+    const double x = bs * b[i] - mean;
+    bp[i] = x;
+    acc[0] += x * x;
+  }
+  double tot[1];
+  if (grid_reduce<1>(acc, partials, counter, tot)) {
+    CompState &c = st->c[0];
+    c.bnorm = sqrt(tot[0]);
+    c.tol_abs = c.tol * c.bnorm;
+    if (c.bnorm == 0.0) {
+      c.zero_rhs = 1;
+      c.done = 1;
+      c.converged = 1;
+      st->all_done = 1;
+    }
+  }
+}
+
+// r = bp - A x, accumulate sum r
+template <class V>
+__global__ void __launch_bounds__(kBlock)
+    k_cg_resid(V v, const double *__restrict__ a, const double *__restrict__ bp,
+               const double *__restrict__ x, double *__restrict__ r,
+               SolverState *st, double *partials, unsigned *counter) {
+  if (st->all_done) return;
+  double acc[1] = {0.0};
+  GRID_LOOP(i, v.n) {
+    Face fc[2 * V::kDim];
+    load_faces(v, i, fc);
+    const double ri = bp[i] - apply_row<V, false>(v, i, fc, a, x);
+    r[i] = ri;
+    acc[0] += ri;
+  }
+  double tot[1];
+  if (grid_reduce<1>(acc, partials, counter, tot))
+    st->c[0].rmean = st->zero_mean ? tot[0] / v.n : 0.0;
+}
+
+// r -= mean(r); z = M r; sums for |r|, z-bar and r.z
+__global__ void __launch_bounds__(kBlock)
+    k_cg_rproj(const double *__restrict__ a, double *__restrict__ r, int32_t n,
+               SolverState *st, double *partials, unsigned *counter) {
+  if (st->all_done) return;
+  const double rmean = st->c[0].rmean;
+  const int pc = st->precond;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  GRID_LOOP(i, n) {
+    const double ri = r[i] - rmean;
+    r[i] = ri;
+    const double zi = prec(pc, a, i, ri);
+    acc[0] += ri * ri;
+    acc[1] += zi;
+    acc[2] += ri * zi;
+    acc[3] += ri;
+  }
+  double tot[4];
+  if (grid_reduce<4>(acc, partials, counter, tot)) {
+    CompState &c = st->c[0];
+    c.res = sqrt(tot[0]);
+    if (c.res <= c.tol_abs) {
+      c.converged = 1;
+      c.done = 1;
+      st->all_done = 1;
+      return;
+    }
+    c.zbar = st->zero_mean ? tot[1] / n : 0.0;
+    c.rz = tot[2] - c.zbar * tot[3];
+  }
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_cg_pinit(const double *__restrict__ a, const double *__restrict__ r,
+               double *__restrict__ p, int32_t n, const SolverState *st) {
+  if (st->all_done) return;
+  const double zbar = st->c[0].zbar;
+  const int pc = st->precond;
+  GRID_LOOP(i, n) p[i] = prec(pc, a, i, r[i]) - zbar;
+}
+
+// q = A p; p.q -> alpha
+template <class V>
+__global__ void __launch_bounds__(kBlock)
+    k_cg_spmv(V v, const double *__restrict__ a, const double *__restrict__ p,
+              double *__restrict__ q, SolverState *st, double *partials,
+              unsigned *counter) {
+  if (st->all_done) return;
+  double acc[1] = {0.0};
+  GRID_LOOP(i, v.n) {
+    Face fc[2 * V::kDim];
+    load_faces(v, i, fc);
+    const double qi = apply_row<V, false>(v, i, fc, a, p);
+    q[i] = qi;
+    acc[0] += p[i] * qi;
+  }
+  double tot[1];
+  if (grid_reduce<1>(acc, partials, counter, tot)) {
+    CompState &c = st->c[0];
+    c.iter += 1;
+    const double pap = tot[0];
+    if (!finite(pap) || fabs(pap) < DBL_MIN) {
+      c.fail = 1;
+      c.done = 1;
+      st->all_done = 1;
+      return;
+    }
+    c.alpha = c.rz / pap;
+  }
+}
+
+// x += alpha p; r -= alpha q; z = M r; convergence and beta
+__global__ void __launch_bounds__(kBlock)
+    k_cg_update(const double *__restrict__ a, const double *__restrict__ p,
+                const double *__restrict__ q, double *__restrict__ x,
+                double *__restrict__ r, int32_t n, SolverState *st,
+                double *partials, unsigned *counter) {
+  if (st->all_done) return;
+  const double alpha = st->c[0].alpha;
+  const int pc = st->precond;
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  GRID_LOOP(i, n) {
+    const double xi = x[i] + alpha * p[i];
+    const double ri = r[i] - alpha * q[i];
+    x[i] = xi;
+    r[i] = ri;
+    const double zi = prec(pc, a, i, ri);
+    acc[0] += ri * ri;
+    acc[1] += zi;
+    acc[2] += ri * zi;
+    acc[3] += ri;
+    acc[4] += xi;
+  }
+  double tot[5];
+  if (grid_reduce<5>(acc, partials, counter, tot)) {
+    CompState &c = st->c[0];
+    c.res = sqrt(tot[0]);
+    if (c.res <= c.tol_abs) {
+      c.converged = 1;
+      c.done = 1;
+      c.project_x = st->zero_mean;
+      c.xmean = st->zero_mean ? tot[4] / n : 0.0;
+      st->all_done = 1;
+      return;
+    }
+    c.zbar = st->zero_mean ? tot[1] / n : 0.0;
+    const double rz_new = tot[2] - c.zbar * tot[3];
+    if (!finite(rz_new) || c.rz == 0.0) {
+      c.fail = 1;
+      c.done = 1;
+      st->all_done = 1;
+      return;
+    }
+    c.beta = rz_new / c.rz;
+    c.rz = rz_new;
+    if (c.iter >= c.maxiter) {
+      c.done = 1;
+      st->all_done = 1;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_cg_pupdate(const double *__restrict__ a, const double *__restrict__ r,
+                 double *__restrict__ p, int32_t n, const SolverState *st) {
+  if (st->all_done) return;
+  const double beta = st->c[0].beta, zbar = st->c[0].zbar;
+  const int pc = st->precond;
+  GRID_LOOP(i, n) p[i] = beta * p[i] + (prec(pc, a, i, r[i]) - zbar);
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_cg_finish(double *__restrict__ x, int32_t n, const SolverState *st) {
+  const CompState &c = st->c[0];
+  if (c.zero_rhs) {
+    GRID_LOOP(i, n) x[i] = 0.0;
+  } else if (c.project_x) {
+    const double m = c.xmean;
+    GRID_LOOP(i, n) x[i] -= m;
+  }
+}
+
+// |bp - A x|
+template <class V>
+__global__ void __launch_bounds__(kBlock)
+    k_true_res(V v, const double *__restrict__ a, int trans, int ncomp,
+               const double *__restrict__ b, const double *__restrict__ x,
+               SolverState *st, double *partials, unsigned *counter) {
+  double acc[3] = {0.0, 0.0, 0.0};
+  const int64_t n = v.n;
+  GRID_LOOP(i, v.n) {
+    Face fc[2 * V::kDim];
+    load_faces(v, i, fc);
+    for (int q = 0; q < ncomp; ++q) {
+      const double ax = trans ? apply_row<V, true>(v, i, fc, a, x + q * n)
+                              : apply_row<V, false>(v, i, fc, a, x + q * n);
+      const double d = b[q * n + i] - ax;
+      acc[q] += d * d;
+    }
+  }
+  double tot[3];
+  if (grid_reduce<3>(acc, partials, counter, tot)) {
+    for (int q = 0; q < ncomp; ++q) st->c[q].true_res = sqrt(tot[q]);
+  }
+}
+
+// ===========================================================================
+// BiCGStab on ncomp right-hand sides sharing one matrix
+
+struct BiVecs {
+  double *r, *rhat, *p, *v, *phat, *s, *shat, *t;  // each (ncomp, n)
+};
+
+__global__ void k_bi_reset(SolverState *st, int ncomp, int maxiter,
+                           int precond, double tol, int fresh,
+                           unsigned active_mask) {
+  st->ncomp = ncomp;
+  st->precond = precond;
+  st->zero_mean = 0;
+  int all = 1;
+  for (int q = 0; q < 3; ++q) {
+    CompState &c = st->c[q];
+    if (fresh) {
+      c.bnorm = 0.0;
+      c.zero_rhs = 0;
+    }
+    c.active = (q < ncomp) && ((active_mask >> q) & 1u);
+    c.tol = tol;
+    c.iter = 0;
+    c.maxiter = maxiter;
+    c.done = !c.active || c.zero_rhs;
+    c.converged = c.active && c.zero_rhs;
+    c.fail = 0;
+    c.pending = 0;
+    c.res = 0.0;
+    c.true_res = 0.0;
+    if (!c.done) all = 0;
+  }
+  st->all_done = all;
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_bi_bnorm(const double *__restrict__ b, int32_t n, SolverState *st,
+               double *partials, unsigned *counter) {
+  const int nc = st->ncomp;
+  double acc[3] = {0.0, 0.0, 0.0};
+  GRID_LOOP(i, n) {
+    for (int q = 0; q < nc; ++q) {
+      const double x = b[(int64_t)q * n + i];
+      acc[q] += x * x;
+    }
+  }
+  double tot[3];
+  if (grid_reduce<3>(acc, partials, counter, tot)) {
+    int all = 1;
+    for (int q = 0; q < nc; ++q) {
+      CompState &c = st->c[q];
+      c.bnorm = sqrt(tot[q]);
+      c.tol_abs = c.tol * c.bnorm;
+      if (c.bnorm == 0.0 && c.active) {
+        c.zero_rhs = 1;
+        c.done = 1;
+        c.converged = 1;
+      }
+      if (!c.done) all = 0;
+    }
+    st->all_done = all;
+  }
+}
+
+// r = b - A x; rhat = r; p = v = 0
+template <class V, bool kTrans>
+__global__ void __launch_bounds__(kBlock)
+    k_bi_init(V v, const double *__restrict__ a, const double *__restrict__ b,
+              const double *__restrict__ x, BiVecs w, SolverState *st,
+              double *partials, unsigned *counter) {
+  if (st->all_done) return;
+  const int nc = st->ncomp;
+  const int64_t n = v.n;
+  int act[3];
+  for (int q = 0; q < 3; ++q) act[q] = q < nc && !st->c[q].done;
+  double acc[3] = {0.0, 0.0, 0.0};
+  GRID_LOOP(i, v.n) {
+    Face fc[2 * V::kDim];
+    load_faces(v, i, fc);
+    for (int q = 0; q < nc; ++q) {
+      if (!act[q]) continue;
+      const int64_t o = q * n;
+      const double ri = b[o + i] - apply_row<V, kTrans>(v, i, fc, a, x + o);
+      w.r[o + i] = ri;
+      w.rhat[o + i] = ri;
+      w.p[o + i] = 0.0;
+      w.v[o + i] = 0.0;
+      acc[q] += ri * ri;
+    }
+  }
+  double tot[3];
+  if (grid_reduce<3>(acc, partials, counter, tot)) {
+    int all = 1;
+    for (int q = 0; q < nc; ++q) {
+      CompState &c = st->c[q];
+      if (act[q]) {
+        c.res = sqrt(tot[q]);
+        if (c.res <= c.tol_abs) {
+          c.converged = 1;
+          c.done = 1;
+        } else {
+          c.rho = c.alpha = c.omega = 1.0;
+          c.iter = 1;
+          c.rho_new = tot[q];
+          if (fabs(c.rho_new) < DBL_MIN || fabs(c.omega) < DBL_MIN) {
+            c.fail = 1;
+            c.done = 1;
+          } else {
+            c.beta = (c.rho_new / c.rho) * (c.alpha / c.omega);
+          }
+        }
+      }
+      if (!c.done) all = 0;
+    }
+    st->all_done = all;
+  }
+}
+
+// p = r + beta (p - omega v); phat = M p
+__global__ void __launch_bounds__(kBlock)
+    k_bi_p(const double *__restrict__ a, BiVecs w, int32_t n,
+           const SolverState *st) {
+  if (st->all_done) return;
+  const int nc = st->ncomp, pc = st->precond;
+  for (int q = 0; q < nc; ++q) {
+    const CompState &c = st->c[q];
+    if (c.done) continue;
+    const double beta = c.beta, omega = c.omega;
+    const int64_t o = (int64_t)q * n;
+    GRID_LOOP(i, n) {
+      const double pi = w.r[o + i] + beta * (w.p[o + i] - omega * w.v[o + i]);
+      w.p[o + i] = pi;
+      w.phat[o + i] = prec(pc, a, i, pi);
+    }
+  }
+}
+
+// v = A phat; rhat.v -> alpha
+template <class V, bool kTrans>
+__global__ void __launch_bounds__(kBlock)
+    k_bi_v(V v, const double *__restrict__ a, BiVecs w, SolverState *st,
+           double *partials, unsigned *counter) {
+  if (st->all_done) return;
+  const int nc = st->ncomp;
+  const int64_t n = v.n;
+  int act[3];
+  for (int q = 0; q < 3; ++q) act[q] = q < nc && !st->c[q].done;
+  double acc[3] = {0.0, 0.0, 0.0};
+  GRID_LOOP(i, v.n) {
+    Face fc[2 * V::kDim];
+    load_faces(v, i, fc);
+    for (int q = 0; q < nc; ++q) {
+      if (!act[q]) continue;
+      const int64_t o = q * n;
+      const double vi = apply_row<V, kTrans>(v, i, fc, a, w.phat + o);
+      w.v[o + i] = vi;
+      acc[q] += w.rhat[o + i] * vi;
+    }
+  }
+  double tot[3];
+  if (grid_reduce<3>(acc, partials, counter, tot)) {
+    int all = 1;
+    for (int q = 0; q < nc; ++q) {
+      CompState &c = st->c[q];
+      if (act[q]) {
+        if (fabs(tot[q]) < DBL_MIN) {
+          c.fail = 1;
+          c.done = 1;
+        } else {
+          c.alpha = c.rho_new / tot[q];
+        }
+      }
+      if (!c.done) all = 0;
+    }
+    st->all_done = all;
+  }
+}
+
+// s = r - alpha v; shat = M s; |s| -> early exit
+__global__ void __launch_bounds__(kBlock)
+    k_bi_s(const double *__restrict__ a, BiVecs w, int32_t n, SolverState *st,
+           double *partials, unsigned *counter) {
+  if (st->all_done) return;
+  const int nc = st->ncomp, pc = st->precond;
+  int act[3];
+  double alpha[3];
+  for (int q = 0; q < 3; ++q) {
+    act[q] = q < nc && !st->c[q].done;
+    alpha[q] = q < nc ? st->c[q].alpha : 0.0;
+  }
+  double acc[3] = {0.0, 0.0, 0.0};
+  GRID_LOOP(i, n) {
+    for (int q = 0; q < nc; ++q) {
+      if (!act[q]) continue;
+      const int64_t o = (int64_t)q * n;
+      const double si = w.r[o + i] - alpha[q] * w.v[o + i];
+      w.s[o + i] = si;
+      w.shat[o + i] = prec(pc, a, i, si);
+      acc[q] += si * si;
+    }
+  }
+  double tot[3];
+  if (grid_reduce<3>(acc, partials, counter, tot)) {
+    // all_done is deliberately left alone: k_bi_t must still run to apply
+    // the early-exit update x += alpha phat
+    for (int q = 0; q < nc; ++q) {
+      CompState &c = st->c[q];
+      if (!act[q]) continue;
+      c.res = sqrt(tot[q]);
+      if (c.res <= c.tol_abs) {
+        c.converged = 1;
+        c.done = 1;
+        c.pending = 1;
+      }
+    }
+  }
+}
+
+// pending comps: x += alpha phat.  active comps: t = A shat; t.t, t.s -> omega
+template <class V, bool kTrans>
+__global__ void __launch_bounds__(kBlock)
+    k_bi_t(V v, const double *__restrict__ a, BiVecs w, double *__restrict__ x,
+           SolverState *st, double *partials, unsigned *counter) {
+  if (st->all_done) return;
+  const int nc = st->ncomp;
+  const int64_t n = v.n;
+  int act[3], pend[3];
+  double alpha[3];
+  for (int q = 0; q < 3; ++q) {
+    act[q] = q < nc && !st->c[q].done;
+    pend[q] = q < nc && st->c[q].pending;
+    alpha[q] = q < nc ? st->c[q].alpha : 0.0;
+  }
+  double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  GRID_LOOP(i, v.n) {
+    Face fc[2 * V::kDim];
+    load_faces(v, i, fc);
+    for (int q = 0; q < nc; ++q) {
+      const int64_t o = q * n;
+      if (pend[q]) x[o + i] += alpha[q] * w.phat[o + i];
+      if (!act[q]) continue;
+      const double ti = apply_row<V, kTrans>(v, i, fc, a, w.shat + o);
+      w.t[o + i] = ti;
+      acc[2 * q] += ti * ti;
+      acc[2 * q + 1] += ti * w.s[o + i];
+    }
+  }
+  double tot[6];
+  if (grid_reduce<6>(acc, partials, counter, tot)) {
+    int all = 1;
+    for (int q = 0; q < nc; ++q) {
+      CompState &c = st->c[q];
+      c.pending = 0;
+      if (act[q]) {
+        const double tt = tot[2 * q];
+        if (tt < DBL_MIN) {
+          c.fail = 1;
+          c.done = 1;
+        } else {
+          c.omega = tot[2 * q + 1] / tt;
+        }
+      }
+      if (!c.done) all = 0;
+    }
+    st->all_done = all;
+  }
+}
+
+// x += alpha phat + omega shat; r = s - omega t; next rho
+__global__ void __launch_bounds__(kBlock)
+    k_bi_x(BiVecs w, double *__restrict__ x, int32_t n, SolverState *st,
+           double *partials, unsigned *counter) {
+  if (st->all_done) return;
+  const int nc = st->ncomp;
+  int act[3];
+  double alpha[3], omega[3];
+  for (int q = 0; q < 3; ++q) {
+    act[q] = q < nc && !st->c[q].done;
+    alpha[q] = q < nc ? st->c[q].alpha : 0.0;
+    omega[q] = q < nc ? st->c[q].omega : 0.0;
+  }
+  double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  GRID_LOOP(i, n) {
+    for (int q = 0; q < nc; ++q) {
+      if (!act[q]) continue;
+      const int64_t o = (int64_t)q * n;
+      x[o + i] = x[o + i] + alpha[q] * w.phat[o + i] + omega[q] * w.shat[o + i];
+      const double ri = w.s[o + i] - omega[q] * w.t[o + i];
+      w.r[o + i] = ri;
+      acc[2 * q] += ri * ri;
+      acc[2 * q + 1] += w.rhat[o + i] * ri;
+    }
+  }
+  double tot[6];
+  if (grid_reduce<6>(acc, partials, counter, tot)) {
+    int all = 1;
+    for (int q = 0; q < nc; ++q) {
+      CompState &c = st->c[q];
+      if (act[q]) {
+        c.res = sqrt(tot[2 * q]);
+        if (c.res <= c.tol_abs) {
+          c.converged = 1;
+          c.done = 1;
+        } else if (c.iter >= c.maxiter) {
+          c.done = 1;
+        } else {
+          c.rho = c.rho_new;
+          c.iter += 1;
+          c.rho_new = tot[2 * q + 1];
+          if (fabs(c.rho_new) < DBL_MIN || fabs(c.omega) < DBL_MIN) {
+            c.fail = 1;
+            c.done = 1;
+          } else {
+            c.beta = (c.rho_new / c.rho) * (c.alpha / c.omega);
+          }
+        }
+      }
+      if (!c.done) all = 0;
+    }
+    st->all_done = all;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_bi_finish(double *__restrict__ x, int32_t n, const SolverState *st) {
+  for (int q = 0; q < st->ncomp; ++q) {
+    if (!st->c[q].zero_rhs) continue;
+    GRID_LOOP(i, n) x[(int64_t)q * n + i] = 0.0;
+  }
+}
+
+}  // namespace pf
+
+// ===========================================================================
+// host drivers
+
+using namespace pf;
+
+static cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
+
+static int read_state(SolverState *dev, SolverState *host, cudaStream_t s) {
+  PF_CUDA(cudaMemcpyAsync(host, dev, sizeof(SolverState),
+                          cudaMemcpyDeviceToHost, s));
+  PF_CUDA(cudaStreamSynchronize(s));
+  return PF_OK;
+}
+
+namespace {
+
+// iterations to launch before the next host poll
+int next_batch(int done_iters, int hint) {
+  int b = std::max(4, std::min(64, done_iters / 2));
+  if (hint > done_iters) b = std::max(2, std::min(b, hint - done_iters));
+  return b;
+}
+
+template <class V>
+int cg_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
+            SolverState &hs, const double *a, const double *bp, double *x,
+            double tol, int maxiter, int precond, int zero_mean,
+            cudaStream_t s) {
+  const int32_t n = v.n;
+  double *r = w.vecs, *p = w.vecs + n, *q = w.vecs + 2 * (int64_t)n;
+  const int ge = grid_for(n), gr = std::min(grid_for(n), pl.red_blocks);
+  launch(k_cg_reset, 1, 1, s, st, maxiter, precond, zero_mean, tol, 0);
+  launch(k_cg_resid<V>, gr, kBlock, s, v, a, bp, x, r, st, w.partials,
+                                      w.counters);
+  launch(k_cg_rproj, gr, kBlock, s, a, r, n, st, w.partials, w.counters);
+  launch(k_cg_pinit, ge, kBlock, s, a, r, p, n, st);
+  PF_LAUNCH_CHECK("cg setup");
+  int launched = 0;
+  for (;;) {
+    int rc = read_state(st, &hs, s);
+    if (rc) return rc;
+    if (hs.all_done || launched >= maxiter) break;
+    const int b = std::min(next_batch(launched, 0), maxiter - launched);
+    for (int k = 0; k < b; ++k) {
+      launch(k_cg_spmv<V>, gr, kBlock, s, v, a, p, q, st, w.partials,
+                                         w.counters);
+      launch(k_cg_update, gr, kBlock, s, a, p, q, x, r, n, st, w.partials,
+                                        w.counters);
+      launch(k_cg_pupdate, ge, kBlock, s, a, r, p, n, st);
+    }
+    PF_LAUNCH_CHECK("cg iterations");
+    launched += b;
+  }
+  launch(k_cg_finish, ge, kBlock, s, x, n, st);
+  if (hs.c[0].converged && !hs.c[0].zero_rhs) {
+    launch(k_true_res<V>, gr, kBlock, s, v, a, 0, 1, bp, x, st, w.partials,
+                                        w.counters);
+  }
+  PF_LAUNCH_CHECK("cg finish");
+  return read_state(st, &hs, s);
+}
+
+}  // namespace
+
+extern "C" int pf_cg_solve(const pf_plan *plan, const double *a,
+                           const double *b, double b_scale, double *x,
+                           int32_t has_x0,
+                           double tol, int32_t maxiter, int32_t zero_mean,
+                           int32_t precond, void *workspace,
+                           pf_solver_report *report_host, void *stream) {
+  if (!plan || !a || !b || !x || !workspace || !report_host || maxiter < 0) {
+    set_error("pf_cg_solve: bad argument");
+    return PF_ERR_ARG;
+  }
+  const Plan &pl = *reinterpret_cast<const Plan *>(plan);
+  Workspace w = carve(workspace, pl.d.n, pl.d.dim);
+  SolverState *st = reinterpret_cast<SolverState *>(w.solver);
+  cudaStream_t s = S(stream);
+  const int32_t n = (int32_t)pl.d.n;
+  double *bp = w.vecs + 3 * (int64_t)n;
+  return dispatch(pl, [&](auto v) {
+    using V = decltype(v);
+    const int gr = std::min(grid_for(n), pl.red_blocks);
+    SolverState hs;
+    if (!has_x0) PF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+    launch(k_cg_reset, 1, 1, s, st, maxiter, precond, zero_mean, tol, 1);
+    launch(k_cg_bsum, gr, kBlock, s, b, b_scale, n, st, w.partials,
+                                    w.counters);
+    launch(k_cg_bproj, gr, kBlock, s, b, b_scale, bp, n, st, w.partials,
+                                     w.counters);
+    PF_LAUNCH_CHECK("cg rhs");
+    int rc = cg_core<V>(pl, v, w, st, hs, a, bp, x, tol, maxiter, precond,
+                        zero_mean, s);
+    if (rc) return rc;
+    const CompState &c = hs.c[0];
+    pf_solver_report rep;
+    rep.fallback_used = 0;
+    rep.breakdown = c.fail;
+    if (c.zero_rhs) {
+      rep.converged = 1;
+      rep.iterations = 0;
+      rep.residual = 0.0;
+      *report_host = rep;
+      return PF_OK;
+    }
+    bool ok = c.converged && c.true_res <= 10.0 * c.tol_abs;
+    double res = c.converged ? c.true_res : c.res;
+    int iters = c.iter;
+    const double bnorm = c.bnorm;
+    if (!ok && precond) {
+      rep.fallback_used = 1;
+      PF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+      rc = cg_core<V>(pl, v, w, st, hs, a, bp, x, tol, 2 * maxiter, 0,
+                      zero_mean, s);
+      if (rc) return rc;
+      const CompState &c2 = hs.c[0];
+      iters += c2.iter;
+      ok = c2.converged && c2.true_res <= 10.0 * c2.tol_abs;
+      res = c2.converged ? c2.true_res : c2.res;
+      rep.breakdown = c2.fail;
+    }
+    rep.converged = ok;
+    rep.iterations = iters;
+    rep.residual = bnorm > 0 ? res / bnorm : 0.0;
+    *report_host = rep;
+    return PF_OK;
+  });
+}
+
+namespace {
+
+template <class V, bool kTrans>
+int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
+            SolverState &hs, const double *a, const double *b, double *x,
+            int ncomp, double tol, int maxiter, int precond, unsigned mask,
+            int fresh, cudaStream_t s) {
+  const int32_t n = v.n;
+  const int64_t len = (int64_t)ncomp * n;
+  BiVecs bv;
+  double *base = w.vecs;
+  bv.r = base;
+  bv.rhat = base + len;
+  bv.p = base + 2 * len;
+  bv.v = base + 3 * len;
+  bv.phat = base + 4 * len;
+  bv.s = base + 5 * len;
+  bv.shat = base + 6 * len;
+  bv.t = base + 7 * len;
+  const int ge = grid_for(n), gr = std::min(grid_for(n), pl.red_blocks);
+  launch(k_bi_reset, 1, 1, s, st, ncomp, maxiter, precond, tol, fresh, mask);
+  if (fresh) launch(k_bi_bnorm, gr, kBlock, s, b, n, st, w.partials, w.counters);
+  launch(k_bi_init<V, kTrans>, gr, kBlock, s, v, a, b, x, bv, st, w.partials,
+                                             w.counters);
+  PF_LAUNCH_CHECK("bicgstab setup");
+  int launched = 0;
+  for (;;) {
+    int rc = read_state(st, &hs, s);
+    if (rc) return rc;
+    if (hs.all_done || launched >= maxiter) break;
+    const int bsz = std::min(launched < 4 ? 2 : next_batch(launched, 0),
+                             maxiter - launched);
+    for (int k = 0; k < bsz; ++k) {
+      launch(k_bi_p, ge, kBlock, s, a, bv, n, st);
+      launch(k_bi_v<V, kTrans>, gr, kBlock, s, v, a, bv, st, w.partials,
+                                              w.counters);
+      launch(k_bi_s, gr, kBlock, s, a, bv, n, st, w.partials, w.counters);
+      launch(k_bi_t<V, kTrans>, gr, kBlock, s, v, a, bv, x, st, w.partials,
+                                              w.counters);
+      launch(k_bi_x, gr, kBlock, s, bv, x, n, st, w.partials, w.counters);
+    }
+    PF_LAUNCH_CHECK("bicgstab iterations");
+    launched += bsz;
+  }
+  launch(k_bi_finish, ge, kBlock, s, x, n, st);
+  launch(k_true_res<V>, gr, kBlock, s, v, a, kTrans ? 1 : 0, ncomp, b, x, st,
+                                      w.partials, w.counters);
+  PF_LAUNCH_CHECK("bicgstab finish");
+  return read_state(st, &hs, s);
+}
+
+}  // namespace
+
+extern "C" int pf_bicgstab_solve(const pf_plan *plan, const double *a,
+                                 int32_t transpose, int32_t ncomp,
+                                 const double *b, double *x, int32_t has_x0,
+                                 double tol, int32_t maxiter, int32_t precond,
+                                 void *workspace,
+                                 pf_solver_report *reports_host,
+                                 void *stream) {
+  if (!plan || !a || !b || !x || !workspace || !reports_host || ncomp < 1 ||
+      ncomp > 3 || maxiter < 0) {
+    set_error("pf_bicgstab_solve: bad argument");
+    return PF_ERR_ARG;
+  }
+  const Plan &pl = *reinterpret_cast<const Plan *>(plan);
+  if (ncomp > pl.d.dim) {
+    set_error("pf_bicgstab_solve: ncomp exceeds the workspace sizing");
+    return PF_ERR_ARG;
+  }
+  Workspace w = carve(workspace, pl.d.n, pl.d.dim);
+  SolverState *st = reinterpret_cast<SolverState *>(w.solver);
+  cudaStream_t s = S(stream);
+  const int32_t n = (int32_t)pl.d.n;
+  return dispatch(pl, [&](auto v) {
+    using V = decltype(v);
+    auto core = [&](SolverState &hs, double tl, int mi, int pc, unsigned mask,
+                    int fresh) {
+      return transpose
+                 ? bi_core<V, true>(pl, v, w, st, hs, a, b, x, ncomp, tl, mi,
+                                    pc, mask, fresh, s)
+                 : bi_core<V, false>(pl, v, w, st, hs, a, b, x, ncomp, tl, mi,
+                                     pc, mask, fresh, s);
+    };
+    if (!has_x0)
+      PF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n * ncomp, s));
+    SolverState hs;
+    int rc = core(hs, tol, maxiter, precond, 0x7u, 1);
+    if (rc) return rc;
+    pf_solver_report rep[3];
+    double bnorm[3];
+    unsigned redo = 0;
+    for (int q = 0; q < ncomp; ++q) {
+      const CompState &c = hs.c[q];
+      bnorm[q] = c.bnorm;
+      rep[q].fallback_used = 0;
+      rep[q].breakdown = c.fail;
+      if (c.zero_rhs) {
+        rep[q].converged = 1;
+        rep[q].iterations = 0;
+        rep[q].residual = 0.0;
+        continue;
+      }
+      const bool ok = c.converged && c.true_res <= 10.0 * c.tol_abs;
+      rep[q].converged = ok;
+      rep[q].iterations = c.iter;
+      rep[q].residual = (c.converged ? c.true_res : c.res) / c.bnorm;
+      if (!ok && precond) redo |= 1u << q;
+    }
+    if (redo) {
+      for (int q = 0; q < ncomp; ++q)
+        if ((redo >> q) & 1u)
+          PF_CUDA(cudaMemsetAsync(x + (int64_t)q * n, 0, sizeof(double) * n, s));
+      rc = core(hs, tol, 2 * maxiter, 0, redo, 0);
+      if (rc) return rc;
+      for (int q = 0; q < ncomp; ++q) {
+        if (!((redo >> q) & 1u)) continue;
+        const CompState &c = hs.c[q];
+        rep[q].fallback_used = 1;
+        rep[q].breakdown = c.fail;
+        rep[q].iterations += c.iter;
+        rep[q].converged = c.converged && c.true_res <= 10.0 * c.tol_abs;
+        rep[q].residual = (c.converged ? c.true_res : c.res) / bnorm[q];
+      }
+    }
+    for (int q = 0; q < ncomp; ++q) reports_host[q] = rep[q];
+    return PF_OK;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// live per-kernel timing of the CG iteration on a real operator (bench.py
+// roofline): runs `iters` iterations that never converge (tol = 0) and
+// times each of the three iteration kernels with CUDA events on `stream`.
+
+extern "C" int pf_cg_profile(const pf_plan *plan, const double *a,
+                             const double *b, int32_t iters, void *workspace,
+                             double *ms_host, void *stream) {
+  if (!plan || !a || !b || !workspace || !ms_host || iters < 1) {
+    set_error("pf_cg_profile: bad argument");
+    return PF_ERR_ARG;
+  }
+  const Plan &pl = *reinterpret_cast<const Plan *>(plan);
+  Workspace w = carve(workspace, pl.d.n, pl.d.dim);
+  SolverState *st = reinterpret_cast<SolverState *>(w.solver);
+  cudaStream_t s = S(stream);
+  const int32_t n = (int32_t)pl.d.n;
+  double *r = w.vecs, *p = w.vecs + n, *q = w.vecs + 2 * (int64_t)n;
+  double *bp = w.vecs + 3 * (int64_t)n, *x = w.vecs + 4 * (int64_t)n;
+  return dispatch(pl, [&](auto v) {
+    using V = decltype(v);
+    const int ge = grid_for(n), gr = std::min(grid_for(n), pl.red_blocks);
+    PF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+    launch(k_cg_reset, 1, 1, s, st, iters + 1, 1, 1, 0.0, 1);
+    launch(k_cg_bsum, gr, kBlock, s, b, 1.0, n, st, w.partials, w.counters);
+    launch(k_cg_bproj, gr, kBlock, s, b, 1.0, bp, n, st, w.partials,
+           w.counters);
+    launch(k_cg_resid<V>, gr, kBlock, s, v, a, bp, x, r, st, w.partials,
+           w.counters);
+    launch(k_cg_rproj, gr, kBlock, s, a, r, n, st, w.partials, w.counters);
+    launch(k_cg_pinit, ge, kBlock, s, a, r, p, n, st);
+    cudaEvent_t ev[4];
+    for (auto &e : ev) PF_CUDA(cudaEventCreate(&e));
+    double tot[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < iters; ++k) {
+      PF_CUDA(cudaEventRecord(ev[0], s));
+      launch(k_cg_spmv<V>, gr, kBlock, s, v, a, p, q, st, w.partials,
+             w.counters);
+      PF_CUDA(cudaEventRecord(ev[1], s));
+      launch(k_cg_update, gr, kBlock, s, a, p, q, x, r, n, st, w.partials,
+             w.counters);
+      PF_CUDA(cudaEventRecord(ev[2], s));
+      launch(k_cg_pupdate, ge, kBlock, s, a, r, p, n, st);
+      PF_CUDA(cudaEventRecord(ev[3], s));
+      PF_CUDA(cudaEventSynchronize(ev[3]));
+      for (int j = 0; j < 3; ++j) {
+        float ms = 0.f;
+        PF_CUDA(cudaEventElapsedTime(&ms, ev[j], ev[j + 1]));
+        tot[j] += ms;
+      }
+    }
+    for (auto &e : ev) cudaEventDestroy(e);
+    SolverState hs;
+    int rc = read_state(st, &hs, s);
+    if (rc) return rc;
+    if (hs.all_done) {
+      set_error("pf_cg_profile: iteration stopped early (breakdown)");
+      return PF_ERR_ARG;
+    }
+    for (int j = 0; j < 3; ++j) ms_host[j] = tot[j] / iters;
+    return PF_OK;
+  });
+}

@@ -1,0 +1,258 @@
+"""GPU tier: the CUDA path (through libpisob200.so) against the reference's
+golden vectors and the CPU oracle on identical inputs and tolerances."""
+
+import numpy as np
+import pytest
+import torch
+
+import golden_cases as G
+from oracle import pisoref as O
+
+pytestmark = pytest.mark.gpu
+
+GPU_TOL = 1e-12       # solver tolerance on the device
+FIELD_TOL = 1e-8      # relative L-inf parity (north star asks 1e-6 in fp64)
+
+
+def _np(x):
+    return x.detach().cpu().numpy() if torch.is_tensor(x) else np.asarray(x)
+
+
+def _gpu_rollout(name, tol=GPU_TOL):
+    from paper_2505_16992_b200 import piso
+    g = G.load(name)
+    dom = G.build(name)
+    dev = torch.device("cuda:0")
+    state = piso.make_state(dom, u0=g["u0"], device=dev)
+    for b, ref in zip(state.bc, G.split_bc(g, g["bc0"])):
+        b.copy_(torch.as_tensor(ref, device=dev))
+    cfg = piso.StepConfig(dt=float(g["dt"]), nu=float(g["nu"]),
+                          n_correctors=int(g["n_correctors"]),
+                          source=G.source_of(g), tol=tol)
+    ws = piso.PisoWorkspace(dom)
+    tapes, outs = [], []
+    for _ in range(int(g["steps"])):
+        tape = piso.StepTape()
+        state, diag = piso.piso_step(dom, state, cfg, ws, tape)
+        tapes.append(tape)
+        outs.append((state, diag))
+    return g, dom, tapes, outs
+
+
+@pytest.mark.parametrize("name", G.ORTHOGONAL)
+def test_forward_matches_reference(name):
+    g, dom, tapes, outs = _gpu_rollout(name)
+    for k, (st, diag) in enumerate(outs):
+        assert G.rel(_np(st.u), g[f"s{k}_u"]) < FIELD_TOL
+        assert G.rel(_np(st.p), g[f"s{k}_p"]) < FIELD_TOL
+        assert G.rel(_np(tapes[k].c_data), g[f"s{k}_C"]) < FIELD_TOL
+        assert G.rel(-_np(tapes[k].k_data), g[f"s{k}_P"]) < FIELD_TOL
+        assert G.rel(_np(tapes[k].rhs_final), g[f"s{k}_rhs"]) < FIELD_TOL
+        assert G.rel(_np(tapes[k].mom_iters[-1]), g[f"s{k}_ustar"]) \
+            < FIELD_TOL
+        for m, corr in enumerate(tapes[k].correctors):
+            assert G.rel(_np(corr.h), g[f"s{k}_h{m}"]) < FIELD_TOL
+            assert G.rel(_np(corr.p_iters[-1]), g[f"s{k}_p{m}"]) < FIELD_TOL
+        if st.bc:
+            bc = np.concatenate([_np(b) for b in st.bc])
+            assert G.rel(bc, g[f"s{k}_bc"]) < FIELD_TOL
+        assert diag.advout_scale == pytest.approx(
+            float(g[f"s{k}_advout_scale"]), rel=1e-9, abs=1e-12)
+        assert diag.div_wide_max == pytest.approx(
+            float(g[f"s{k}_div_wide_max"]), rel=1e-6, abs=1e-9)
+        assert diag.momentum_iterations > 0
+        assert diag.pressure_iterations > 0
+
+
+@pytest.mark.parametrize("name", G.ORTHOGONAL)
+@pytest.mark.parametrize("path", ["full", "adv_only", "p_only", "none"])
+def test_backward_matches_reference(name, path):
+    from paper_2505_16992_b200 import adjoint
+    g, dom, tapes, outs = _gpu_rollout(name)
+    dev = torch.device("cuda:0")
+    cot = adjoint.GradState(u=torch.as_tensor(g["cot_u"], device=dev),
+                            p=torch.as_tensor(g["cot_p"], device=dev))
+    cots = [None] * (len(tapes) - 1) + [cot]
+    r = adjoint.backward_rollout(dom, tapes, cots, path=path, tol=GPU_TOL)
+    key = f"g_{path}"
+    assert G.rel(_np(r.u), g[key + "_u"]) < FIELD_TOL
+    assert r.nu == pytest.approx(float(g[key + "_nu"]), rel=FIELD_TOL,
+                                 abs=1e-12)
+    assert G.rel(_np(r.source), g[key + "_source"]) < FIELD_TOL
+    if r.bc:
+        bc = np.concatenate([_np(b) for b in r.bc])
+        assert G.rel(bc, g[key + "_bc"]) < FIELD_TOL
+    if path == "none":
+        assert r.solve_iterations == 0
+    else:
+        assert r.solve_iterations > 0
+
+
+def test_backward_step_single_matches_reference():
+    from paper_2505_16992_b200 import adjoint
+    g, dom, tapes, outs = _gpu_rollout("channel")
+    dev = torch.device("cuda:0")
+    cot = adjoint.GradState(u=torch.as_tensor(g["cot_u"], device=dev),
+                            p=torch.as_tensor(g["cot_p"], device=dev))
+    r = adjoint.backward_step(dom, tapes[0], cot, tol=GPU_TOL)
+    assert G.rel(_np(r.u), g["g1_u"]) < FIELD_TOL
+    assert r.nu == pytest.approx(float(g["g1_nu"]), rel=FIELD_TOL)
+    assert G.rel(_np(r.source), g["g1_source"]) < FIELD_TOL
+    assert G.rel(np.concatenate([_np(b) for b in r.bc]), g["g1_bc"]) \
+        < FIELD_TOL
+
+
+def test_backward_bitwise_deterministic():
+    from paper_2505_16992_b200 import adjoint
+    g, dom, tapes, outs = _gpu_rollout("box3d")
+    dev = torch.device("cuda:0")
+    cot = adjoint.GradState(u=torch.as_tensor(g["cot_u"], device=dev),
+                            p=torch.zeros(dom.n, dtype=torch.float64,
+                                          device=dev))
+    g1 = adjoint.backward_step(dom, tapes[-1], cot, tol=GPU_TOL)
+    g2 = adjoint.backward_step(dom, tapes[-1], cot, tol=GPU_TOL)
+    assert torch.equal(g1.u, g2.u)
+    assert g1.nu == g2.nu
+    assert torch.equal(g1.source, g2.source)
+
+
+def test_zero_cotangent_gives_zero_gradient():
+    from paper_2505_16992_b200 import adjoint
+    g, dom, tapes, outs = _gpu_rollout("cavity8")
+    for p in adjoint.GradientPath:
+        r = adjoint.backward_step(dom, tapes[0],
+                                  adjoint.GradState.zeros(dom), path=p)
+        assert float(r.u.abs().max()) == 0.0
+        assert r.nu == 0.0
+        assert all(float(b.abs().max()) == 0.0 for b in r.bc)
+
+
+@pytest.mark.parametrize("name", ["channel", "twoblock_rot", "obstacle"])
+def test_stencil_matvec_and_transpose(name):
+    from paper_2505_16992_b200 import linalg
+    g = G.load(name)
+    dom = G.build(name)
+    plan = dom.device_plan("cuda:0")
+    rng = np.random.default_rng(3)
+    st = g["s0_C"]
+    x = rng.standard_normal(dom.n)
+    for tr in (False, True):
+        y = linalg.stencil_matvec(plan, torch.as_tensor(st, device="cuda:0"),
+                                  torch.as_tensor(x, device="cuda:0"),
+                                  transpose=tr)
+        ref = O.stencil_matvec(dom, st, x, transpose=tr)
+        assert G.rel(_np(y), ref) < 1e-14
+
+
+@pytest.mark.parametrize("name", ["channel", "refined_cavity", "obstacle"])
+def test_cg_matches_oracle_krylov_iterations(name):
+    """Same Jacobi-PCG recurrence as the oracle restatement: same solution
+    and the same iteration count (+-1 for round-off at the threshold)."""
+    from paper_2505_16992_b200 import linalg
+    g = G.load(name)
+    dom = G.build(name)
+    plan = dom.device_plan("cuda:0")
+    K = -g["s0_P"]
+    rng = np.random.default_rng(5)
+    b = rng.standard_normal(dom.n)
+    x_o, ok_o, it_o = O.cg(dom, K, b, tol=1e-10)
+    x, rep = linalg.cg_solve(plan, torch.as_tensor(K, device="cuda:0"),
+                             torch.as_tensor(b, device="cuda:0"), tol=1e-10,
+                             zero_mean=True)
+    assert rep.converged and ok_o
+    assert abs(rep.iterations - it_o) <= 1
+    assert G.rel(_np(x), x_o) < 1e-8
+
+
+@pytest.mark.parametrize("name", ["channel", "backstep"])
+def test_bicgstab_matches_oracle_krylov(name):
+    from paper_2505_16992_b200 import linalg
+    g = G.load(name)
+    dom = G.build(name)
+    plan = dom.device_plan("cuda:0")
+    C = g["s0_C"]
+    rng = np.random.default_rng(6)
+    b = rng.standard_normal((dom.dim, dom.n))
+    x, reps = linalg.bicgstab_solve(plan, torch.as_tensor(C, device="cuda:0"),
+                                    torch.as_tensor(b, device="cuda:0"),
+                                    tol=1e-12)
+    for c in range(dom.dim):
+        xo, ok, it = O.bicgstab(dom, C, b[c], tol=1e-12)
+        assert reps[c].converged and ok
+        assert abs(reps[c].iterations - it) <= 1
+        assert G.rel(_np(x[c]), xo) < 1e-9
+    # transposed system
+    xt, reps = linalg.bicgstab_solve(plan, torch.as_tensor(C, device="cuda:0"),
+                                     torch.as_tensor(b, device="cuda:0"),
+                                     tol=1e-12, transpose=True)
+    for c in range(dom.dim):
+        xo = O.solve_exact(dom, C, b[c], transpose=True)
+        assert G.rel(_np(xt[c]), xo) < 1e-9
+
+
+def test_solver_error_on_nonconvergence():
+    from paper_2505_16992_b200 import linalg
+    g = G.load("channel")
+    dom = G.build("channel")
+    plan = dom.device_plan("cuda:0")
+    K = torch.as_tensor(-g["s0_P"], device="cuda:0")
+    b = torch.as_tensor(np.random.default_rng(0).standard_normal(dom.n),
+                        device="cuda:0")
+    with pytest.raises(linalg.SolverError) as ei:
+        linalg.cg_solve(plan, K, b, tol=1e-14, maxiter=2, zero_mean=True,
+                        stage="pressure[c0i0]")
+    rep = ei.value.report
+    assert not rep.converged and rep.fallback_used
+    assert rep.stage == "pressure[c0i0]"
+    assert rep.iterations == 2 + 4
+
+
+def test_zero_rhs_returns_zero():
+    from paper_2505_16992_b200 import linalg
+    dom = G.build("cavity8")
+    plan = dom.device_plan("cuda:0")
+    K = torch.as_tensor(-G.load("cavity8")["s0_P"], device="cuda:0")
+    x, rep = linalg.cg_solve(plan, K, torch.zeros(dom.n, dtype=torch.float64,
+                                                  device="cuda:0"),
+                             x0=torch.ones(dom.n, dtype=torch.float64,
+                                           device="cuda:0"), zero_mean=True)
+    assert rep.converged and rep.iterations == 0 and rep.residual == 0.0
+    assert float(x.abs().max()) == 0.0
+
+
+def test_nonorthogonal_grid_is_rejected_loudly():
+    from paper_2505_16992_b200 import piso
+    dom = G.build("distorted_nonortho")
+    st = piso.make_state(dom, device="cuda:0")
+    with pytest.raises(NotImplementedError):
+        piso.piso_step(dom, st, piso.StepConfig(dt=0.1, nu=0.1))
+
+
+def test_step_validates_dt_nu():
+    from paper_2505_16992_b200 import piso
+    dom = G.build("cavity8")
+    st = piso.make_state(dom, device="cuda:0")
+    with pytest.raises(ValueError):
+        piso.piso_step(dom, st, piso.StepConfig(dt=0.0, nu=0.1))
+    with pytest.raises(ValueError):
+        piso.piso_step(dom, st, piso.StepConfig(dt=0.1, nu=-1.0))
+
+
+def test_shear_mode_exact_implicit_decay():
+    """Known answer (T/test_piso.py:56-73): one step damps the periodic
+    shear mode by exactly 1/(1 + nu k^2 dt)."""
+    from paper_2505_16992_b200 import mesh, piso
+    nx, ny = 6, 16
+    dom = mesh.make_box((nx, ny))
+    y = dom.centers[:, 1]
+    eps, nu, dt = 1e-3, 0.3, 0.7
+    u0 = np.zeros((dom.n, 2))
+    u0[:, 0] = eps * np.sin(2 * np.pi * y / ny)
+    st = piso.make_state(dom, u0=u0, device="cuda:0")
+    new, diag = piso.piso_step(dom, st, piso.StepConfig(dt=dt, nu=nu,
+                                                        tol=1e-12))
+    k2 = 2.0 - 2.0 * np.cos(2 * np.pi / ny)
+    expected = u0[:, 0] / (1.0 + nu * k2 * dt)
+    assert np.allclose(_np(new.u[:, 0]), expected, atol=1e-12)
+    assert float(new.u[:, 1].abs().max()) < 1e-12
+    assert float(new.p.abs().max()) < 1e-10
