@@ -56,6 +56,10 @@ extern "C" {
 #define PF_TOPO_GATHER 0 /* multi-block: packed neighbour table          */
 #define PF_TOPO_BOX 1    /* single block: neighbours by index arithmetic */
 
+#define PF_PRECOND_NONE 0
+#define PF_PRECOND_JACOBI 1
+#define PF_PRECOND_MG 2
+
 #define PF_BKIND_DIRICHLET 0
 #define PF_BKIND_OUTFLOW 1
 
@@ -175,8 +179,21 @@ PF_API int pf_stencil_matvec(const pf_plan *plan, const double *a, int32_t trans
 PF_API int pf_cg_solve(const pf_plan *plan, const double *a, const double *b,
                        double b_scale, double *x, int32_t has_x0, double tol,
                        int32_t maxiter, int32_t zero_mean, int32_t precond,
-                       void *workspace, pf_solver_report *report_host,
-                       void *stream);
+                       void *workspace, void *mg_workspace,
+                       pf_solver_report *report_host, void *stream);
+
+/* Geometric multigrid for the pressure operator of a box plan (the GPU
+ * replacement of the reference's ILU(0) preconditioner, S/linalg.py:88-108):
+ * Y-line block-Jacobi smoothing, X/Z semi-coarsening with Galerkin
+ * aggregation, exact singular coarsest line solve.  pf_cg_solve with
+ * precond == PF_PRECOND_MG uses the hierarchy last built by pf_mg_setup on
+ * the same mg_workspace.  pf_mg_workspace_bytes returns 0 (and pf_mg_levels
+ * 0) when the plan does not support it (gather topology, periodic line
+ * axis). */
+PF_API int64_t pf_mg_workspace_bytes(const pf_plan *plan);
+PF_API int pf_mg_levels(const pf_plan *plan);
+PF_API int pf_mg_setup(const pf_plan *plan, const double *k,
+                       void *mg_workspace, void *stream);
 
 /* ncomp independent Jacobi-preconditioned BiCGStab solves sharing matrix `a`
  * (transpose != 0 solves with A^t) -- bicgstab_solve / _bicgstab_core,

@@ -61,8 +61,11 @@ _SIGS = {
                           ctypes.POINTER(c_dbl), c_ptr],
     "pf_stencil_matvec": [c_ptr, c_ptr, c_int, c_int, c_ptr, c_ptr, c_ptr],
     "pf_cg_solve": [c_ptr, c_ptr, c_ptr, c_dbl, c_ptr, c_int, c_dbl, c_int,
-                    c_int, c_int, c_ptr, ctypes.POINTER(SolverReportC),
+                    c_int, c_int, c_ptr, c_ptr, ctypes.POINTER(SolverReportC),
                     c_ptr],
+    "pf_mg_workspace_bytes": [c_ptr],
+    "pf_mg_levels": [c_ptr],
+    "pf_mg_setup": [c_ptr, c_ptr, c_ptr, c_ptr],
     "pf_bicgstab_solve": [c_ptr, c_ptr, c_int, c_int, c_ptr, c_ptr, c_int,
                           c_dbl, c_int, c_int, c_ptr,
                           ctypes.POINTER(SolverReportC), c_ptr],
@@ -89,7 +92,7 @@ _SIGS = {
     "pf_reduce_maxabs": [c_ptr, c_ptr, c_i64, c_ptr, ctypes.POINTER(c_dbl),
                          c_ptr],
 }
-_RESTYPES = {"pf_workspace_bytes": c_i64, "pf_last_error": ctypes.c_char_p,
+_RESTYPES = {"pf_workspace_bytes": c_i64, "pf_mg_workspace_bytes": c_i64, "pf_last_error": ctypes.c_char_p,
              "pf_launch_count": ctypes.c_uint64}
 
 EXPORTED = sorted(list(_SIGS) + ["pf_last_error"])

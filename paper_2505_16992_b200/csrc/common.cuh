@@ -41,12 +41,38 @@ inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block,
   kernel<<<grid, block, 0, stream>>>(args...);
 }
 
+// Multigrid hierarchy of a box plan (see mg.cuh); arrays are bound to the
+// caller's MG workspace on every call.
+constexpr int kMgMaxLevels = 16;
+
+struct MgLevel {
+  int32_t sx, sy, sz;   // canonical dims
+  int32_t px, pz;       // periodic X / Z
+  int32_t fx, fy, fz;   // coarsening factors to the next level
+  int32_t pinned;       // singular coarsest line problem
+  int64_t n;
+  double *wx, *wy, *wz;  // +face weights
+  double *cp, *ivd;      // Thomas factors along Y
+  double *r, *x, *t;     // level rhs, solution, scratch
+};
+
+struct MgHierarchy {
+  int nlev;
+  int ax_of[3];  // physical axis of canonical X, Y, Z (-1: absent)
+  MgLevel lv[kMgMaxLevels];
+  double omega;
+};
+
+
 // Host-side plan: the immutable device description plus derived launch
 // parameters.
 struct Plan {
   pf_plan_desc d;
   int num_sms;
   int red_blocks;  // grid of reduction kernels
+  bool has_mg;     // geometric multigrid available for this topology
+  MgHierarchy mg;
+  int64_t mg_bytes;
 };
 
 // ---------------------------------------------------------------------------

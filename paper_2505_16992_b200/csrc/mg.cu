@@ -1,0 +1,418 @@
+// mg.cu -- geometric multigrid V(1,1) preconditioner (see mg.cuh).
+//
+// Level layout: canonical (X, Y, Z) C-order, index ((x*sy)+y)*sz+z, so the
+// Y lines of the smoother are strided by sz and threads of a warp take
+// consecutive z -- every line-solve load is coalesced across the warp.
+// Each level coarsens X, Y, Z by 2 while the axis is even (Y while it stays
+// longer than 2); coarse face weights are sums of the fine faces crossing
+// the coarse face (Galerkin with piecewise-constant aggregation).
+#include <algorithm>
+
+#include "mg.cuh"
+
+namespace pf {
+
+constexpr int kLineBlock = 128;
+constexpr int kChunk = 8;  // rows batched per load phase of a line sweep
+
+__device__ __forceinline__ int32_t parent(const MgLevel &F, const MgLevel &C,
+                                          int32_t x, int32_t y, int32_t z) {
+  return ((x / F.fx) * C.sy + y / F.fy) * C.sz + z / F.fz;
+}
+
+#define MG_DONE_RETURN \
+  if (done && *done) return
+
+// level-0 face weights from the K stencil (row 1 + 2a + 1 holds -w)
+__global__ void __launch_bounds__(kBlock)
+    k_mg_faces0(MgLevel L, const double *__restrict__ k, int64_t n, int ax0,
+                int ax1, int ax2, const int *done) {
+  MG_DONE_RETURN;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  L.wx[i] = ax0 >= 0 ? -k[(int64_t)(2 + 2 * ax0) * n + i] : 0.0;
+  L.wy[i] = -k[(int64_t)(2 + 2 * ax1) * n + i];
+  L.wz[i] = ax2 >= 0 ? -k[(int64_t)(2 + 2 * ax2) * n + i] : 0.0;
+}
+
+// coarse face = sum of the fine faces crossing it
+__global__ void __launch_bounds__(kBlock)
+    k_mg_aggregate(MgLevel F, MgLevel C, const int *done) {
+  MG_DONE_RETURN;
+  const int32_t I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= C.n) return;
+  const Cell3 c = decode(C, I);
+  double wx = 0.0, wy = 0.0, wz = 0.0;
+  for (int dx = 0; dx < F.fx; ++dx)
+    for (int dy = 0; dy < F.fy; ++dy)
+      for (int dz = 0; dz < F.fz; ++dz) {
+        const int32_t j = ((F.fx * c.x + dx) * F.sy + F.fy * c.y + dy) * F.sz +
+                          F.fz * c.z + dz;
+        if (dx == F.fx - 1) wx += F.wx[j];
+        if (dy == F.fy - 1) wy += F.wy[j];
+        if (dz == F.fz - 1) wz += F.wz[j];
+      }
+  C.wx[I] = C.sx > 1 ? wx : 0.0;  // a 1-wide periodic axis: self loop
+  C.wy[I] = wy;
+  C.wz[I] = C.sz > 1 ? wz : 0.0;
+}
+
+// Thomas factors of the Y-line matrices (diagonal = sum of the 6 faces)
+__global__ void __launch_bounds__(kBlock)
+    k_mg_factor(MgLevel L, const int *done) {
+  MG_DONE_RETURN;
+  const int32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L.sx * L.sz) return;
+  const int32_t x = l / L.sz, z = l % L.sz;
+  double cprev = 0.0, wprev = 0.0;
+  for (int y = 0; y < L.sy; ++y) {
+    Cell3 c;
+    c.x = x;
+    c.y = y;
+    c.z = z;
+    c.i = (x * L.sy + y) * L.sz + z;
+    if (L.pinned && y == L.sy - 1) {
+      L.ivd[c.i] = 1.0;
+      L.cp[c.i] = 0.0;
+      break;
+    }
+    const Nbhd b = nbhd(L, c);
+    const double d = b.wxp + b.wxm + b.wyp + b.wym + b.wzp + b.wzm;
+    const double iv = 1.0 / (d + wprev * cprev);
+    const double cc = -b.wyp * iv;
+    L.ivd[c.i] = iv;
+    L.cp[c.i] = cc;
+    cprev = cc;
+    wprev = b.wyp;
+  }
+}
+
+// Y-line solve T z = rhs for the line (x, z), loads batched kChunk rows at a
+// time so the serial recurrence never waits on one load per row.  `tmp`
+// holds the forward sweep and may alias rhs (each element is read before it
+// is overwritten).  mode 0: out = w z; 1: out += w z; 2: out += P xc + w z.
+template <int kMode>
+__device__ __forceinline__ void line_solve(const MgLevel &L, int32_t x,
+                                           int32_t z, const double *rhs,
+                                           double *tmp, double *out,
+                                           double omega,
+                                           const double *cx = nullptr,
+                                           const MgLevel *C = nullptr) {
+  const int32_t st = L.sz;
+  const int32_t base = x * L.sy * L.sz + z;
+  const int32_t sy = L.sy;
+  double dp = 0.0, wprev = 0.0;
+  for (int y0 = 0; y0 < sy; y0 += kChunk) {
+    double rr[kChunk], iv[kChunk], ww[kChunk];
+#pragma unroll
+    for (int k = 0; k < kChunk; ++k) {
+      const int y = y0 + k;
+      if (y < sy) {
+        const int32_t i = base + y * st;
+        rr[k] = rhs[i];
+        iv[k] = L.ivd[i];
+        ww[k] = L.wy[i];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kChunk; ++k) {
+      const int y = y0 + k;
+      if (y < sy) {
+        dp = (L.pinned && y == sy - 1) ? 0.0 : (rr[k] + wprev * dp) * iv[k];
+        wprev = ww[k];
+        tmp[base + y * st] = dp;
+      }
+    }
+  }
+  double znext = 0.0;
+  int32_t cbase = 0, cst = 0;
+  if (kMode == 2) {
+    cbase = (x / L.fx) * C->sy * C->sz + z / L.fz;
+    cst = C->sz;
+  }
+  for (int y0 = sy - 1; y0 >= 0; y0 -= kChunk) {
+    double tt[kChunk], cc[kChunk], oo[kChunk];
+#pragma unroll
+    for (int k = 0; k < kChunk; ++k) {
+      const int y = y0 - k;
+      if (y >= 0) {
+        const int32_t i = base + y * st;
+        tt[k] = tmp[i];
+        cc[k] = L.cp[i];
+        if (kMode == 1) oo[k] = out[i];
+        if (kMode == 2) oo[k] = out[i] + cx[cbase + (y / L.fy) * cst];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kChunk; ++k) {
+      const int y = y0 - k;
+      if (y >= 0) {
+        const double zv = tt[k] - cc[k] * znext;
+        znext = zv;
+        out[base + y * st] = kMode == 0 ? omega * zv : oo[k] + omega * zv;
+      }
+    }
+  }
+}
+
+// x = omega T^-1 r
+__global__ void __launch_bounds__(kLineBlock)
+    k_mg_smooth0(MgLevel L, const double *__restrict__ r, double *x,
+                 double omega, const int *done) {
+  MG_DONE_RETURN;
+  const int32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L.sx * L.sz) return;
+  line_solve<0>(L, l / L.sz, l % L.sz, r, x, x, omega);
+}
+
+// x += omega T^-1 res  (res is consumed as scratch)
+__global__ void __launch_bounds__(kLineBlock)
+    k_mg_smooth1(MgLevel L, double *res, double *x, double omega,
+                 const int *done) {
+  MG_DONE_RETURN;
+  const int32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L.sx * L.sz) return;
+  line_solve<1>(L, l / L.sz, l % L.sz, res, res, x, omega);
+}
+
+// x += P x_c + omega T^-1 res   (res = r - K (x + P x_c), previous pass)
+__global__ void __launch_bounds__(kLineBlock)
+    k_mg_smooth2(MgLevel L, double *res, double *x, double omega, MgLevel C,
+                 const int *done) {
+  MG_DONE_RETURN;
+  const int32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= L.sx * L.sz) return;
+  line_solve<2>(L, l / L.sz, l % L.sz, res, res, x, omega, C.x, &C);
+}
+
+// coarse rhs = sum over the aggregate of r - K x
+__global__ void __launch_bounds__(kBlock)
+    k_mg_resid_restrict(MgLevel F, const double *__restrict__ r,
+                        const double *__restrict__ x, MgLevel C,
+                        const int *done) {
+  MG_DONE_RETURN;
+  const int32_t I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= C.n) return;
+  const Cell3 cc = decode(C, I);
+  double acc = 0.0;
+  for (int dx = 0; dx < F.fx; ++dx)
+    for (int dy = 0; dy < F.fy; ++dy)
+      for (int dz = 0; dz < F.fz; ++dz) {
+        Cell3 c;
+        c.x = F.fx * cc.x + dx;
+        c.y = F.fy * cc.y + dy;
+        c.z = F.fz * cc.z + dz;
+        c.i = (c.x * F.sy + c.y) * F.sz + c.z;
+        const Nbhd b = nbhd(F, c);
+        acc += r[c.i] - kx(b, c.i, x);
+      }
+  C.r[I] = acc;
+}
+
+// res = r - K (x + P x_c): prolongation fused into the residual; x itself is
+// updated by k_mg_smooth2, so no thread writes what another thread reads
+__global__ void __launch_bounds__(kBlock)
+    k_mg_prolong_resid(MgLevel F, const double *__restrict__ r,
+                       const double *__restrict__ x, double *__restrict__ res,
+                       MgLevel C, const int *done) {
+  MG_DONE_RETURN;
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= F.n) return;
+  const Cell3 c = decode(F, i);
+  const Nbhd b = nbhd(F, c);
+  const double *cxv = C.x;
+  const int32_t xp = c.x + 1 < F.sx ? c.x + 1 : 0;
+  const int32_t xm = c.x > 0 ? c.x - 1 : F.sx - 1;
+  const int32_t zp = c.z + 1 < F.sz ? c.z + 1 : 0;
+  const int32_t zm = c.z > 0 ? c.z - 1 : F.sz - 1;
+  const int32_t yp = c.y + 1 < F.sy ? c.y + 1 : c.y;
+  const int32_t ym = c.y > 0 ? c.y - 1 : c.y;
+  const double vi = x[i] + cxv[parent(F, C, c.x, c.y, c.z)];
+  const double kv =
+      b.wxp * (vi - x[b.xp] - cxv[parent(F, C, xp, c.y, c.z)]) +
+      b.wxm * (vi - x[b.xm] - cxv[parent(F, C, xm, c.y, c.z)]) +
+      b.wyp * (vi - x[b.yp] - cxv[parent(F, C, c.x, yp, c.z)]) +
+      b.wym * (vi - x[b.ym] - cxv[parent(F, C, c.x, ym, c.z)]) +
+      b.wzp * (vi - x[b.zp] - cxv[parent(F, C, c.x, c.y, zp)]) +
+      b.wzm * (vi - x[b.zm] - cxv[parent(F, C, c.x, c.y, zm)]);
+  res[i] = r[i] - kv;
+}
+
+// res = r - K x
+__global__ void __launch_bounds__(kBlock)
+    k_mg_resid(MgLevel L, const double *__restrict__ r,
+               const double *__restrict__ x, double *__restrict__ res,
+               const int *done) {
+  MG_DONE_RETURN;
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L.n) return;
+  const Cell3 c = decode(L, i);
+  const Nbhd b = nbhd(L, c);
+  res[i] = r[i] - kx(b, i, x);
+}
+
+// exact solve of the singular coarsest line problem, projected to zero mean
+__global__ void __launch_bounds__(kBlock)
+    k_mg_coarsest(MgLevel L, const int *done) {
+  MG_DONE_RETURN;
+  if (threadIdx.x == 0) line_solve<0>(L, 0, 0, L.r, L.x, L.x, 1.0);
+  __syncthreads();
+  double v[1] = {0.0};
+  for (int32_t i = threadIdx.x; i < L.n; i += blockDim.x) v[0] += L.x[i];
+  block_reduce<1>(v);
+  __shared__ double mean;
+  if (threadIdx.x == 0) mean = v[0] / (double)L.n;
+  __syncthreads();
+  for (int32_t i = threadIdx.x; i < L.n; i += blockDim.x) L.x[i] -= mean;
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+bool mg_plan(const Plan &p, MgHierarchy &h, int64_t *bytes) {
+  h.nlev = 0;
+  h.omega = 0.85;
+  *bytes = 0;
+  if (p.d.topo != PF_TOPO_BOX) return false;
+  const int d = p.d.dim;
+  int sx, sy, sz, px, pz;
+  if (d == 3) {
+    h.ax_of[0] = 0;
+    h.ax_of[1] = 1;
+    h.ax_of[2] = 2;
+    sx = (int)p.d.box_shape[0];
+    sy = (int)p.d.box_shape[1];
+    sz = (int)p.d.box_shape[2];
+    px = p.d.box_periodic[0];
+    pz = p.d.box_periodic[2];
+    if (p.d.box_periodic[1]) return false;
+  } else {
+    h.ax_of[0] = -1;
+    h.ax_of[1] = 0;
+    h.ax_of[2] = 1;
+    sx = 1;
+    sy = (int)p.d.box_shape[0];
+    sz = (int)p.d.box_shape[1];
+    px = 0;
+    pz = p.d.box_periodic[1];
+    if (p.d.box_periodic[0]) return false;
+  }
+  if (sy < 2 || (sx <= 1 && sz <= 1)) return false;
+  int64_t total = 0;
+  for (;;) {
+    MgLevel &L = h.lv[h.nlev];
+    L = MgLevel{};
+    L.sx = sx;
+    L.sy = sy;
+    L.sz = sz;
+    L.px = px;
+    L.pz = pz;
+    L.n = (int64_t)sx * sy * sz;
+    L.fx = (sx % 2 == 0) ? 2 : 1;
+    L.fy = (sy % 2 == 0 && sy > 2) ? 2 : 1;
+    L.fz = (sz % 2 == 0) ? 2 : 1;
+    total += (h.nlev == 0 ? 6 : 8) * L.n;
+    ++h.nlev;
+    const bool last = (L.fx == 1 && L.fz == 1) || h.nlev == kMgMaxLevels;
+    if (last) {
+      L.fx = L.fy = L.fz = 1;
+      L.pinned = (sx == 1 && sz == 1);
+      break;
+    }
+    sx /= L.fx;
+    sy /= L.fy;
+    sz /= L.fz;
+  }
+  *bytes = total * 8;
+  return true;
+}
+
+void mg_bind(MgHierarchy &h, void *base) {
+  double *q = static_cast<double *>(base);
+  for (int k = 0; k < h.nlev; ++k) {
+    MgLevel &L = h.lv[k];
+    L.wx = q;
+    q += L.n;
+    L.wy = q;
+    q += L.n;
+    L.wz = q;
+    q += L.n;
+    L.cp = q;
+    q += L.n;
+    L.ivd = q;
+    q += L.n;
+    L.t = q;
+    q += L.n;
+    if (k > 0) {
+      L.r = q;
+      q += L.n;
+      L.x = q;
+      q += L.n;
+    } else {
+      L.r = L.x = nullptr;
+    }
+  }
+}
+
+static int lines_grid(const MgLevel &L) {
+  return grid_for((int64_t)L.sx * L.sz, kLineBlock);
+}
+
+int mg_setup(const MgHierarchy &h, const double *k, int64_t n, cudaStream_t s,
+             const int *done) {
+  launch(k_mg_faces0, grid_for(n), kBlock, s, h.lv[0], k, n, h.ax_of[0],
+         h.ax_of[1], h.ax_of[2], done);
+  for (int l = 0; l + 1 < h.nlev; ++l)
+    launch(k_mg_aggregate, grid_for(h.lv[l + 1].n), kBlock, s, h.lv[l],
+           h.lv[l + 1], done);
+  for (int l = 0; l < h.nlev; ++l)
+    launch(k_mg_factor, grid_for((int64_t)h.lv[l].sx * h.lv[l].sz), kBlock,
+           s, h.lv[l], done);
+  PF_LAUNCH_CHECK("mg_setup");
+  return PF_OK;
+}
+
+static void vcycle(const MgHierarchy &h, int l, const double *r, double *x,
+                   cudaStream_t s, const int *done) {
+  const MgLevel &L = h.lv[l];
+  if (l == h.nlev - 1) {
+    if (L.pinned) {
+      launch(k_mg_coarsest, 1, kBlock, s, L, done);
+    } else {
+      launch(k_mg_smooth0, lines_grid(L), kLineBlock, s, L, r, x, h.omega,
+             done);
+      for (int it = 0; it < 4; ++it) {
+        launch(k_mg_resid, grid_for(L.n), kBlock, s, L, r, (const double *)x,
+               L.t, done);
+        launch(k_mg_smooth1, lines_grid(L), kLineBlock, s, L, L.t, x,
+               h.omega, done);
+      }
+    }
+    return;
+  }
+  const MgLevel &C = h.lv[l + 1];
+  launch(k_mg_smooth0, lines_grid(L), kLineBlock, s, L, r, x, h.omega, done);
+  launch(k_mg_resid_restrict, grid_for(C.n), kBlock, s, L, r,
+         (const double *)x, C, done);
+  vcycle(h, l + 1, C.r, C.x, s, done);
+  launch(k_mg_prolong_resid, grid_for(L.n), kBlock, s, L, r,
+         (const double *)x, L.t, C, done);
+  launch(k_mg_smooth2, lines_grid(L), kLineBlock, s, L, L.t, x, h.omega, C,
+         done);
+}
+
+int mg_apply(const MgHierarchy &h, const double *r, double *z, cudaStream_t s,
+             const int *done) {
+  MgHierarchy hh = h;
+  hh.lv[0].r = const_cast<double *>(r);
+  hh.lv[0].x = z;
+  if (hh.nlev == 1 && hh.lv[0].pinned) {
+    launch(k_mg_coarsest, 1, kBlock, s, hh.lv[0], done);
+  } else {
+    vcycle(hh, 0, r, z, s, done);
+  }
+  PF_LAUNCH_CHECK("mg_apply");
+  return PF_OK;
+}
+
+}  // namespace pf

@@ -3,6 +3,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "mg.cuh"
 
 namespace pf {
 
@@ -81,6 +82,7 @@ extern "C" int pf_plan_create(const pf_plan_desc *desc, pf_plan **out) {
   p->d = d;
   p->num_sms = sms;
   p->red_blocks = sms * 8 < kMaxRedBlocks ? sms * 8 : kMaxRedBlocks;
+  p->has_mg = mg_plan(*p, p->mg, &p->mg_bytes);
   *out = reinterpret_cast<pf_plan *>(p);
   return PF_OK;
 }
@@ -94,4 +96,32 @@ extern "C" int64_t pf_workspace_bytes(const pf_plan *plan) {
   if (!plan) return -1;
   const Plan &p = *reinterpret_cast<const Plan *>(plan);
   return workspace_bytes(p.d.n, p.d.dim);
+}
+
+extern "C" int64_t pf_mg_workspace_bytes(const pf_plan *plan) {
+  if (!plan) return -1;
+  const Plan &p = *reinterpret_cast<const Plan *>(plan);
+  return p.has_mg ? p.mg_bytes : 0;
+}
+
+extern "C" int pf_mg_levels(const pf_plan *plan) {
+  if (!plan) return -1;
+  const Plan &p = *reinterpret_cast<const Plan *>(plan);
+  return p.has_mg ? p.mg.nlev : 0;
+}
+
+extern "C" int pf_mg_setup(const pf_plan *plan, const double *k,
+                           void *mg_workspace, void *stream) {
+  if (!plan || !k || !mg_workspace) {
+    set_error("pf_mg_setup: null argument");
+    return PF_ERR_ARG;
+  }
+  const Plan &p = *reinterpret_cast<const Plan *>(plan);
+  if (!p.has_mg) {
+    set_error("pf_mg_setup: multigrid is not available for this plan");
+    return PF_ERR_UNSUPPORTED;
+  }
+  MgHierarchy h = p.mg;
+  mg_bind(h, mg_workspace);
+  return mg_setup(h, k, p.d.n, static_cast<cudaStream_t>(stream), nullptr);
 }

@@ -51,8 +51,20 @@ def default_maxiter(n):
     return max(200, 40 * int(round(n ** 0.5)))
 
 
+PRECOND_NONE, PRECOND_JACOBI, PRECOND_MG = 0, 1, 2
+
+
 def _precond_flag(precond):
-    return 0 if precond is None else 1
+    """None -> unpreconditioned; "jacobi" -> Jacobi; "mg" -> multigrid;
+    "ilu0" (the reference's default name) / "auto" -> multigrid where the
+    plan supports it for this solve, Jacobi otherwise."""
+    if precond is None:
+        return PRECOND_NONE
+    if precond in ("jacobi",):
+        return PRECOND_JACOBI
+    if precond in ("mg", "multigrid"):
+        return PRECOND_MG
+    return -1        # auto
 
 
 def _report(c, stage):
@@ -74,11 +86,22 @@ def cg_solve(plan, data, b, x0=None, tol=None, maxiter=None,
         if out is None else out
     if x0 is not None:
         x.copy_(x0)
+    pc = _precond_flag(precond)
+    if pc == -1:
+        # multigrid is built for the zero-mean pressure operator (symmetric
+        # face form with zero row sums); everything else gets Jacobi
+        pc = PRECOND_MG if (zero_mean and plan.has_mg) else PRECOND_JACOBI
+    mgw = None
+    if pc == PRECOND_MG:
+        if not plan.mg_prepare(data):
+            raise ValueError("multigrid preconditioner unavailable for this "
+                             "domain")
+        mgw = plan.mg_workspace
     rep = _lib.SolverReportC()
     _lib.call("pf_cg_solve", plan.handle, _lib.ptr(data), _lib.ptr(b),
               float(b_scale), _lib.ptr(x), int(x0 is not None), tol, maxiter,
-              int(bool(zero_mean)), _precond_flag(precond),
-              _lib.ptr(plan.workspace), ctypes.byref(rep), plan.stream)
+              int(bool(zero_mean)), pc, _lib.ptr(plan.workspace),
+              _lib.ptr(mgw), ctypes.byref(rep), plan.stream)
     report = _report(rep, stage)
     if not report.converged and raise_on_fail:
         raise SolverError(report)
@@ -102,9 +125,11 @@ def bicgstab_solve(plan, data, b, x0=None, tol=None, maxiter=None,
     if x0 is not None:
         x.copy_(x0.reshape(k, n))
     reps = (_lib.SolverReportC * k)()
+    pc = _precond_flag(precond)
+    pc = PRECOND_JACOBI if pc in (-1, PRECOND_MG) else pc
     _lib.call("pf_bicgstab_solve", plan.handle, _lib.ptr(data),
               int(bool(transpose)), k, _lib.ptr(b2), _lib.ptr(x),
-              int(x0 is not None), tol, maxiter, _precond_flag(precond),
+              int(x0 is not None), tol, maxiter, pc,
               _lib.ptr(plan.workspace), reps, plan.stream)
     if stages is None:
         stages = [stage] * k

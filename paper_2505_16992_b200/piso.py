@@ -334,6 +334,15 @@ def piso_step(domain, state, cfg, workspace=None, tape=None):
     dt, nu = float(cfg.dt), float(cfg.nu)
     if dt <= 0 or nu <= 0:
         raise ValueError("dt and nu must be positive")
+    if not torch.is_tensor(state.u):
+        # a reference-style state of NumPy arrays: move it to the device
+        dev = _default_device(None)
+        plan0 = domain.device_plan(dev)
+        state = FlowState(soa(state.u, domain.n, domain.dim, dev).t(),
+                          scalar_field(state.p, domain.n, dev),
+                          bc_views(plan0, bc_soa(plan0, state.bc,
+                                                 domain.dim)),
+                          state.t, state.step)
     dev = state.u.device
     _lib.require_cuda(dev)
     if domain.has_cross_terms():

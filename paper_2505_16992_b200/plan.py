@@ -128,6 +128,10 @@ class DevicePlan:
             nbytes = int(_lib.load().pf_workspace_bytes(handle))
             self.workspace = torch.zeros(nbytes, dtype=torch.uint8,
                                          device=device)
+            self.mg_bytes = int(_lib.load().pf_mg_workspace_bytes(handle))
+            self.mg_levels = int(_lib.load().pf_mg_levels(handle))
+        self.mg_workspace = None
+        self._mg_key = None
 
     def _packed_table(self):
         dom = self.domain
@@ -151,6 +155,40 @@ class DevicePlan:
             raise ValueError("a cell face has neither a neighbour nor a "
                              "boundary face")
         return table.astype(np.int32)
+
+    # multigrid ----------------------------------------------------------------
+
+    @property
+    def has_mg(self):
+        return self.mg_bytes > 0
+
+    def mg_prepare(self, k_stencil):
+        """Build (or reuse) the multigrid hierarchy for operator K.  The key
+        is a per-tensor id plus torch's in-place version counter, so a freed
+        and re-allocated tensor at the same address never reuses a stale
+        hierarchy."""
+        if not self.has_mg:
+            return False
+        uid = getattr(k_stencil, "_pf_mg_uid", None)
+        if uid is None:
+            DevicePlan._uid += 1
+            uid = DevicePlan._uid
+            try:
+                k_stencil._pf_mg_uid = uid
+            except AttributeError:
+                uid = None
+        key = (uid, k_stencil._version) if uid is not None else None
+        if key is not None and key == self._mg_key:
+            return True
+        if self.mg_workspace is None:
+            self.mg_workspace = torch.empty(self.mg_bytes, dtype=torch.uint8,
+                                            device=self.device)
+        _lib.call("pf_mg_setup", self.handle, _lib.ptr(k_stencil),
+                  _lib.ptr(self.mg_workspace), self.stream)
+        self._mg_key = key
+        return True
+
+    _uid = 0
 
     # convenience --------------------------------------------------------------
 
