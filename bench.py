@@ -232,6 +232,86 @@ class ClockSampler:
 # our arm
 
 
+# algorithmic bytes per cell (3D fp64) of the pressure-solver kernels, as
+# tabulated in DESIGN.md: minimum traffic with every array read or written
+# once and stencil neighbours reused on chip
+KERNEL_BYTES = {
+    "k_cg_spmv_faces": 40,        # 3 face weights + p + q
+    "k_cg_spmv": 40,              # survey SpMV_P minimum (stencil form moves 72)
+    "k_cg_update": 48,            # x, p, r, q read; x, r written
+    "k_mg_smooth0 (level 0)": 40,  # r, 1/den, w_y, c' read; x written
+    "k_mg_resid_restrict (level 0)": 41,   # r, x, 3 faces; 1/8 coarse r
+    "k_mg_prolong_resid (level 0)": 49,    # r, x, 3 faces, 1/8 coarse x; res
+    "k_mg_smooth2 (level 0)": 49,  # res, 1/den, w_y, c', x, 1/8 coarse; x
+    "k_cg_zsum": 16,              # r, z
+    "k_cg_pupdate": 24,           # z, p read; p written
+}
+
+
+def measure_roofline(args, dom, plan, state, nu, dt, dev):
+    """Per-kernel live timing of the production pressure-CG iteration on this
+    step's operator (CUDA events on the launching stream, pf_cg_profile);
+    the roofline entry is the kernel with the largest time share."""
+    import ctypes
+    import torch
+    from paper_2505_16992_b200 import _lib
+    from paper_2505_16992_b200 import piso as P
+    c = P.assemble_momentum(dom, state.u, nu, dt)
+    k = torch.empty_like(c)
+    _lib.call("pf_assemble_pressure", plan.handle, _lib.ptr(c), 0,
+              _lib.ptr(k), plan.stream)
+    b = torch.randn(dom.n, dtype=torch.float64, device=dev)
+    mg = plan.has_mg
+    if mg:
+        plan.mg_prepare(k)
+    ms = (ctypes.c_double * 10)()
+    _lib.call("pf_cg_profile", plan.handle, _lib.ptr(k), _lib.ptr(b),
+              args.profile_iters, 2 if mg else 1, _lib.ptr(plan.workspace),
+              _lib.ptr(plan.mg_workspace if mg else None), ms, plan.stream)
+    names = (["k_cg_spmv_faces" if mg else "k_cg_spmv", "k_cg_update"]
+             + (["k_mg_smooth0 (level 0)", "k_mg_resid_restrict (level 0)",
+                 "mg coarse levels", "k_mg_prolong_resid (level 0)",
+                 "k_mg_smooth2 (level 0)", "k_cg_zsum"] if mg else
+                [None] * 6) + ["k_cg_pupdate"])
+    idx = [0, 1, 2, 3, 4, 5, 6, 7, 8]
+    per = {}
+    for j, nm in zip(idx, names):
+        if nm is not None:
+            per[nm] = float(ms[j])
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    n = dom.n
+    cand = {k: v for k, v in per.items() if k in KERNEL_BYTES and v > 0}
+    top = max(cand, key=cand.get)
+    top_gbs = KERNEL_BYTES[top] * n / (cand[top] * 1e-3) / 1e9
+    it_ms = float(ms[9])
+    it_bytes = sum(KERNEL_BYTES[k] for k in cand)
+    fine_ms = sum(cand.values())
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.config, {}).get(top)
+        except (OSError, ValueError, AttributeError):
+            traffic = None
+    return {"bound": "hbm", "kernel": top, "achieved": top_gbs, "peak": peak,
+            "unit": "GB/s", "frac": top_gbs / peak, "traffic": traffic,
+            "peak_source": peak_src, "bytes_per_cell": KERNEL_BYTES[top],
+            "cells_per_launch": n, "ms_per_launch": cand[top],
+            "pressure_cg_iteration": {
+                "preconditioner": "multigrid" if mg else "jacobi",
+                "ms": it_ms, "level0_and_cg_ms": fine_ms,
+                "level0_and_cg_bytes_per_cell": it_bytes,
+                "level0_and_cg_achieved_gbs":
+                    it_bytes * n / (fine_ms * 1e-3) / 1e9,
+                "ms_per_kernel": per}}
+
+
 def build_workload(args, dev):
     import numpy as np
     import torch
@@ -349,37 +429,7 @@ def main():
         ms_e2e = float(t.item())
     e2e_value = world * dom.n * args.steps / (ms_e2e / 1e3) / 1e6
 
-    # roofline of the dominant kernel (CG SpMV) on this step's operator
-    import ctypes
-    from paper_2505_16992_b200 import piso as P
-    c = P.assemble_momentum(dom, state.u, nu, dt)
-    k = torch.empty_like(c)
-    _lib.call("pf_assemble_pressure", plan.handle, _lib.ptr(c), 0,
-              _lib.ptr(k), plan.stream)
-    b = torch.randn(dom.n, dtype=torch.float64, device=dev)
-    ms3 = (ctypes.c_double * 3)()
-    _lib.call("pf_cg_profile", plan.handle, _lib.ptr(k), _lib.ptr(b),
-              args.profile_iters, _lib.ptr(plan.workspace), ms3, plan.stream)
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except OSError:
-        pass
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    n = dom.n
-    spmv_bytes = 40 * n          # (d+2) s: 3 face coefficients + x + y
-    iter_bytes = 136 * n         # SURVEY §8 d fused Jacobi-PCG iteration
-    spmv_gbs = spmv_bytes / (ms3[0] * 1e-3) / 1e9
-    iter_ms = ms3[0] + ms3[1] + ms3[2]
-    iter_gbs = iter_bytes / (iter_ms * 1e-3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic_spmv.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(args.config)
-        except (OSError, ValueError):
-            traffic = None
+    roofline = measure_roofline(args, dom, plan, state, nu, dt, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -404,16 +454,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reichardt_init seed 0, random cotangent)",
             "config": workload_config(args),
-            "roofline": {"bound": "hbm", "kernel": "k_cg_spmv (PCG SpMV + p.Ap)",
-                         "achieved": spmv_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": spmv_gbs / peak, "traffic": traffic,
-                         "peak_source": peak_src,
-                         "bytes_per_cell": 40, "ms_per_launch": ms3[0],
-                         "cg_iteration": {"bytes_per_cell": 136,
-                                          "ms": iter_ms,
-                                          "achieved_gbs": iter_gbs,
-                                          "frac": iter_gbs / peak,
-                                          "ms_per_kernel": list(ms3)}},
+            "roofline": roofline,
             "cpu_baseline": cpu,
             "clocks": clk,
             "e2e": {"value": e2e_value, "unit": UNIT,

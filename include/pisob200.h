@@ -206,12 +206,17 @@ PF_API int pf_bicgstab_solve(const pf_plan *plan, const double *a, int32_t trans
                       pf_solver_report *reports_host, void *stream);
 
 /* Live timing of the CG iteration kernels on operator `a` (tol = 0, so the
- * recurrence never stops): ms_host[0..2] = average ms per launch of the
- * SpMV + p.Ap kernel, the x/r update + reductions kernel and the direction
- * update kernel over `iters` iterations, timed with CUDA events on
- * `stream`.  Used by bench.py for the roofline figure. */
+ * recurrence never stops), over `iters` iterations, timed with CUDA events
+ * on `stream`; average ms per iteration of:
+ *   ms_host[0] SpMV + p.Ap   [1] x/r update + sums
+ *   [2..6] multigrid level 0: line smooth | residual+restrict | all coarse
+ *          levels | prolong+residual | line smooth with correction
+ *          (precond == PF_PRECOND_MG; zero otherwise)
+ *   [7] z sums   [8] direction update   [9] whole iteration.
+ * Used by bench.py for the roofline figure. */
 PF_API int pf_cg_profile(const pf_plan *plan, const double *a,
-                         const double *b, int32_t iters, void *workspace,
+                         const double *b, int32_t iters, int32_t precond,
+                         void *workspace, void *mg_workspace,
                          double *ms_host, void *stream);
 
 /* ---- adjoint stage kernels (S/adjoint.py) --------------------------------- */

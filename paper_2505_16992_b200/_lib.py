@@ -69,7 +69,7 @@ _SIGS = {
     "pf_bicgstab_solve": [c_ptr, c_ptr, c_int, c_int, c_ptr, c_ptr, c_int,
                           c_dbl, c_int, c_int, c_ptr,
                           ctypes.POINTER(SolverReportC), c_ptr],
-    "pf_cg_profile": [c_ptr, c_ptr, c_ptr, c_int, c_ptr,
+    "pf_cg_profile": [c_ptr, c_ptr, c_ptr, c_int, c_int, c_ptr, c_ptr,
                       ctypes.POINTER(c_dbl), c_ptr],
     "pf_bwd_correct_velocity": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
                                 c_ptr, c_ptr, c_ptr],

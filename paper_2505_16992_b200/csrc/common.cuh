@@ -64,6 +64,15 @@ struct MgHierarchy {
 };
 
 
+// Cached CUDA graph of the multigrid CG iteration (keyed by the buffers it
+// was captured on) and the private stream used for capturing it.
+struct GraphCache {
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t cap = nullptr;
+  const void *key[3] = {nullptr, nullptr, nullptr};
+  unsigned long long nkern = 0;
+};
+
 // Host-side plan: the immutable device description plus derived launch
 // parameters.
 struct Plan {
@@ -73,6 +82,7 @@ struct Plan {
   bool has_mg;     // geometric multigrid available for this topology
   MgHierarchy mg;
   int64_t mg_bytes;
+  mutable GraphCache graph;
 };
 
 // ---------------------------------------------------------------------------

@@ -17,7 +17,9 @@ constexpr int kChunk = 8;  // rows batched per load phase of a line sweep
 
 __device__ __forceinline__ int32_t parent(const MgLevel &F, const MgLevel &C,
                                           int32_t x, int32_t y, int32_t z) {
-  return ((x / F.fx) * C.sy + y / F.fy) * C.sz + z / F.fz;
+  // coarsening factors are 1 or 2: shifts instead of integer division
+  return ((x >> (F.fx - 1)) * C.sy + (y >> (F.fy - 1))) * C.sz +
+         (z >> (F.fz - 1));
 }
 
 #define MG_DONE_RETURN \
@@ -127,7 +129,7 @@ __device__ __forceinline__ void line_solve(const MgLevel &L, int32_t x,
   double znext = 0.0;
   int32_t cbase = 0, cst = 0;
   if (kMode == 2) {
-    cbase = (x / L.fx) * C->sy * C->sz + z / L.fz;
+    cbase = (x >> (L.fx - 1)) * C->sy * C->sz + (z >> (L.fz - 1));
     cst = C->sz;
   }
   for (int y0 = sy - 1; y0 >= 0; y0 -= kChunk) {
@@ -140,7 +142,7 @@ __device__ __forceinline__ void line_solve(const MgLevel &L, int32_t x,
         tt[k] = tmp[i];
         cc[k] = L.cp[i];
         if (kMode == 1) oo[k] = out[i];
-        if (kMode == 2) oo[k] = out[i] + cx[cbase + (y / L.fy) * cst];
+        if (kMode == 2) oo[k] = out[i] + cx[cbase + (y >> (L.fy - 1)) * cst];
       }
     }
 #pragma unroll
@@ -373,7 +375,10 @@ int mg_setup(const MgHierarchy &h, const double *k, int64_t n, cudaStream_t s,
 }
 
 static void vcycle(const MgHierarchy &h, int l, const double *r, double *x,
-                   cudaStream_t s, const int *done) {
+                   cudaStream_t s, const int *done, cudaEvent_t *ev = nullptr) {
+  auto mark = [&](int k) {
+    if (ev && l == 0) cudaEventRecord(ev[k], s);
+  };
   const MgLevel &L = h.lv[l];
   if (l == h.nlev - 1) {
     if (L.pinned) {
@@ -391,25 +396,31 @@ static void vcycle(const MgHierarchy &h, int l, const double *r, double *x,
     return;
   }
   const MgLevel &C = h.lv[l + 1];
+  mark(0);
   launch(k_mg_smooth0, lines_grid(L), kLineBlock, s, L, r, x, h.omega, done);
+  mark(1);
   launch(k_mg_resid_restrict, grid_for(C.n), kBlock, s, L, r,
          (const double *)x, C, done);
+  mark(2);
   vcycle(h, l + 1, C.r, C.x, s, done);
+  mark(3);
   launch(k_mg_prolong_resid, grid_for(L.n), kBlock, s, L, r,
          (const double *)x, L.t, C, done);
+  mark(4);
   launch(k_mg_smooth2, lines_grid(L), kLineBlock, s, L, L.t, x, h.omega, C,
          done);
+  mark(5);
 }
 
 int mg_apply(const MgHierarchy &h, const double *r, double *z, cudaStream_t s,
-             const int *done) {
+             const int *done, cudaEvent_t *ev) {
   MgHierarchy hh = h;
   hh.lv[0].r = const_cast<double *>(r);
   hh.lv[0].x = z;
   if (hh.nlev == 1 && hh.lv[0].pinned) {
     launch(k_mg_coarsest, 1, kBlock, s, hh.lv[0], done);
   } else {
-    vcycle(hh, 0, r, z, s, done);
+    vcycle(hh, 0, r, z, s, done, ev);
   }
   PF_LAUNCH_CHECK("mg_apply");
   return PF_OK;

@@ -84,7 +84,9 @@ void mg_bind(MgHierarchy &h, void *base);
 int mg_setup(const MgHierarchy &h, const double *k_stencil, int64_t n,
              cudaStream_t s, const int *all_done);
 // z = V(r) on the fine level; every kernel returns at once when *all_done.
+// `ev` (optional, 6 events) is recorded around the level-0 kernels:
+// smooth0 | restrict | coarse levels | prolong | smooth2.
 int mg_apply(const MgHierarchy &h, const double *r, double *z,
-             cudaStream_t s, const int *all_done);
+             cudaStream_t s, const int *all_done, cudaEvent_t *ev = nullptr);
 
 }  // namespace pf

@@ -78,7 +78,7 @@ extern "C" int pf_plan_create(const pf_plan_desc *desc, pf_plan **out) {
   int dev = 0, sms = 148;
   PF_CUDA(cudaGetDevice(&dev));
   PF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  Plan *p = new Plan;
+  Plan *p = new Plan();
   p->d = d;
   p->num_sms = sms;
   p->red_blocks = sms * 8 < kMaxRedBlocks ? sms * 8 : kMaxRedBlocks;
@@ -88,7 +88,12 @@ extern "C" int pf_plan_create(const pf_plan_desc *desc, pf_plan **out) {
 }
 
 extern "C" int pf_plan_destroy(pf_plan *plan) {
-  delete reinterpret_cast<Plan *>(plan);
+  Plan *p = reinterpret_cast<Plan *>(plan);
+  if (p) {
+    if (p->graph.exec) cudaGraphExecDestroy(p->graph.exec);
+    if (p->graph.cap) cudaStreamDestroy(p->graph.cap);
+  }
+  delete p;
   return PF_OK;
 }
 

@@ -754,6 +754,106 @@ int next_batch(int done_iters, int hint) {
   return b;
 }
 
+// one multigrid-preconditioned CG iteration on workspace buffers only
+void mg_iteration(const Plan &pl, Workspace &w, SolverState *st,
+                  const MgHierarchy *mg, double *x, cudaStream_t s) {
+  const int32_t n = (int32_t)pl.d.n;
+  double *r = w.vecs, *p = w.vecs + n, *q = w.vecs + 2 * (int64_t)n;
+  double *z = w.vecs + 4 * (int64_t)n;
+  const int ge = grid_for(n), gr = std::min(grid_for(n), pl.red_blocks);
+  launch(k_cg_spmv_faces, gr, kBlock, s, mg->lv[0], (const double *)p, q, st,
+         w.partials, w.counters);
+  launch(k_cg_update, gr, kBlock, s, (const double *)nullptr,
+         (const double *)p, (const double *)q, x, r, n, st, w.partials,
+         w.counters);
+  mg_apply(*mg, r, z, s, &st->all_done);
+  launch(k_cg_zsum, gr, kBlock, s, (const double *)r, (const double *)z, n, 0,
+         st, w.partials, w.counters);
+  launch(k_cg_pupdate, ge, kBlock, s, (const double *)nullptr,
+         (const double *)r, (const double *)z, p, n, st);
+}
+
+constexpr int kGraphIters = 4;  // MG-PCG iterations per graph launch
+
+// Graph of kGraphIters iterations, cached on the plan for its buffers.
+int mg_graph(const Plan &pl, Workspace &w, SolverState *st,
+             const MgHierarchy *mg, double *x, cudaGraphExec_t *out,
+             unsigned long long *nkern) {
+  GraphCache &gc = pl.graph;
+  const void *key[3] = {w.vecs, mg->lv[0].wx, x};
+  if (gc.exec && gc.key[0] == key[0] && gc.key[1] == key[1] &&
+      gc.key[2] == key[2]) {
+    *out = gc.exec;
+    *nkern = gc.nkern;
+    return PF_OK;
+  }
+  if (gc.exec) {
+    cudaGraphExecDestroy(gc.exec);
+    gc.exec = nullptr;
+  }
+  if (!gc.cap) PF_CUDA(cudaStreamCreateWithFlags(&gc.cap, cudaStreamNonBlocking));
+  const unsigned long long before = g_launches;
+  PF_CUDA(cudaStreamBeginCapture(gc.cap, cudaStreamCaptureModeThreadLocal));
+  for (int k = 0; k < kGraphIters; ++k) mg_iteration(pl, w, st, mg, x, gc.cap);
+  cudaGraph_t graph;
+  PF_CUDA(cudaStreamEndCapture(gc.cap, &graph));
+  gc.nkern = g_launches - before;
+  g_launches = before;  // captured, not launched
+  cudaError_t e = cudaGraphInstantiate(&gc.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  PF_CUDA(e);
+  for (int j = 0; j < 3; ++j) gc.key[j] = key[j];
+  *out = gc.exec;
+  *nkern = gc.nkern;
+  return PF_OK;
+}
+
+template <class V>
+int cg_core_mg(const Plan &pl, const V &v, Workspace &w, SolverState *st,
+               SolverState &hs, const double *a, const double *bp, double *x,
+               double tol, int maxiter, int zero_mean, const MgHierarchy *mg,
+               cudaStream_t s) {
+  const int32_t n = v.n;
+  double *r = w.vecs, *p = w.vecs + n;
+  double *z = w.vecs + 4 * (int64_t)n;
+  const int *done = &st->all_done;
+  const int ge = grid_for(n), gr = std::min(grid_for(n), pl.red_blocks);
+  launch(k_cg_reset, 1, 1, s, st, maxiter, 2, zero_mean, tol, 0);
+  launch(k_cg_resid<V>, gr, kBlock, s, v, a, bp, (const double *)x, r, st,
+         w.partials, w.counters);
+  launch(k_cg_rproj, gr, kBlock, s, a, r, n, st, w.partials, w.counters);
+  int rc = mg_apply(*mg, r, z, s, done);
+  if (rc) return rc;
+  launch(k_cg_zsum, gr, kBlock, s, (const double *)r, (const double *)z, n, 1,
+         st, w.partials, w.counters);
+  launch(k_cg_pinit, ge, kBlock, s, a, r, (const double *)z, p, n, st);
+  PF_LAUNCH_CHECK("mg-cg setup");
+  cudaGraphExec_t exec;
+  unsigned long long nk = 0;
+  rc = mg_graph(pl, w, st, mg, x, &exec, &nk);
+  if (rc) return rc;
+  int launched = 0;
+  for (;;) {
+    rc = read_state(st, &hs, s);
+    if (rc) return rc;
+    if (hs.all_done || launched >= maxiter) break;
+    int b = std::min(next_batch(launched, 0), maxiter - launched);
+    b = std::max(1, (b + kGraphIters - 1) / kGraphIters);
+    for (int k = 0; k < b; ++k) {
+      PF_CUDA(cudaGraphLaunch(exec, s));
+      g_launches += nk;
+    }
+    launched += b * kGraphIters;
+  }
+  launch(k_cg_finish, ge, kBlock, s, x, n, st);
+  if (hs.c[0].converged && !hs.c[0].zero_rhs) {
+    launch(k_true_res<V>, gr, kBlock, s, v, a, 0, 1, bp, (const double *)x,
+           st, w.partials, w.counters);
+  }
+  PF_LAUNCH_CHECK("mg-cg finish");
+  return PF_OK;
+}
+
 template <class V>
 int cg_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
             SolverState &hs, const double *a, const double *bp, double *x,
@@ -764,6 +864,19 @@ int cg_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   double *z = w.vecs + 4 * (int64_t)n;
   const int *done = &st->all_done;
   const int ge = grid_for(n), gr = std::min(grid_for(n), pl.red_blocks);
+  if (precond == 2) {
+    // the multigrid iteration runs from a CUDA graph whose buffers are all
+    // workspace-resident: iterate on a workspace copy of x
+    double *xw = w.vecs + 5 * (int64_t)n;
+    PF_CUDA(cudaMemcpyAsync(xw, x, sizeof(double) * n,
+                            cudaMemcpyDeviceToDevice, s));
+    int rc = cg_core_mg(pl, v, w, st, hs, a, bp, xw, tol, maxiter, zero_mean,
+                        mg, s);
+    if (rc) return rc;
+    PF_CUDA(cudaMemcpyAsync(x, xw, sizeof(double) * n,
+                            cudaMemcpyDeviceToDevice, s));
+    return read_state(st, &hs, s);
+  }
   launch(k_cg_reset, 1, 1, s, st, maxiter, precond, zero_mean, tol, 0);
   launch(k_cg_resid<V>, gr, kBlock, s, v, a, bp, x, r, st, w.partials,
                                       w.counters);
@@ -1026,52 +1139,91 @@ extern "C" int pf_bicgstab_solve(const pf_plan *plan, const double *a,
 // times each of the three iteration kernels with CUDA events on `stream`.
 
 extern "C" int pf_cg_profile(const pf_plan *plan, const double *a,
-                             const double *b, int32_t iters, void *workspace,
+                             const double *b, int32_t iters, int32_t precond,
+                             void *workspace, void *mg_workspace,
                              double *ms_host, void *stream) {
-  if (!plan || !a || !b || !workspace || !ms_host || iters < 1) {
+  if (!plan || !a || !b || !workspace || !ms_host || iters < 1 ||
+      precond < 0 || precond > 2) {
     set_error("pf_cg_profile: bad argument");
     return PF_ERR_ARG;
   }
   const Plan &pl = *reinterpret_cast<const Plan *>(plan);
+  MgHierarchy mg;
+  if (precond == 2) {
+    if (!pl.has_mg || !mg_workspace) {
+      set_error("pf_cg_profile: multigrid unavailable");
+      return PF_ERR_UNSUPPORTED;
+    }
+    mg = pl.mg;
+    mg_bind(mg, mg_workspace);
+  }
   Workspace w = carve(workspace, pl.d.n, pl.d.dim);
   SolverState *st = reinterpret_cast<SolverState *>(w.solver);
   cudaStream_t s = S(stream);
   const int32_t n = (int32_t)pl.d.n;
   double *r = w.vecs, *p = w.vecs + n, *q = w.vecs + 2 * (int64_t)n;
-  double *bp = w.vecs + 3 * (int64_t)n, *x = w.vecs + 4 * (int64_t)n;
+  double *bp = w.vecs + 3 * (int64_t)n, *z = w.vecs + 4 * (int64_t)n;
+  double *x = w.vecs + 5 * (int64_t)n;
+  const int *done = &st->all_done;
   return dispatch(pl, [&](auto v) {
     using V = decltype(v);
     const int ge = grid_for(n), gr = std::min(grid_for(n), pl.red_blocks);
     PF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
-    launch(k_cg_reset, 1, 1, s, st, iters + 1, 1, 1, 0.0, 1);
+    launch(k_cg_reset, 1, 1, s, st, iters + 1, precond, 1, 0.0, 1);
     launch(k_cg_bsum, gr, kBlock, s, b, 1.0, n, st, w.partials, w.counters);
     launch(k_cg_bproj, gr, kBlock, s, b, 1.0, bp, n, st, w.partials,
            w.counters);
     launch(k_cg_resid<V>, gr, kBlock, s, v, a, bp, x, r, st, w.partials,
            w.counters);
     launch(k_cg_rproj, gr, kBlock, s, a, r, n, st, w.partials, w.counters);
-    launch(k_cg_pinit, ge, kBlock, s, a, r, (const double *)nullptr, p, n,
-           st);
-    cudaEvent_t ev[4];
+    if (precond == 2) {
+      int rc = mg_apply(mg, r, z, s, done);
+      if (rc) return rc;
+      launch(k_cg_zsum, gr, kBlock, s, (const double *)r, (const double *)z,
+             n, 1, st, w.partials, w.counters);
+    }
+    launch(k_cg_pinit, ge, kBlock, s, a, r, (const double *)z, p, n, st);
+    // events: 0 start | 1 spmv | 2 update | 3..8 mg level-0 marks | 9 zsum |
+    // 10 pupdate
+    cudaEvent_t ev[11];
     for (auto &e : ev) PF_CUDA(cudaEventCreate(&e));
-    double tot[3] = {0.0, 0.0, 0.0};
+    double tot[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     for (int k = 0; k < iters; ++k) {
       PF_CUDA(cudaEventRecord(ev[0], s));
-      launch(k_cg_spmv<V>, gr, kBlock, s, v, a, p, q, st, w.partials,
-             w.counters);
+      if (precond == 2)
+        launch(k_cg_spmv_faces, gr, kBlock, s, mg.lv[0], (const double *)p,
+               q, st, w.partials, w.counters);
+      else
+        launch(k_cg_spmv<V>, gr, kBlock, s, v, a, p, q, st, w.partials,
+               w.counters);
       PF_CUDA(cudaEventRecord(ev[1], s));
       launch(k_cg_update, gr, kBlock, s, a, p, q, x, r, n, st, w.partials,
              w.counters);
       PF_CUDA(cudaEventRecord(ev[2], s));
-      launch(k_cg_pupdate, ge, kBlock, s, a, r, (const double *)nullptr, p, n,
-             st);
-      PF_CUDA(cudaEventRecord(ev[3], s));
-      PF_CUDA(cudaEventSynchronize(ev[3]));
-      for (int j = 0; j < 3; ++j) {
+      if (precond == 2) {
+        int rc = mg_apply(mg, r, z, s, done, ev + 3);
+        if (rc) return rc;
+        launch(k_cg_zsum, gr, kBlock, s, (const double *)r,
+               (const double *)z, n, 0, st, w.partials, w.counters);
+      } else {
+        for (int j = 3; j < 9; ++j) PF_CUDA(cudaEventRecord(ev[j], s));
+      }
+      PF_CUDA(cudaEventRecord(ev[9], s));
+      launch(k_cg_pupdate, ge, kBlock, s, a, r, (const double *)z, p, n, st);
+      PF_CUDA(cudaEventRecord(ev[10], s));
+      PF_CUDA(cudaEventSynchronize(ev[10]));
+      // spmv, update, [mg: smooth0, restrict, coarse, prolong, smooth2],
+      // zsum, pupdate, whole iteration
+      const int from[9] = {0, 1, 3, 4, 5, 6, 7, 8, 9};
+      const int to[9] = {1, 2, 4, 5, 6, 7, 8, 9, 10};
+      for (int j = 0; j < 9; ++j) {
         float ms = 0.f;
-        PF_CUDA(cudaEventElapsedTime(&ms, ev[j], ev[j + 1]));
+        PF_CUDA(cudaEventElapsedTime(&ms, ev[from[j]], ev[to[j]]));
         tot[j] += ms;
       }
+      float ms = 0.f;
+      PF_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[10]));
+      tot[9] += ms;
     }
     for (auto &e : ev) cudaEventDestroy(e);
     SolverState hs;
@@ -1081,7 +1233,7 @@ extern "C" int pf_cg_profile(const pf_plan *plan, const double *a,
       set_error("pf_cg_profile: iteration stopped early (breakdown)");
       return PF_ERR_ARG;
     }
-    for (int j = 0; j < 3; ++j) ms_host[j] = tot[j] / iters;
+    for (int j = 0; j < 10; ++j) ms_host[j] = tot[j] / iters;
     return PF_OK;
   });
 }
