@@ -90,6 +90,15 @@ typedef struct pf_plan_desc {
   const double *bjac;    /* (m) face J                                */
   const double *bt;      /* (d, m) face T[a][j], a = face axis        */
   const double *balpha;  /* (m) face alpha[a][a]                      */
+  /* non-orthogonal grids only (NULL / 0 otherwise): the lagged cross
+   * fluxes of S/piso.py:322-353, 375-392, 431-449 */
+  const double *alpha_full;  /* (d*d, n) alpha[a][k] at row a*d + k       */
+  const double *balpha_row;  /* (d, m)   face alpha[a][k], a = face axis  */
+  const int32_t *bfid;       /* (m)      face id of each boundary entry   */
+  const int32_t *finfo;      /* (nfaces, 8): offset, m, dim0, dim1,
+                                tangential-terms active, axis, side, 0    */
+  int32_t nfaces;
+  int32_t has_cross;         /* cell cross terms active                   */
 } pf_plan_desc;
 
 typedef struct pf_plan pf_plan;
@@ -270,6 +279,37 @@ PF_API int pf_adj_momentum_rhs(const pf_plan *plan, const double *cot_rhs,
 PF_API int pf_adj_assemble_momentum(const pf_plan *plan, const double *dc,
                              double nu, double *du_n, double *dnu_dev,
                              void *workspace, void *stream);
+
+/* ---- non-orthogonal grids (plans built with alpha_full) ------------------- */
+
+/* rhs += momentum_cross_rhs(u_cross, nu), S/piso.py:322-342 (lagged viscous
+ * cross fluxes divided by J; the tangential boundary flux of
+ * S/piso.py:375-392 is part of pf_momentum_rhs on such plans) */
+PF_API int pf_momentum_cross_rhs(const pf_plan *plan, const double *u,
+                                 double nu, double *rhs_inout,
+                                 void *workspace, void *stream);
+/* b_out = b0 - pressure_cross_rhs(A^-1, p_prev), S/piso.py:431-449, 617 */
+PF_API int pf_pressure_cross_rhs(const pf_plan *plan, const double *c,
+                                 const double *p_prev, const double *b0,
+                                 double *b_out, void *workspace, void *stream);
+/* _adj_pressure_cross, S/adjoint.py:156-178, for the cotangent
+ * cot_scale * cot_out: dA += ..., dp_prev = ... */
+PF_API int pf_adj_pressure_cross(const pf_plan *plan, const double *c,
+                                 const double *p_prev, const double *cot_out,
+                                 double cot_scale, double *da,
+                                 double *dp_prev, void *workspace,
+                                 void *stream);
+/* _adj_momentum_cross, S/adjoint.py:181-205: du_cross (+)= ..., *dnu_dev +=
+ * ... */
+PF_API int pf_adj_momentum_cross(const pf_plan *plan, const double *u,
+                                 double nu, const double *cot_out,
+                                 double *du_cross, int32_t accumulate,
+                                 double *dnu_dev, void *workspace,
+                                 void *stream);
+
+/* y += alpha x over len entries (device vectors) */
+PF_API int pf_axpy(const pf_plan *plan, double alpha, const double *x,
+                   double *y, int64_t len, void *stream);
 
 /* ---- boundary preprocessing (S/piso.py:467-509) --------------------------- */
 

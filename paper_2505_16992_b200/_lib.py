@@ -33,6 +33,8 @@ class PlanDesc(ctypes.Structure):
         ("jac", c_ptr), ("tmat", c_ptr), ("alpha_diag", c_ptr),
         ("m", c_i64), ("bcell", c_ptr), ("bface", c_ptr), ("bjac", c_ptr),
         ("bt", c_ptr), ("balpha", c_ptr),
+        ("alpha_full", c_ptr), ("balpha_row", c_ptr), ("bfid", c_ptr),
+        ("finfo", c_ptr), ("nfaces", c_int), ("has_cross", c_int),
     ]
 
 
@@ -83,6 +85,14 @@ _SIGS = {
                             c_ptr, c_ptr, c_ptr],
     "pf_adj_assemble_momentum": [c_ptr, c_ptr, c_dbl, c_ptr, c_ptr, c_ptr,
                                  c_ptr],
+    "pf_momentum_cross_rhs": [c_ptr, c_ptr, c_dbl, c_ptr, c_ptr, c_ptr],
+    "pf_pressure_cross_rhs": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
+                              c_ptr],
+    "pf_adj_pressure_cross": [c_ptr, c_ptr, c_ptr, c_ptr, c_dbl, c_ptr,
+                              c_ptr, c_ptr, c_ptr],
+    "pf_adj_momentum_cross": [c_ptr, c_ptr, c_dbl, c_ptr, c_ptr, c_int,
+                              c_ptr, c_ptr, c_ptr],
+    "pf_axpy": [c_ptr, c_dbl, c_ptr, c_ptr, c_i64, c_ptr],
     "pf_advective_outflow_update": [c_ptr, c_ptr, c_ptr, c_dbl, c_ptr,
                                     ctypes.POINTER(c_dbl), c_ptr],
     "pf_reduce_sum": [c_ptr, c_ptr, c_i64, c_ptr, ctypes.POINTER(c_dbl),

@@ -117,10 +117,12 @@ def backward_step(domain, tape, cot, path=GradientPath.FULL, tol=None,
                   _lib.ptr(cp_out if m == n_corr - 1 else None),
                   _lib.ptr(plan.workspace), hs)
         g_h = cu                     # dh = cu; the divergence adjoint adds
-        # only the last outer iterate carries a cotangent on orthogonal grids
-        # (the lagged-cross adjoint that would feed earlier ones is zero)
-        it = len(corr.p_iters) - 1
-        if path.pressure_solve:
+        n_it = len(corr.p_iters)
+        if path.pressure_solve and not plan.cell_cross:
+            # orthogonal grids: the lagged-cross adjoint that would feed the
+            # earlier outer iterates is identically zero, so only the last
+            # iterate carries a cotangent
+            it = n_it - 1
             y, rep = cg_solve(plan, K, cot_p, tol=tol, maxiter=maxiter,
                               zero_mean=True, stage="adjoint_pressure")
             reports.append(rep)
@@ -130,6 +132,31 @@ def backward_step(domain, tape, cot, path=GradientPath.FULL, tol=None,
             # forward solved (-P) p = proj(-b): db = -y
             _lib.call("pf_adj_divergence_rhs", plan.handle, _lib.ptr(y),
                       -1.0, _lib.ptr(g_h), _lib.ptr(dbc), hs)
+        elif path.pressure_solve:
+            # S/adjoint.py:456-470: reversed outer iterates, each adjoint
+            # solve feeding the previous iterate through the cross flux
+            cot_b0 = torch.zeros(n, dtype=F64, device=dev)
+            cp_it = cot_p
+            for it in reversed(range(n_it)):
+                y, rep = cg_solve(plan, K, cp_it, tol=tol, maxiter=maxiter,
+                                  zero_mean=True, stage="adjoint_pressure")
+                if rep.iterations or rep.residual:
+                    reports.append(rep)
+                _lib.call("pf_bwd_pressure_outer", plan.handle, _lib.ptr(y),
+                          _lib.ptr(corr.p_iters[it]), _lib.ptr(dKf), hs)
+                _lib.call("pf_axpy", plan.handle, -1.0, _lib.ptr(y),
+                          _lib.ptr(cot_b0), n, hs)
+                if it > 0:
+                    nxt = torch.empty(n, dtype=F64, device=dev)
+                    # cot of the cross flux = -db = y
+                    _lib.call("pf_adj_pressure_cross", plan.handle,
+                              _lib.ptr(C), _lib.ptr(corr.p_iters[it - 1]),
+                              _lib.ptr(y), 1.0, _lib.ptr(dA), _lib.ptr(nxt),
+                              _lib.ptr(plan.workspace), hs)
+                    cp_it = nxt
+            pressure_done = True
+            _lib.call("pf_adj_divergence_rhs", plan.handle, _lib.ptr(cot_b0),
+                      1.0, _lib.ptr(g_h), _lib.ptr(dbc), hs)
         _lib.call("pf_bwd_h_stage", plan.handle, _lib.ptr(C), _lib.ptr(g_h),
                   _lib.ptr(soa(corr.h, n, d, dev)),
                   _lib.ptr(soa(corr.u_hin, n, d, dev)), _lib.ptr(dA),
@@ -141,32 +168,57 @@ def backward_step(domain, tape, cot, path=GradientPath.FULL, tol=None,
         _lib.call("pf_bwd_pressure_matrix", plan.handle, _lib.ptr(C),
                   _lib.ptr(dKf), _lib.ptr(dA), hs)
 
-    # predictor (S/adjoint.py:343-405); only the last outer iterate is fed
-    grhs = g_rhs
-    if path.advection_solve:
-        y, reps = bicgstab_solve(plan, C, cu, tol=tol, maxiter=maxiter,
-                                 transpose=True,
-                                 stages=[f"adjoint_momentum[{c}]"
-                                         for c in range(d)])
-        reports.extend(reps)
-        u_star = soa(tape.mom_iters[-1], n, d, dev)
-        _lib.call("pf_bwd_momentum_outer", plan.handle, _lib.ptr(y),
-                  _lib.ptr(u_star), _lib.ptr(dC), hs)
-        grhs = y.add_(g_rhs)
+    # predictor (S/adjoint.py:343-405)
     du_n = torch.zeros((d, n), dtype=F64, device=dev)
     bcd = getattr(tape, "_bc_dm", None)
     if bcd is None and plan.m:
         from .piso import bc_soa
         bcd = bc_soa(plan, tape.bc, d)
-    _lib.call("pf_adj_momentum_rhs", plan.handle, _lib.ptr(grhs),
-              _lib.ptr(bcd), float(tape.nu), float(tape.dt), _lib.ptr(du_n),
-              _lib.ptr(dbc), _lib.ptr(dnu), _lib.ptr(plan.workspace), hs)
+    n_outer = len(tape.mom_iters)
+    stages = [f"adjoint_momentum[{c}]" for c in range(d)]
+    # on orthogonal grids the cross-flux adjoint feeding earlier outer
+    # iterates vanishes: only the last iterate carries a cotangent
+    its = range(n_outer - 1, -1, -1) if plan.cell_cross else [n_outer - 1]
+    dsource = None
+    cot_us = cu
+    for it in its:
+        grhs = torch.zeros((d, n), dtype=F64, device=dev)
+        if path.advection_solve:
+            y, reps = bicgstab_solve(plan, C, cot_us, tol=tol,
+                                     maxiter=maxiter, transpose=True,
+                                     stages=stages)
+            reports.extend(r for r in reps if r.iterations or r.residual)
+            u_star = soa(tape.mom_iters[it], n, d, dev)
+            _lib.call("pf_bwd_momentum_outer", plan.handle, _lib.ptr(y),
+                      _lib.ptr(u_star), _lib.ptr(dC), hs)
+            grhs = y
+        if it == n_outer - 1:
+            grhs.add_(g_rhs)
+        _lib.call("pf_adj_momentum_rhs", plan.handle, _lib.ptr(grhs),
+                  _lib.ptr(bcd), float(tape.nu), float(tape.dt),
+                  _lib.ptr(du_n), _lib.ptr(dbc), _lib.ptr(dnu),
+                  _lib.ptr(plan.workspace), hs)
+        dsource = grhs if dsource is None else dsource.add_(grhs)
+        if plan.cell_cross:
+            u_in = soa(tape.mom_inputs[it], n, d, dev)
+            if it == 0:
+                _lib.call("pf_adj_momentum_cross", plan.handle,
+                          _lib.ptr(u_in), float(tape.nu), _lib.ptr(grhs),
+                          _lib.ptr(du_n), 1, _lib.ptr(dnu),
+                          _lib.ptr(plan.workspace), hs)
+            else:
+                nxt = torch.empty((d, n), dtype=F64, device=dev)
+                _lib.call("pf_adj_momentum_cross", plan.handle,
+                          _lib.ptr(u_in), float(tape.nu), _lib.ptr(grhs),
+                          _lib.ptr(nxt), 0, _lib.ptr(dnu),
+                          _lib.ptr(plan.workspace), hs)
+                cot_us = nxt
     _lib.call("pf_adj_assemble_momentum", plan.handle, _lib.ptr(dC),
               float(tape.nu), _lib.ptr(du_n), _lib.ptr(dnu),
               _lib.ptr(plan.workspace), hs)
     iters = sum(r.iterations for r in reports)
     return GradState(u=du_n.t(), p=torch.zeros(n, dtype=F64, device=dev),
-                     nu=float(dnu.item()), source=grhs.t(),
+                     nu=float(dnu.item()), source=dsource.t(),
                      bc=bc_views(plan, dbc), solve_iterations=iters)
 
 

@@ -329,6 +329,41 @@ __global__ void __launch_bounds__(kBlock)
 #pragma unroll
     for (int k = 0; k < D; ++k)
       dbc[k * m + e] += cr[k] * coef + (cot_uflux * fj) * tr[k];
+    if (kind == PF_BKIND_DIRICHLET && v.finfo) {
+      const FaceGeo g = face_geo(v, e);
+      if (g.active) {
+        // _adj_boundary_cross (S/adjoint.py:215-233)
+        double term[D];
+        bcross_term(v, g, e, bc, term);
+        const double sc = nsgn * nu / v.J(i);
+        double dot = 0.0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) dot += cr[c] * (term[c] * sc);
+        acc[0] += dot / nu;
+        // face_grad_adjoint of fa * cot_pre along each tangential axis
+        auto val = [&](int32_t e2, int q, int c) {
+          const int32_t i2 = __ldg(v.bcell + e2);
+          const double fa = __ldg(v.balpha_row +
+                                  (int64_t)tang_axis(g.axis, q) * m + e2);
+          return fa * (cot[c * n + i2] * (nsgn * nu / v.J(i2)));
+        };
+        for (int q = 0; q < g.ndim; ++q) {
+          const int L = g.dims[q], j = g.j[q], st = g.st[q];
+          if (L < 2) continue;
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            double o = 0.0;
+            if (j - 1 >= 0) o += (j - 1 == 0) ? val(e - st, q, c)
+                                              : 0.5 * val(e - st, q, c);
+            if (j + 1 <= L - 1) o -= (j + 1 == L - 1) ? val(e + st, q, c)
+                                                      : 0.5 * val(e + st, q, c);
+            if (j == 0) o -= val(e, q, c);
+            if (j == L - 1) o += val(e, q, c);
+            dbc[c * m + e] += o;
+          }
+        }
+      }
+    }
   }
   double tot[1];
   if (grid_reduce<1>(acc, partials, counter, tot)) *dnu += tot[0];

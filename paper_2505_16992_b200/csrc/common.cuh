@@ -202,7 +202,16 @@ struct View {
   const double *__restrict__ bjac;
   const double *__restrict__ bt;  // (D, m)
   const double *__restrict__ balpha;
+  // non-orthogonal grids only
+  const double *__restrict__ alpha_full;  // (D*D, n)
+  const double *__restrict__ balpha_row;  // (D, m) face alpha[a][k]
+  const int32_t *__restrict__ bfid;       // (m) face id
+  const int32_t *__restrict__ finfo;      // (nfaces, 8)
+  int32_t has_cross;
 
+  __device__ __forceinline__ double AF(int a, int k, int32_t i) const {
+    return __ldg(alpha_full + (int64_t)(a * D + k) * n + i);
+  }
   __device__ __forceinline__ double T(int a, int j, int32_t i) const {
     return __ldg(tmat + (int64_t)(a * D + j) * n + i);
   }
@@ -245,7 +254,83 @@ View<D, Topo> make_view(const Plan &p, const Topo &topo) {
   v.bjac = p.d.bjac;
   v.bt = p.d.bt;
   v.balpha = p.d.balpha;
+  v.alpha_full = p.d.alpha_full;
+  v.balpha_row = p.d.balpha_row;
+  v.bfid = p.d.bfid;
+  v.finfo = p.d.finfo;
+  v.has_cross = p.d.has_cross;
   return v;
+}
+
+// ---------------------------------------------------------------------------
+// tangential-derivative viscous flux through a prescribed face
+// (_boundary_cross_term, S/piso.py:375-392) and its adjoint
+// (_adj_boundary_cross, S/adjoint.py:215-233).  A face is an area_shape grid
+// of boundary entries in C order; face_grad is central inside and one-sided
+// at the ends (S/piso.py:134-159).
+
+struct FaceGeo {
+  int32_t off, ndim, dims[2], st[2], j[2], active, axis;
+};
+
+template <class V>
+__device__ __forceinline__ FaceGeo face_geo(const V &v, int32_t e) {
+  FaceGeo g;
+  const int32_t *fi = v.finfo + 8 * __ldg(v.bfid + e);
+  g.off = fi[0];
+  g.ndim = V::kDim - 1;
+  g.dims[0] = fi[2];
+  g.dims[1] = fi[3];
+  g.active = fi[4];
+  g.axis = fi[5];
+  const int32_t l = e - g.off;
+  if (V::kDim == 3) {
+    g.j[0] = l / g.dims[1];
+    g.j[1] = l % g.dims[1];
+    g.st[0] = g.dims[1];
+    g.st[1] = 1;
+  } else {
+    g.j[0] = l;
+    g.j[1] = 0;
+    g.st[0] = 1;
+    g.st[1] = 0;
+  }
+  return g;
+}
+
+// k-th tangential axis (the q-th axis other than the face axis)
+__device__ __forceinline__ int tang_axis(int axis, int q) {
+  return q < axis ? q : q + 1;
+}
+
+// term[c] of the boundary cross flux at entry e (before the N nu / J scale)
+template <class V>
+__device__ __forceinline__ void bcross_term(const V &v, const FaceGeo &g,
+                                            int32_t e,
+                                            const double *__restrict__ bc,
+                                            double (&term)[V::kDim]) {
+  constexpr int D = V::kDim;
+#pragma unroll
+  for (int c = 0; c < D; ++c) term[c] = 0.0;
+  for (int q = 0; q < g.ndim; ++q) {
+    const int L = g.dims[q], j = g.j[q], st = g.st[q];
+    const double fa = __ldg(v.balpha_row + (int64_t)tang_axis(g.axis, q) *
+                                               v.m + e);
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const double *b = bc + (int64_t)c * v.m;
+      double dub;
+      if (L == 1)
+        dub = 0.0;
+      else if (j == 0)
+        dub = b[e + st] - b[e];
+      else if (j == L - 1)
+        dub = b[e] - b[e - st];
+      else
+        dub = 0.5 * (b[e + st] - b[e - st]);
+      term[c] += fa * dub;
+    }
+  }
 }
 
 template <int D>

@@ -90,12 +90,23 @@ __global__ void __launch_bounds__(kBlock)
     const double nsgn = (f & 1) ? 1.0 : -1.0;
     const double uflux = v.bflux(bc, e);
     double w;
-    if ((__ldg(v.bface + e) >> 4) == PF_BKIND_DIRICHLET)
+    const bool dirichlet = (__ldg(v.bface + e) >> 4) == PF_BKIND_DIRICHLET;
+    if (dirichlet)
       w = (2.0 * nu * __ldg(v.balpha + e) - uflux * nsgn) * invj;
     else
       w = -uflux * nsgn * invj;
 #pragma unroll
     for (int c = 0; c < D; ++c) r[c] += bc[(int64_t)c * v.m + e] * w;
+    if (dirichlet && v.finfo) {
+      const FaceGeo g = face_geo(v, e);
+      if (g.active) {
+        double term[D];
+        bcross_term(v, g, e, bc, term);
+        const double sc = nsgn * nu / v.J(i);
+#pragma unroll
+        for (int c = 0; c < D; ++c) r[c] += term[c] * sc;
+      }
+    }
   }
 #pragma unroll
   for (int c = 0; c < D; ++c) rhs[c * n + i] = r[c];

@@ -345,10 +345,6 @@ def piso_step(domain, state, cfg, workspace=None, tape=None):
                           state.t, state.step)
     dev = state.u.device
     _lib.require_cuda(dev)
-    if domain.has_cross_terms():
-        raise NotImplementedError(
-            "non-orthogonal grids (lagged cross fluxes, S/piso.py:322-353, "
-            "431-449) are not implemented on the device path")
     plan = domain.device_plan(dev)
     n, d = domain.n, domain.dim
     hstream = plan.stream
@@ -371,17 +367,20 @@ def piso_step(domain, state, cfg, workspace=None, tape=None):
               _lib.ptr(flux), _lib.ptr(c_data), hstream)
 
     n_outer = 1 + int(cfg.nonortho_correctors)
-    rhs = torch.empty((d, n), dtype=F64, device=dev)
     mom_inputs, mom_iters = [], []
     u_prev = u_n
     u_star = None
     stages = [f"momentum[{c}]" for c in range(d)]
     for _ in range(n_outer):
-        # the lagged cross flux is identically zero on orthogonal grids, so
-        # every outer iteration sees the same right-hand side and warm start
+        # rhs = u_n/dt + S + boundary terms (+ the lagged cross flux of the
+        # previous outer iterate on non-orthogonal grids, S/piso.py:582)
+        rhs = torch.empty((d, n), dtype=F64, device=dev)
         _lib.call("pf_momentum_rhs", plan.handle, _lib.ptr(u_n),
                   _lib.ptr(bc), _lib.ptr(src), uniform, nu, dt,
                   _lib.ptr(rhs), hstream)
+        if plan.cell_cross:
+            _lib.call("pf_momentum_cross_rhs", plan.handle, _lib.ptr(u_prev),
+                      nu, _lib.ptr(rhs), _lib.ptr(plan.workspace), hstream)
         u_star, reps = bicgstab_solve(plan, c_data, rhs,
                                       x0=ws.warm(("mom",)), tol=cfg.tol,
                                       maxiter=cfg.maxiter, stages=stages)
@@ -410,7 +409,15 @@ def piso_step(domain, state, cfg, workspace=None, tape=None):
                   _lib.ptr(bc), _lib.ptr(flux), _lib.ptr(b0), hstream)
         p_iters = []
         for it in range(n_outer):
-            p_sol, rep = cg_solve(plan, k_data, b0, x0=ws.warm(("prs",)),
+            b = b0
+            if plan.cell_cross and it > 0:
+                # b = b0 - lagged pressure cross flux (S/piso.py:617)
+                b = torch.empty(n, dtype=F64, device=dev)
+                _lib.call("pf_pressure_cross_rhs", plan.handle,
+                          _lib.ptr(c_data), _lib.ptr(p_iters[-1]),
+                          _lib.ptr(b0), _lib.ptr(b), _lib.ptr(plan.workspace),
+                          hstream)
+            p_sol, rep = cg_solve(plan, k_data, b, x0=ws.warm(("prs",)),
                                   tol=cfg.tol, maxiter=cfg.maxiter,
                                   zero_mean=True, b_scale=-1.0,
                                   stage=f"pressure[c{m}i{it}]")

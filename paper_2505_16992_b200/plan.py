@@ -88,6 +88,29 @@ class DevicePlan:
             self.bcell = self.bface = self.bjac = self.bt = self.balpha = None
         self.has_outflow = any(f.kind == "advective_outflow" for f in faces)
 
+        # --- non-orthogonal metric terms ---------------------------------------
+        self.cell_cross = domain.cell_cross_terms()
+        face_active = [domain.face_cross_active(f) for f in faces]
+        self.nonortho = self.cell_cross or any(face_active)
+        self.alpha_full = self.balpha_row = self.bfid = self.finfo = None
+        if self.nonortho:
+            af = np.ascontiguousarray(domain.alpha.reshape(n, d * d).T)
+            self.alpha_full = torch.as_tensor(af, **f64)
+            if m:
+                row = np.concatenate([f.face_alpha[:, f.axis, :]
+                                      for f in faces]).T
+                self.balpha_row = torch.as_tensor(np.ascontiguousarray(row),
+                                                  **f64)
+                self.bfid = torch.as_tensor(np.concatenate(
+                    [np.full(f.m, k, np.int32) for k, f in enumerate(faces)]),
+                    **i32)
+                info = np.zeros((len(faces), 8), np.int32)
+                for k, (f, off) in enumerate(zip(faces, self.face_offsets)):
+                    dims = list(f.area_shape) + [1, 1]
+                    info[k] = [off, f.m, dims[0], dims[1], int(face_active[k]),
+                               f.axis, f.side, 0]
+                self.finfo = torch.as_tensor(info.reshape(-1), **i32)
+
         # --- topology ----------------------------------------------------------
         desc = _lib.PlanDesc()
         desc.dim = d
@@ -120,6 +143,14 @@ class DevicePlan:
             desc.bjac = self.bjac.data_ptr()
             desc.bt = self.bt.data_ptr()
             desc.balpha = self.balpha.data_ptr()
+        if self.nonortho:
+            desc.alpha_full = self.alpha_full.data_ptr()
+            desc.has_cross = int(self.cell_cross)
+            if m:
+                desc.balpha_row = self.balpha_row.data_ptr()
+                desc.bfid = self.bfid.data_ptr()
+                desc.finfo = self.finfo.data_ptr()
+                desc.nfaces = len(faces)
         self._desc = desc
         handle = ctypes.c_void_p()
         with torch.cuda.device(device):

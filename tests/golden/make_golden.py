@@ -35,6 +35,9 @@ sys.path.insert(0, build_ref.ref_path())
 from pisoflow import adjoint, mesh, piso  # noqa: E402
 from pisoflow.kernels import LANE  # noqa: E402
 
+sys.path.insert(0, os.path.dirname(HERE))
+from golden_cases import sheared3d  # noqa: E402
+
 TOL = 1e-13
 
 
@@ -86,6 +89,10 @@ def cases():
     out.append(("distorted_nonortho", dom,
                 dict(dt=0.07, nu=0.2, nonortho_correctors=1),
                 rand((dom.n, 2), 0.3), None, 2))
+    dom = sheared3d(mesh)
+    out.append(("sheared3d", dom,
+                dict(dt=0.05, nu=0.1, nonortho_correctors=2),
+                rand((dom.n, 3), 0.2), rand((dom.n, 3), 0.1), 2))
     return out, rng
 
 

@@ -11,7 +11,8 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 ORTHOGONAL = ["cavity8", "box3d", "channel", "twoblock_rot", "backstep",
               "obstacle", "refined_cavity"]
-ALL = ORTHOGONAL + ["distorted_nonortho"]
+NONORTHO = ["distorted_nonortho", "sheared3d"]
+ALL = ORTHOGONAL + NONORTHO
 
 
 def build(name):
@@ -36,6 +37,8 @@ def build(name):
         return mesh.Domain([blk], bnd)
     if name == "distorted_nonortho":
         return mesh.make_poiseuille((6, 4), distort=0.35)
+    if name == "sheared3d":
+        return sheared3d(mesh)
     raise KeyError(name)
 
 
@@ -58,3 +61,26 @@ def rel(a, b):
     b = np.asarray(b, dtype=np.float64)
     scale = max(np.abs(b).max() if b.size else 0.0, 1e-300)
     return float(np.abs(a - b).max() / scale) if a.size else 0.0
+
+
+def sheared3d(mesh):
+    """Non-orthogonal 3D block: periodic in x and z (faces conformal up to a
+    rigid shift), walls at y = 0 / 1 with a moving lid; the walls are not
+    plane so their face metrics carry tangential terms."""
+    x = np.linspace(0.0, 1.0, 5)
+    y = np.linspace(0.0, 1.0, 6)
+    z = np.linspace(0.0, 1.0, 5)
+    X, Y, Z = np.meshgrid(x, y, z, indexing="ij")
+    Xp = X + 0.08 * np.sin(2 * np.pi * Y) * np.cos(2 * np.pi * Z)
+    Yp = Y + 0.05 * np.sin(np.pi * Y) * np.cos(2 * np.pi * X)
+    Zp = Z + 0.08 * np.sin(2 * np.pi * X) * np.sin(np.pi * Y)
+    blk = mesh.BlockSpec(np.stack([Xp, Yp, Zp], axis=-1))
+    ident = (0, 1, 2)
+    flip = (False, False, False)
+    bnd = {(0, 0, 0): mesh.Connection(0, 0, 1, ident, flip),
+           (0, 0, 1): mesh.Connection(0, 0, 0, ident, flip),
+           (0, 2, 0): mesh.Connection(0, 2, 1, ident, flip),
+           (0, 2, 1): mesh.Connection(0, 2, 0, ident, flip),
+           (0, 1, 0): mesh.Dirichlet(0.0),
+           (0, 1, 1): mesh.Dirichlet((0.5, 0.0, 0.2))}
+    return mesh.Domain([blk], bnd)

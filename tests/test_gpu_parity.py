@@ -28,6 +28,7 @@ def _gpu_rollout(name, tol=GPU_TOL):
         b.copy_(torch.as_tensor(ref, device=dev))
     cfg = piso.StepConfig(dt=float(g["dt"]), nu=float(g["nu"]),
                           n_correctors=int(g["n_correctors"]),
+                          nonortho_correctors=int(g["nonortho"]),
                           source=G.source_of(g), tol=tol)
     ws = piso.PisoWorkspace(dom)
     tapes, outs = [], []
@@ -39,7 +40,7 @@ def _gpu_rollout(name, tol=GPU_TOL):
     return g, dom, tapes, outs
 
 
-@pytest.mark.parametrize("name", G.ORTHOGONAL)
+@pytest.mark.parametrize("name", G.ALL)
 def test_forward_matches_reference(name):
     g, dom, tapes, outs = _gpu_rollout(name)
     for k, (st, diag) in enumerate(outs):
@@ -64,7 +65,7 @@ def test_forward_matches_reference(name):
         assert diag.pressure_iterations > 0
 
 
-@pytest.mark.parametrize("name", G.ORTHOGONAL)
+@pytest.mark.parametrize("name", G.ALL)
 @pytest.mark.parametrize("path", ["full", "adv_only", "p_only", "none"])
 def test_backward_matches_reference(name, path):
     from paper_2505_16992_b200 import adjoint
@@ -266,12 +267,11 @@ def test_zero_rhs_returns_zero():
     assert float(x.abs().max()) == 0.0
 
 
-def test_nonorthogonal_grid_is_rejected_loudly():
-    from paper_2505_16992_b200 import piso
+def test_nonorthogonal_plan_carries_cross_terms():
     dom = G.build("distorted_nonortho")
-    st = piso.make_state(dom, device="cuda:0")
-    with pytest.raises(NotImplementedError):
-        piso.piso_step(dom, st, piso.StepConfig(dt=0.1, nu=0.1))
+    plan = dom.device_plan("cuda:0")
+    assert plan.nonortho and plan.cell_cross
+    assert plan.alpha_full is not None and plan.finfo is not None
 
 
 def test_step_validates_dt_nu():
