@@ -1,0 +1,110 @@
+"""Learned-SGS channel LES training step (BASELINE config 5).
+
+The paper trains a CNN corrector S_theta(u) as a body force inside the PISO
+step (the reference's hook is ``StepConfig.source``,
+S/piso.py:50, with cotangent ``GradState.source``, S/adjoint.py:57).  One
+training step here is:
+
+1. a k-step unrolled rollout of the differentiable PISO step
+   (:func:`~paper_2505_16992_b200.autograd.piso_step_fn`) on one
+   64 x 48 x 64 channel sample per process, with source = wall forcing +
+   S_theta(u);
+2. a loss on the rollout (mean streamwise profile against a target, summed
+   over the unrolled frames);
+3. ``loss.backward()`` -- the discrete adjoint through every step, then the
+   CNN's own backward;
+4. data-parallel gradient averaging across processes (one sample per GPU;
+   the only collective of the path, SURVEY.md §8 e).
+
+The CNN itself is an ordinary torch module (cuDNN convolutions); the PISO
+step and its adjoint run in libpisob200.so.
+"""
+
+import torch
+import torch.distributed as dist
+
+from . import autograd as _ag
+
+
+class SGSCorrector(torch.nn.Module):
+    """Small 3D CNN mapping the velocity (n, 3) of a box grid to a body force
+    (n, 3): periodic padding along the periodic axes, replicate along the
+    walls."""
+
+    def __init__(self, shape, periodic, width=8, scale=1e-3):
+        super().__init__()
+        self.shape = tuple(shape)
+        self.periodic = tuple(periodic)
+        self.scale = scale
+        self.c1 = torch.nn.Conv3d(3, width, 3, dtype=torch.float64)
+        self.c2 = torch.nn.Conv3d(width, 3, 1, dtype=torch.float64)
+
+    def _pad(self, x):
+        out = x
+        for ax in range(3):
+            dim = 2 + ax
+            if self.periodic[ax]:
+                out = torch.cat([out.narrow(dim, out.shape[dim] - 1, 1), out,
+                                 out.narrow(dim, 0, 1)], dim=dim)
+            else:
+                out = torch.cat([out.narrow(dim, 0, 1), out,
+                                 out.narrow(dim, out.shape[dim] - 1, 1)],
+                                dim=dim)
+        return out
+
+    def forward(self, u):
+        x = u.t().reshape(1, 3, *self.shape)
+        y = self.c2(torch.nn.functional.gelu(self.c1(self._pad(x))))
+        return self.scale * y.reshape(3, -1).t()
+
+
+def unrolled_loss(domain, u0, bc, model, forcing, nu, cfg, steps,
+                  target_profile, step_fn=None):
+    """Differentiable k-step rollout and its loss.  ``step_fn`` defaults to
+    the PISO step (tests inject a CPU stand-in to exercise the host logic).
+    Returns (loss, final velocity)."""
+    step_fn = step_fn or (lambda u, src: _ag.piso_step_fn(domain, u, src, nu,
+                                                          bc, cfg)[0])
+    shape = model.shape
+    u = u0
+    loss = u0.new_zeros(())
+    for _ in range(steps):
+        src = forcing(u.detach(), nu) + model(u)
+        u = step_fn(u, src)
+        prof = u[:, 0].reshape(shape).mean(dim=(0, 2))
+        loss = loss + ((prof - target_profile) ** 2).mean()
+    return loss / steps, u
+
+
+def average_gradients(model):
+    """All-reduce-mean the parameter gradients over the default process
+    group (the data-parallel collective of config 5)."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return
+    world = dist.get_world_size()
+    if world == 1:
+        return
+    grads = [p.grad for p in model.parameters() if p.grad is not None]
+    flat = torch.cat([g.reshape(-1) for g in grads])
+    dist.all_reduce(flat)
+    flat /= world
+    off = 0
+    for g in grads:
+        g.copy_(flat[off:off + g.numel()].reshape(g.shape))
+        off += g.numel()
+
+
+def train_step(domain, u0, bc, model, opt, forcing, nu, cfg, steps,
+               target_profile, step_fn=None):
+    """One data-parallel training step; returns the (local) loss value."""
+    opt.zero_grad(set_to_none=True)
+    loss, _ = unrolled_loss(domain, u0, bc, model, forcing, nu, cfg, steps,
+                            target_profile, step_fn)
+    loss.backward()
+    average_gradients(model)
+    opt.step()
+    return float(loss.detach())
+
+
+__all__ = ["SGSCorrector", "unrolled_loss", "average_gradients",
+           "train_step"]
