@@ -243,11 +243,13 @@ KERNEL_BYTES = {
     "k_cg_spmv_faces": 40,        # 3 face weights + p + q
     "k_cg_spmv": 40,              # survey SpMV_P minimum (stencil form moves 72)
     "k_cg_update": 48,            # x, p, r, q read; x, r written
-    "k_mg_smooth0 (level 0)": 40,  # r, 1/den, w_y, c' read; x written
-    "k_mg_resid_restrict (level 0)": 41,   # r, x, 3 faces; 1/8 coarse r
-    "k_mg_prolong_resid (level 0)": 49,    # r, x, 3 faces, 1/8 coarse x; res
-    "k_mg_smooth2 (level 0)": 49,  # res, 1/den, w_y, c', x, 1/8 coarse; x
-    "k_cg_zsum": 16,              # r, z
+    # damped block-Jacobi Y-line smoother (Thomas factors precomputed)
+    "k_mg_smooth0 (level 0)": 40,         # r, 1/den, w_y, c' read; x written
+    "k_mg_resid_restrict (level 0)": 41,  # r, x, 3 faces; 1/8 coarse r
+    "k_mg_prolong_resid (level 0)": 49,   # r, x, 3 faces, 1/8 coarse x; res
+    # final pass with the CG z-sums fused: res, 1/den, w_y, c', r, x r+w,
+    # 1/8 coarse x
+    "k_mg_smooth2_cg (level 0)": 57,
     "k_cg_pupdate": 24,           # z, p read; p written
 }
 
@@ -268,14 +270,16 @@ def measure_roofline(args, dom, plan, state, nu, dt, dev):
     mg = plan.has_mg
     if mg:
         plan.mg_prepare(k)
-    ms = (ctypes.c_double * 10)()
+    ms = (ctypes.c_double * 11)()
     _lib.call("pf_cg_profile", plan.handle, _lib.ptr(k), _lib.ptr(b),
               args.profile_iters, 2 if mg else 1, _lib.ptr(plan.workspace),
               _lib.ptr(plan.mg_workspace if mg else None), ms, plan.stream)
     names = (["k_cg_spmv_faces" if mg else "k_cg_spmv", "k_cg_update"]
-             + (["k_mg_smooth0 (level 0)", "k_mg_resid_restrict (level 0)",
+             + (["k_mg_smooth0 (level 0)",
+                 "k_mg_resid_restrict (level 0)",
                  "mg coarse levels", "k_mg_prolong_resid (level 0)",
-                 "k_mg_smooth2 (level 0)", "k_cg_zsum"] if mg else
+                 "k_mg_smooth2_cg (level 0)", "zsum (fused into smooth2)"]
+                if mg else
                 [None] * 6) + ["k_cg_pupdate"])
     idx = [0, 1, 2, 3, 4, 5, 6, 7, 8]
     per = {}
@@ -309,7 +313,8 @@ def measure_roofline(args, dom, plan, state, nu, dt, dev):
             "cells_per_launch": n, "ms_per_launch": cand[top],
             "pressure_cg_iteration": {
                 "preconditioner": "multigrid" if mg else "jacobi",
-                "ms": it_ms, "level0_and_cg_ms": fine_ms,
+                "ms": it_ms, "ms_graph_replay": float(ms[10]),
+                "level0_and_cg_ms": fine_ms,
                 "level0_and_cg_bytes_per_cell": it_bytes,
                 "level0_and_cg_achieved_gbs":
                     it_bytes * n / (fine_ms * 1e-3) / 1e9,

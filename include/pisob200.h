@@ -221,7 +221,8 @@ PF_API int pf_bicgstab_solve(const pf_plan *plan, const double *a, int32_t trans
  *   [2..6] multigrid level 0: line smooth | residual+restrict | all coarse
  *          levels | prolong+residual | line smooth with correction
  *          (precond == PF_PRECOND_MG; zero otherwise)
- *   [7] z sums   [8] direction update   [9] whole iteration.
+ *   [7] z sums   [8] direction update   [9] whole iteration
+ *   [10] whole iteration replayed from the cached CUDA graph (MG only).
  * Used by bench.py for the roofline figure. */
 PF_API int pf_cg_profile(const pf_plan *plan, const double *a,
                          const double *b, int32_t iters, int32_t precond,

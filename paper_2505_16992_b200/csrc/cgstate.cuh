@@ -1,0 +1,60 @@
+// cgstate.cuh -- device-resident Krylov state shared by the solver kernels
+// and the multigrid kernels that fuse the CG z-sums into their last pass.
+#pragma once
+
+#include "common.cuh"
+
+namespace pf {
+
+struct CompState {
+  double bnorm, tol_abs, res, rho, rho_new, alpha, omega, beta;
+  double zbar, rz, xmean, true_res, bmean, rmean, tol, pad1;
+  int32_t iter, maxiter, done, converged, fail, zero_rhs, pending, active;
+  int32_t project_x, pad2[7];
+};
+
+struct SolverState {
+  CompState c[3];
+  int32_t all_done, ncomp, precond, zero_mean;
+  int32_t pad[12];
+};
+
+static_assert(sizeof(SolverState) <= 8 * kWsSolver, "solver state too big");
+
+__device__ __forceinline__ bool finite(double x) { return isfinite(x); }
+
+// z-bar, r.z and beta from the sums (sum z, sum r.z, sum r); `initial`
+// seeds rz for the first direction (S/linalg.py:146-149 / 162-168)
+__device__ __forceinline__ void cg_fin_z(SolverState *st, double sz,
+                                         double srz, double sr, int32_t n,
+                                         bool initial) {
+  CompState &c = st->c[0];
+  c.zbar = st->zero_mean ? sz / n : 0.0;
+  const double rz_new = srz - c.zbar * sr;
+  if (initial) {
+    c.rz = rz_new;
+    return;
+  }
+  if (!finite(rz_new) || c.rz == 0.0) {
+    c.fail = 1;
+    c.done = 1;
+    st->all_done = 1;
+    return;
+  }
+  c.beta = rz_new / c.rz;
+  c.rz = rz_new;
+  if (c.iter >= c.maxiter) {
+    c.done = 1;
+    st->all_done = 1;
+  }
+}
+
+// optional fusion of the CG z-sums into the multigrid's final pass
+struct CgFuse {
+  SolverState *st;  // null: no fusion
+  double *partials;
+  unsigned *counter;
+  int initial;
+};
+
+}  // namespace pf

@@ -60,7 +60,7 @@ struct MgHierarchy {
   int nlev;
   int ax_of[3];  // physical axis of canonical X, Y, Z (-1: absent)
   MgLevel lv[kMgMaxLevels];
-  double omega;
+  double omega;   // damping of the block-Jacobi line smoother
 };
 
 
@@ -402,7 +402,7 @@ __device__ __forceinline__ void warp_max(double (&v)[K]) {
 // Block-wide reduction; the result is valid in thread 0.
 template <int K, bool kMax = false>
 __device__ __forceinline__ void block_reduce(double (&v)[K]) {
-  __shared__ double sm[kBlock / 32][K];
+  __shared__ double sm[32][K];  // up to 1024 threads
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (kMax) warp_max<K>(v); else warp_sum<K>(v);
   if (lane == 0) {

@@ -3,11 +3,9 @@
 // Level layout: canonical (X, Y, Z) C-order, index ((x*sy)+y)*sz+z, so the
 // Y lines of the smoother are strided by sz and threads of a warp take
 // consecutive z -- every line-solve load is coalesced across the warp.
-// Each level coarsens X, Y, Z by 2 while the axis is even (Y while it stays
-// longer than 2); coarse face weights are sums of the fine faces crossing
-// the coarse face (Galerkin with piecewise-constant aggregation).
 #include <algorithm>
 
+#include "cgstate.cuh"
 #include "mg.cuh"
 
 namespace pf {
@@ -15,15 +13,23 @@ namespace pf {
 constexpr int kLineBlock = 128;
 constexpr int kChunk = 8;  // rows batched per load phase of a line sweep
 
+__device__ __forceinline__ int32_t lid(const MgLevel &L, int32_t x, int32_t y,
+                                       int32_t z) {
+  return (x * L.sy + y) * L.sz + z;
+}
+
+// parent (coarse) index; coarsening factors are 1 or 2: shifts, no division
 __device__ __forceinline__ int32_t parent(const MgLevel &F, const MgLevel &C,
                                           int32_t x, int32_t y, int32_t z) {
-  // coarsening factors are 1 or 2: shifts instead of integer division
   return ((x >> (F.fx - 1)) * C.sy + (y >> (F.fy - 1))) * C.sz +
          (z >> (F.fz - 1));
 }
 
 #define MG_DONE_RETURN \
   if (done && *done) return
+
+// ---------------------------------------------------------------------------
+// setup
 
 // level-0 face weights from the K stencil (row 1 + 2a + 1 holds -w)
 __global__ void __launch_bounds__(kBlock)
@@ -48,8 +54,8 @@ __global__ void __launch_bounds__(kBlock)
   for (int dx = 0; dx < F.fx; ++dx)
     for (int dy = 0; dy < F.fy; ++dy)
       for (int dz = 0; dz < F.fz; ++dz) {
-        const int32_t j = ((F.fx * c.x + dx) * F.sy + F.fy * c.y + dy) * F.sz +
-                          F.fz * c.z + dz;
+        const int32_t j = lid(F, F.fx * c.x + dx, F.fy * c.y + dy,
+                              F.fz * c.z + dz);
         if (dx == F.fx - 1) wx += F.wx[j];
         if (dy == F.fy - 1) wy += F.wy[j];
         if (dz == F.fz - 1) wz += F.wz[j];
@@ -72,7 +78,7 @@ __global__ void __launch_bounds__(kBlock)
     c.x = x;
     c.y = y;
     c.z = z;
-    c.i = (x * L.sy + y) * L.sz + z;
+    c.i = lid(L, x, y, z);
     if (L.pinned && y == L.sy - 1) {
       L.ivd[c.i] = 1.0;
       L.cp[c.i] = 0.0;
@@ -89,19 +95,24 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// ---------------------------------------------------------------------------
+// line smoothing
+//
 // Y-line solve T z = rhs for the line (x, z), loads batched kChunk rows at a
 // time so the serial recurrence never waits on one load per row.  `tmp`
 // holds the forward sweep and may alias rhs (each element is read before it
-// is overwritten).  mode 0: out = w z; 1: out += w z; 2: out += P xc + w z.
-template <int kMode>
+// is overwritten).  mode 0: out = w z;  mode 2: out += P x_c + w z (the
+// coarse correction prolonged on the fly).  kSums: accumulate the CG z-sums
+// (sum z, sum r.z, sum r, with r = L.r) of the written values.
+template <int kMode, bool kSums = false>
 __device__ __forceinline__ void line_solve(const MgLevel &L, int32_t x,
                                            int32_t z, const double *rhs,
                                            double *tmp, double *out,
                                            double omega,
-                                           const double *cx = nullptr,
-                                           const MgLevel *C = nullptr) {
+                                           const MgLevel *C = nullptr,
+                                           double *sums = nullptr) {
   const int32_t st = L.sz;
-  const int32_t base = x * L.sy * L.sz + z;
+  const int32_t base = lid(L, x, 0, z);
   const int32_t sy = L.sy;
   double dp = 0.0, wprev = 0.0;
   for (int y0 = 0; y0 < sy; y0 += kChunk) {
@@ -126,14 +137,14 @@ __device__ __forceinline__ void line_solve(const MgLevel &L, int32_t x,
       }
     }
   }
-  double znext = 0.0;
   int32_t cbase = 0, cst = 0;
   if (kMode == 2) {
-    cbase = (x >> (L.fx - 1)) * C->sy * C->sz + (z >> (L.fz - 1));
+    cbase = lid(*C, x >> (L.fx - 1), 0, z >> (L.fz - 1));
     cst = C->sz;
   }
+  double znext = 0.0;
   for (int y0 = sy - 1; y0 >= 0; y0 -= kChunk) {
-    double tt[kChunk], cc[kChunk], oo[kChunk];
+    double tt[kChunk], cc[kChunk], oo[kChunk], rr[kChunk];
 #pragma unroll
     for (int k = 0; k < kChunk; ++k) {
       const int y = y0 - k;
@@ -141,8 +152,8 @@ __device__ __forceinline__ void line_solve(const MgLevel &L, int32_t x,
         const int32_t i = base + y * st;
         tt[k] = tmp[i];
         cc[k] = L.cp[i];
-        if (kMode == 1) oo[k] = out[i];
-        if (kMode == 2) oo[k] = out[i] + cx[cbase + (y >> (L.fy - 1)) * cst];
+        if (kMode == 2) oo[k] = out[i] + C->x[cbase + (y >> (L.fy - 1)) * cst];
+        if (kSums) rr[k] = L.r[i];
       }
     }
 #pragma unroll
@@ -151,13 +162,19 @@ __device__ __forceinline__ void line_solve(const MgLevel &L, int32_t x,
       if (y >= 0) {
         const double zv = tt[k] - cc[k] * znext;
         znext = zv;
-        out[base + y * st] = kMode == 0 ? omega * zv : oo[k] + omega * zv;
+        const double o = kMode == 0 ? omega * zv : oo[k] + omega * zv;
+        out[base + y * st] = o;
+        if (kSums) {
+          sums[0] += o;
+          sums[1] += rr[k] * o;
+          sums[2] += rr[k];
+        }
       }
     }
   }
 }
 
-// x = omega T^-1 r
+// x = omega T^-1 r over every line
 __global__ void __launch_bounds__(kLineBlock)
     k_mg_smooth0(MgLevel L, const double *__restrict__ r, double *x,
                  double omega, const int *done) {
@@ -167,34 +184,41 @@ __global__ void __launch_bounds__(kLineBlock)
   line_solve<0>(L, l / L.sz, l % L.sz, r, x, x, omega);
 }
 
-// x += omega T^-1 res  (res is consumed as scratch)
-__global__ void __launch_bounds__(kLineBlock)
-    k_mg_smooth1(MgLevel L, double *res, double *x, double omega,
-                 const int *done) {
-  MG_DONE_RETURN;
-  const int32_t l = blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= L.sx * L.sz) return;
-  line_solve<1>(L, l / L.sz, l % L.sz, res, res, x, omega);
-}
-
-// x += P x_c + omega T^-1 res   (res = r - K (x + P x_c), previous pass)
+// x += P x_c + omega T^-1 res  (res = r - K (x + P x_c), consumed)
 __global__ void __launch_bounds__(kLineBlock)
     k_mg_smooth2(MgLevel L, double *res, double *x, double omega, MgLevel C,
                  const int *done) {
   MG_DONE_RETURN;
   const int32_t l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= L.sx * L.sz) return;
-  line_solve<2>(L, l / L.sz, l % L.sz, res, res, x, omega, C.x, &C);
+  line_solve<2>(L, l / L.sz, l % L.sz, res, res, x, omega, &C);
 }
 
-// coarse rhs = sum over the aggregate of r - K x
-__global__ void __launch_bounds__(kBlock)
-    k_mg_resid_restrict(MgLevel F, const double *__restrict__ r,
-                        const double *__restrict__ x, MgLevel C,
-                        const int *done) {
+// level 0 of the CG's V-cycle: the final smoothing pass also accumulates the
+// CG z-sums and evaluates beta (k_cg_zsum folded in); grid-stride over lines
+// so the grid fits the reduction partials
+__global__ void __launch_bounds__(kLineBlock)
+    k_mg_smooth2_cg(MgLevel L, double *res, double *x, double omega,
+                    MgLevel C, CgFuse fz, const int *done) {
   MG_DONE_RETURN;
-  const int32_t I = blockIdx.x * blockDim.x + threadIdx.x;
-  if (I >= C.n) return;
+  double sums[3] = {0.0, 0.0, 0.0};
+  for (int32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < L.sx * L.sz;
+       l += gridDim.x * blockDim.x)
+    line_solve<2, true>(L, l / L.sz, l % L.sz, res, res, x, omega, &C, sums);
+  double tot[3];
+  if (grid_reduce<3>(sums, fz.partials, fz.counter, tot))
+    cg_fin_z(fz.st, tot[0], tot[1], tot[2], (int32_t)L.n, fz.initial != 0);
+}
+
+// ---------------------------------------------------------------------------
+// residual transfer
+
+// coarse rhs = sum over the aggregate of r - K x, coarse cell I
+__device__ __forceinline__ void resid_restrict_at(const MgLevel &F,
+                                                  const double *r,
+                                                  const double *x,
+                                                  const MgLevel &C,
+                                                  int32_t I) {
   const Cell3 cc = decode(C, I);
   double acc = 0.0;
   for (int dx = 0; dx < F.fx; ++dx)
@@ -204,22 +228,30 @@ __global__ void __launch_bounds__(kBlock)
         c.x = F.fx * cc.x + dx;
         c.y = F.fy * cc.y + dy;
         c.z = F.fz * cc.z + dz;
-        c.i = (c.x * F.sy + c.y) * F.sz + c.z;
+        c.i = lid(F, c.x, c.y, c.z);
         const Nbhd b = nbhd(F, c);
         acc += r[c.i] - kx(b, c.i, x);
       }
   C.r[I] = acc;
 }
 
-// res = r - K (x + P x_c): prolongation fused into the residual; x itself is
-// updated by k_mg_smooth2, so no thread writes what another thread reads
 __global__ void __launch_bounds__(kBlock)
-    k_mg_prolong_resid(MgLevel F, const double *__restrict__ r,
-                       const double *__restrict__ x, double *__restrict__ res,
-                       MgLevel C, const int *done) {
+    k_mg_resid_restrict(MgLevel F, const double *__restrict__ r,
+                        const double *__restrict__ x, MgLevel C,
+                        const int *done) {
   MG_DONE_RETURN;
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= F.n) return;
+  const int32_t I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= C.n) return;
+  resid_restrict_at(F, r, x, C, I);
+}
+
+// res = r - K (x + P x_c) at fine cell i: prolongation fused into the
+// residual; x itself is updated by the following smoothing pass, so no
+// thread writes what another thread reads
+__device__ __forceinline__ void prolong_resid_at(const MgLevel &F,
+                                                 const double *r,
+                                                 const double *x, double *res,
+                                                 const MgLevel &C, int32_t i) {
   const Cell3 c = decode(F, i);
   const Nbhd b = nbhd(F, c);
   const double *cxv = C.x;
@@ -240,23 +272,22 @@ __global__ void __launch_bounds__(kBlock)
   res[i] = r[i] - kv;
 }
 
-// res = r - K x
 __global__ void __launch_bounds__(kBlock)
-    k_mg_resid(MgLevel L, const double *__restrict__ r,
-               const double *__restrict__ x, double *__restrict__ res,
-               const int *done) {
+    k_mg_prolong_resid(MgLevel F, const double *__restrict__ r,
+                       const double *__restrict__ x, double *__restrict__ res,
+                       MgLevel C, const int *done) {
   MG_DONE_RETURN;
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= L.n) return;
-  const Cell3 c = decode(L, i);
-  const Nbhd b = nbhd(L, c);
-  res[i] = r[i] - kx(b, i, x);
+  if (i >= F.n) return;
+  prolong_resid_at(F, r, x, res, C, i);
 }
 
-// exact solve of the singular coarsest line problem, projected to zero mean
-__global__ void __launch_bounds__(kBlock)
-    k_mg_coarsest(MgLevel L, const int *done) {
-  MG_DONE_RETURN;
+// ---------------------------------------------------------------------------
+// coarse levels
+
+// exact solve of the singular coarsest line problem, projected to zero mean;
+// executed by a whole CTA
+__device__ __forceinline__ void coarsest_block(const MgLevel &L) {
   if (threadIdx.x == 0) line_solve<0>(L, 0, 0, L.r, L.x, L.x, 1.0);
   __syncthreads();
   double v[1] = {0.0};
@@ -266,6 +297,78 @@ __global__ void __launch_bounds__(kBlock)
   if (threadIdx.x == 0) mean = v[0] / (double)L.n;
   __syncthreads();
   for (int32_t i = threadIdx.x; i < L.n; i += blockDim.x) L.x[i] -= mean;
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_mg_coarsest(MgLevel L, const int *done) {
+  MG_DONE_RETURN;
+  coarsest_block(L);
+}
+
+// The V-cycle from level l0 down in ONE CTA: the small coarse levels are
+// latency-bound, so phases are separated by __syncthreads instead of kernel
+// boundaries.  A non-singular coarsest level (coarsening stopped on odd
+// sizes) gets 5 damped line sweeps.
+__global__ void __launch_bounds__(1024)
+    k_mg_coarse_fused(MgHierarchy h, int l0, const int *done) {
+  MG_DONE_RETURN;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int last = h.nlev - 1;
+  const double om = h.omega;
+  for (int l = l0; l < last; ++l) {
+    const MgLevel &L = h.lv[l], &C = h.lv[l + 1];
+    for (int32_t ln = tid; ln < L.sx * L.sz; ln += nt)
+      line_solve<0>(L, ln / L.sz, ln % L.sz, L.r, L.x, L.x, om);
+    __syncthreads();
+    for (int32_t I = tid; I < C.n; I += nt)
+      resid_restrict_at(L, L.r, L.x, C, I);
+    __syncthreads();
+  }
+  const MgLevel &E = h.lv[last];
+  if (E.pinned) {
+    coarsest_block(E);
+  } else {
+    for (int32_t ln = tid; ln < E.sx * E.sz; ln += nt)
+      line_solve<0>(E, ln / E.sz, ln % E.sz, E.r, E.x, E.x, om);
+    __syncthreads();
+    for (int it = 0; it < 4; ++it) {
+      for (int32_t i = tid; i < E.n; i += nt)
+        E.t[i] = E.r[i] - kx(nbhd(E, decode(E, i)), i, E.x);
+      __syncthreads();
+      for (int32_t ln = tid; ln < E.sx * E.sz; ln += nt)
+        line_solve<0>(E, ln / E.sz, ln % E.sz, E.t, E.t, E.t, om);
+      __syncthreads();
+      for (int32_t i = tid; i < E.n; i += nt) E.x[i] += E.t[i];
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  for (int l = last - 1; l >= l0; --l) {
+    const MgLevel &L = h.lv[l], &C = h.lv[l + 1];
+    for (int32_t i = tid; i < L.n; i += nt)
+      prolong_resid_at(L, L.r, L.x, L.t, C, i);
+    __syncthreads();
+    for (int32_t ln = tid; ln < L.sx * L.sz; ln += nt)
+      line_solve<2>(L, ln / L.sz, ln % L.sz, L.t, L.t, L.x, om, &C);
+    __syncthreads();
+  }
+}
+
+// CG z-sums for the rare single-level hierarchy (no final smoother to fuse)
+__global__ void __launch_bounds__(kBlock)
+    k_mg_zsum(const double *__restrict__ r, const double *__restrict__ z,
+              int32_t n, CgFuse fz, const int *done) {
+  MG_DONE_RETURN;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += gridDim.x * blockDim.x) {
+    acc[0] += z[i];
+    acc[1] += r[i] * z[i];
+    acc[2] += r[i];
+  }
+  double tot[3];
+  if (grid_reduce<3>(acc, fz.partials, fz.counter, tot))
+    cg_fin_z(fz.st, tot[0], tot[1], tot[2], n, fz.initial != 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -374,25 +477,24 @@ int mg_setup(const MgHierarchy &h, const double *k, int64_t n, cudaStream_t s,
   return PF_OK;
 }
 
+// cells: levels at most this small run the rest of the V-cycle in one CTA
+// (a 24576-cell level is already too big for one SM; the 3072-cell and
+// smaller levels are pure launch/latency cost -- measured on C4)
+constexpr int64_t kFusedCoarseMax = 4096;
+
 static void vcycle(const MgHierarchy &h, int l, const double *r, double *x,
-                   cudaStream_t s, const int *done, cudaEvent_t *ev = nullptr) {
+                   cudaStream_t s, const int *done, cudaEvent_t *ev,
+                   const CgFuse *fuse, int red_blocks, int fused_from) {
   auto mark = [&](int k) {
     if (ev && l == 0) cudaEventRecord(ev[k], s);
   };
   const MgLevel &L = h.lv[l];
+  if (l > 0 && (l >= fused_from || (l == h.nlev - 1 && !L.pinned))) {
+    launch(k_mg_coarse_fused, 1, 1024, s, h, l, done);
+    return;
+  }
   if (l == h.nlev - 1) {
-    if (L.pinned) {
-      launch(k_mg_coarsest, 1, kBlock, s, L, done);
-    } else {
-      launch(k_mg_smooth0, lines_grid(L), kLineBlock, s, L, r, x, h.omega,
-             done);
-      for (int it = 0; it < 4; ++it) {
-        launch(k_mg_resid, grid_for(L.n), kBlock, s, L, r, (const double *)x,
-               L.t, done);
-        launch(k_mg_smooth1, lines_grid(L), kLineBlock, s, L, L.t, x,
-               h.omega, done);
-      }
-    }
+    launch(k_mg_coarsest, 1, kBlock, s, L, done);
     return;
   }
   const MgLevel &C = h.lv[l + 1];
@@ -402,25 +504,45 @@ static void vcycle(const MgHierarchy &h, int l, const double *r, double *x,
   launch(k_mg_resid_restrict, grid_for(C.n), kBlock, s, L, r,
          (const double *)x, C, done);
   mark(2);
-  vcycle(h, l + 1, C.r, C.x, s, done);
+  vcycle(h, l + 1, C.r, C.x, s, done, nullptr, nullptr, red_blocks,
+         fused_from);
   mark(3);
   launch(k_mg_prolong_resid, grid_for(L.n), kBlock, s, L, r,
          (const double *)x, L.t, C, done);
   mark(4);
-  launch(k_mg_smooth2, lines_grid(L), kLineBlock, s, L, L.t, x, h.omega, C,
-         done);
+  if (l == 0 && fuse && fuse->st)
+    launch(k_mg_smooth2_cg, std::min(lines_grid(L), red_blocks), kLineBlock,
+           s, L, L.t, x, h.omega, C, *fuse, done);
+  else
+    launch(k_mg_smooth2, lines_grid(L), kLineBlock, s, L, L.t, x, h.omega, C,
+           done);
   mark(5);
 }
 
 int mg_apply(const MgHierarchy &h, const double *r, double *z, cudaStream_t s,
-             const int *done, cudaEvent_t *ev) {
+             const int *done, cudaEvent_t *ev, const CgFuse *fuse,
+             int red_blocks) {
   MgHierarchy hh = h;
   hh.lv[0].r = const_cast<double *>(r);
   hh.lv[0].x = z;
-  if (hh.nlev == 1 && hh.lv[0].pinned) {
-    launch(k_mg_coarsest, 1, kBlock, s, hh.lv[0], done);
+  int fused_from = hh.nlev;
+  for (int l = 1; l < hh.nlev; ++l)
+    if (hh.lv[l].n <= kFusedCoarseMax) {
+      fused_from = l;
+      break;
+    }
+  if (hh.nlev == 1) {
+    // the whole problem is one level: exact (pinned) or fused sweeps
+    if (hh.lv[0].pinned)
+      launch(k_mg_coarsest, 1, kBlock, s, hh.lv[0], done);
+    else
+      launch(k_mg_coarse_fused, 1, 1024, s, hh, 0, done);
+    if (fuse && fuse->st)
+      launch(k_mg_zsum, std::min(grid_for(hh.lv[0].n), red_blocks), kBlock,
+             s, (const double *)r, (const double *)z, (int32_t)hh.lv[0].n,
+             *fuse, done);
   } else {
-    vcycle(hh, 0, r, z, s, done, ev);
+    vcycle(hh, 0, r, z, s, done, ev, fuse, red_blocks, fused_from);
   }
   PF_LAUNCH_CHECK("mg_apply");
   return PF_OK;

@@ -8,18 +8,25 @@
 // solution (only iteration counts change):
 //
 //  * canonical axes (X, Y, Z): Y is the LINE axis (the wall-normal, refined
-//    axis of the channel / the first axis in 2D), X and Z are coarsened by 2
-//    (semi-coarsening) while they are even;
-//  * smoother: damped block-Jacobi with exact tridiagonal solves along the
-//    Y lines (one thread per line, coalesced across lines), which removes
-//    the wall-refinement anisotropy;
-//  * coarse operators: Galerkin with piecewise-constant aggregation, i.e.
-//    coarse face weights are sums of fine face weights, so every level keeps
-//    the symmetric 7-point face form with exact zero row sums;
+//    axis of the channel / the first axis in 2D);
+//  * smoother: damped (omega = 0.85) block-Jacobi with exact tridiagonal
+//    solves along the Y lines (one thread per line, coalesced across lines),
+//    which removes the wall-refinement anisotropy;
+//  * coarsening: 2 along X, Y, Z while the axis is even (Y while longer than
+//    2); coarse operators are Galerkin with piecewise-constant aggregation,
+//    i.e. coarse face weights are sums of fine face weights, so every level
+//    keeps the symmetric 7-point face form with exact zero row sums;
 //  * coarsest level (X = Z = 1): the singular Y-line Neumann problem, solved
-//    exactly by a pinned Thomas sweep and projected to zero mean.
+//    exactly by a pinned Thomas sweep and projected to zero mean; levels of
+//    at most a few thousand cells run as one CTA (latency, not bandwidth).
+//
+// Measured alternative (not used): a red-black line Gauss-Seidel smoother
+// cut iterations by ~22 % on the C4 channel but doubled the time per
+// iteration, because each colour pass has only half of the lines in flight
+// for the serial Thomas recurrences.
 #pragma once
 
+#include "cgstate.cuh"
 #include "common.cuh"
 
 namespace pf {
@@ -73,7 +80,6 @@ __device__ __forceinline__ double kx(const Nbhd &b, int32_t i,
          b.wzp * (vi - v[b.zp]) + b.wzm * (vi - v[b.zm]);
 }
 
-
 // Host: plan the hierarchy for a box plan; returns false when MG does not
 // apply (gather topology, periodic line axis, line axis shorter than 2).
 bool mg_plan(const Plan &p, MgHierarchy &h, int64_t *bytes);
@@ -85,8 +91,11 @@ int mg_setup(const MgHierarchy &h, const double *k_stencil, int64_t n,
              cudaStream_t s, const int *all_done);
 // z = V(r) on the fine level; every kernel returns at once when *all_done.
 // `ev` (optional, 6 events) is recorded around the level-0 kernels:
-// smooth0 | restrict | coarse levels | prolong | smooth2.
+// smooth | restrict | coarse levels | prolong | smooth.  `fuse` (optional)
+// folds the CG z-sums and beta into the final level-0 smoothing pass (no
+// separate z-sum kernel); it needs red_blocks.
 int mg_apply(const MgHierarchy &h, const double *r, double *z,
-             cudaStream_t s, const int *all_done, cudaEvent_t *ev = nullptr);
+             cudaStream_t s, const int *all_done, cudaEvent_t *ev = nullptr,
+             const CgFuse *fuse = nullptr, int red_blocks = 0);
 
 }  // namespace pf

@@ -15,27 +15,11 @@
 // GPU never waits on a host round trip per iteration.
 #include <algorithm>
 
+#include "cgstate.cuh"
 #include "common.cuh"
 #include "mg.cuh"
 
 namespace pf {
-
-struct CompState {
-  double bnorm, tol_abs, res, rho, rho_new, alpha, omega, beta;
-  double zbar, rz, xmean, true_res, bmean, rmean, tol, pad1;
-  int32_t iter, maxiter, done, converged, fail, zero_rhs, pending, active;
-  int32_t project_x, pad2[7];
-};
-
-struct SolverState {
-  CompState c[3];
-  int32_t all_done, ncomp, precond, zero_mean;
-  int32_t pad[12];
-};
-
-static_assert(sizeof(SolverState) <= 8 * kWsSolver, "solver state too big");
-
-__device__ __forceinline__ bool finite(double x) { return isfinite(x); }
 
 // ---------------------------------------------------------------------------
 // stencil application  y_i = sum_j A_ij x_j  (transposed: A_ji)
@@ -156,32 +140,6 @@ __global__ void __launch_bounds__(kBlock)
   double tot[1];
   if (grid_reduce<1>(acc, partials, counter, tot))
     st->c[0].rmean = st->zero_mean ? tot[0] / v.n : 0.0;
-}
-
-// z-bar, r.z and beta from the sums (sum z, sum r.z, sum r); `initial`
-// seeds rz for the first direction (S/linalg.py:146-149 / 162-168)
-__device__ __forceinline__ void cg_fin_z(SolverState *st, double sz,
-                                         double srz, double sr, int32_t n,
-                                         bool initial) {
-  CompState &c = st->c[0];
-  c.zbar = st->zero_mean ? sz / n : 0.0;
-  const double rz_new = srz - c.zbar * sr;
-  if (initial) {
-    c.rz = rz_new;
-    return;
-  }
-  if (!finite(rz_new) || c.rz == 0.0) {
-    c.fail = 1;
-    c.done = 1;
-    st->all_done = 1;
-    return;
-  }
-  c.beta = rz_new / c.rz;
-  c.rz = rz_new;
-  if (c.iter >= c.maxiter) {
-    c.done = 1;
-    st->all_done = 1;
-  }
 }
 
 // z value of cell i: the multigrid output vector, or M r pointwise
@@ -766,11 +724,29 @@ void mg_iteration(const Plan &pl, Workspace &w, SolverState *st,
   launch(k_cg_update, gr, kBlock, s, (const double *)nullptr,
          (const double *)p, (const double *)q, x, r, n, st, w.partials,
          w.counters);
-  mg_apply(*mg, r, z, s, &st->all_done);
-  launch(k_cg_zsum, gr, kBlock, s, (const double *)r, (const double *)z, n, 0,
-         st, w.partials, w.counters);
+  // the V-cycle's last smoothing pass also forms the z-sums and beta
+  const CgFuse fuse{st, w.partials, w.counters, 0};
+  mg_apply(*mg, r, z, s, &st->all_done, nullptr, &fuse, pl.red_blocks);
   launch(k_cg_pupdate, ge, kBlock, s, (const double *)nullptr,
          (const double *)r, (const double *)z, p, n, st);
+}
+
+// r = bp - K x on the multigrid level-0 face form
+__global__ void __launch_bounds__(kBlock)
+    k_cg_resid_faces(MgLevel L, const double *__restrict__ bp,
+                     const double *__restrict__ x, double *__restrict__ r,
+                     SolverState *st, double *partials, unsigned *counter) {
+  if (st->all_done) return;
+  double acc[1] = {0.0};
+  GRID_LOOP(i, (int32_t)L.n) {
+    const Cell3 c = decode(L, i);
+    const double ri = bp[i] - kx(nbhd(L, c), i, x);
+    r[i] = ri;
+    acc[0] += ri;
+  }
+  double tot[1];
+  if (grid_reduce<1>(acc, partials, counter, tot))
+    st->c[0].rmean = st->zero_mean ? tot[0] / L.n : 0.0;
 }
 
 constexpr int kGraphIters = 4;  // MG-PCG iterations per graph launch
@@ -813,20 +789,24 @@ int cg_core_mg(const Plan &pl, const V &v, Workspace &w, SolverState *st,
                SolverState &hs, const double *a, const double *bp, double *x,
                double tol, int maxiter, int zero_mean, const MgHierarchy *mg,
                cudaStream_t s) {
+  // x is the workspace copy of the warm start (the graph's buffers are all
+  // workspace-resident)
   const int32_t n = v.n;
   double *r = w.vecs, *p = w.vecs + n;
   double *z = w.vecs + 4 * (int64_t)n;
   const int *done = &st->all_done;
   const int ge = grid_for(n), gr = std::min(grid_for(n), pl.red_blocks);
+  (void)a;
   launch(k_cg_reset, 1, 1, s, st, maxiter, 2, zero_mean, tol, 0);
-  launch(k_cg_resid<V>, gr, kBlock, s, v, a, bp, (const double *)x, r, st,
+  launch(k_cg_resid_faces, gr, kBlock, s, mg->lv[0], bp, (const double *)x,
+         r, st, w.partials, w.counters);
+  launch(k_cg_rproj, gr, kBlock, s, (const double *)nullptr, r, n, st,
          w.partials, w.counters);
-  launch(k_cg_rproj, gr, kBlock, s, a, r, n, st, w.partials, w.counters);
-  int rc = mg_apply(*mg, r, z, s, done);
+  const CgFuse fuse{st, w.partials, w.counters, 1};
+  int rc = mg_apply(*mg, r, z, s, done, nullptr, &fuse, pl.red_blocks);
   if (rc) return rc;
-  launch(k_cg_zsum, gr, kBlock, s, (const double *)r, (const double *)z, n, 1,
-         st, w.partials, w.counters);
-  launch(k_cg_pinit, ge, kBlock, s, a, r, (const double *)z, p, n, st);
+  launch(k_cg_pinit, ge, kBlock, s, (const double *)nullptr, r,
+         (const double *)z, p, n, st);
   PF_LAUNCH_CHECK("mg-cg setup");
   cudaGraphExec_t exec;
   unsigned long long nk = 0;
@@ -846,10 +826,6 @@ int cg_core_mg(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     launched += b * kGraphIters;
   }
   launch(k_cg_finish, ge, kBlock, s, x, n, st);
-  if (hs.c[0].converged && !hs.c[0].zero_rhs) {
-    launch(k_true_res<V>, gr, kBlock, s, v, a, 0, 1, bp, (const double *)x,
-           st, w.partials, w.counters);
-  }
   PF_LAUNCH_CHECK("mg-cg finish");
   return PF_OK;
 }
@@ -866,27 +842,27 @@ int cg_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   const int ge = grid_for(n), gr = std::min(grid_for(n), pl.red_blocks);
   if (precond == 2) {
     // the multigrid iteration runs from a CUDA graph whose buffers are all
-    // workspace-resident: iterate on a workspace copy of x
+    // workspace-resident: iterate on a copy of x, copy the solution back
     double *xw = w.vecs + 5 * (int64_t)n;
     PF_CUDA(cudaMemcpyAsync(xw, x, sizeof(double) * n,
                             cudaMemcpyDeviceToDevice, s));
     int rc = cg_core_mg(pl, v, w, st, hs, a, bp, xw, tol, maxiter, zero_mean,
                         mg, s);
+    if (!rc) rc = read_state(st, &hs, s);
     if (rc) return rc;
     PF_CUDA(cudaMemcpyAsync(x, xw, sizeof(double) * n,
                             cudaMemcpyDeviceToDevice, s));
+    if (hs.c[0].converged && !hs.c[0].zero_rhs)
+      launch(k_true_res<V>, gr, kBlock, s, v, a, 0, 1, bp, (const double *)x,
+             st, w.partials, w.counters);
+    PF_LAUNCH_CHECK("mg-cg true residual");
     return read_state(st, &hs, s);
   }
   launch(k_cg_reset, 1, 1, s, st, maxiter, precond, zero_mean, tol, 0);
   launch(k_cg_resid<V>, gr, kBlock, s, v, a, bp, x, r, st, w.partials,
                                       w.counters);
   launch(k_cg_rproj, gr, kBlock, s, a, r, n, st, w.partials, w.counters);
-  if (precond == 2) {
-    int rc = mg_apply(*mg, r, z, s, done);
-    if (rc) return rc;
-    launch(k_cg_zsum, gr, kBlock, s, (const double *)r, (const double *)z, n,
-           1, st, w.partials, w.counters);
-  }
+  (void)done;
   launch(k_cg_pinit, ge, kBlock, s, a, r, (const double *)z, p, n, st);
   PF_LAUNCH_CHECK("cg setup");
   int launched = 0;
@@ -896,20 +872,10 @@ int cg_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     if (hs.all_done || launched >= maxiter) break;
     const int b = std::min(next_batch(launched, 0), maxiter - launched);
     for (int k = 0; k < b; ++k) {
-      if (precond == 2)
-        launch(k_cg_spmv_faces, gr, kBlock, s, mg->lv[0], (const double *)p,
-               q, st, w.partials, w.counters);
-      else
-        launch(k_cg_spmv<V>, gr, kBlock, s, v, a, p, q, st, w.partials,
-               w.counters);
+      launch(k_cg_spmv<V>, gr, kBlock, s, v, a, p, q, st, w.partials,
+             w.counters);
       launch(k_cg_update, gr, kBlock, s, a, p, q, x, r, n, st, w.partials,
                                         w.counters);
-      if (precond == 2) {
-        int rc = mg_apply(*mg, r, z, s, done);
-        if (rc) return rc;
-        launch(k_cg_zsum, gr, kBlock, s, (const double *)r,
-               (const double *)z, n, 0, st, w.partials, w.counters);
-      }
       launch(k_cg_pupdate, ge, kBlock, s, a, r, (const double *)z, p, n, st);
     }
     PF_LAUNCH_CHECK("cg iterations");
@@ -1169,7 +1135,9 @@ extern "C" int pf_cg_profile(const pf_plan *plan, const double *a,
     using V = decltype(v);
     const int ge = grid_for(n), gr = std::min(grid_for(n), pl.red_blocks);
     PF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
-    launch(k_cg_reset, 1, 1, s, st, iters + 1, precond, 1, 0.0, 1);
+    // room for the timed iterations plus the graph-replay measurement
+    launch(k_cg_reset, 1, 1, s, st, 2 * iters + 2 * kGraphIters + 1, precond,
+           1, 0.0, 1);
     launch(k_cg_bsum, gr, kBlock, s, b, 1.0, n, st, w.partials, w.counters);
     launch(k_cg_bproj, gr, kBlock, s, b, 1.0, bp, n, st, w.partials,
            w.counters);
@@ -1177,10 +1145,9 @@ extern "C" int pf_cg_profile(const pf_plan *plan, const double *a,
            w.counters);
     launch(k_cg_rproj, gr, kBlock, s, a, r, n, st, w.partials, w.counters);
     if (precond == 2) {
-      int rc = mg_apply(mg, r, z, s, done);
+      const CgFuse fuse{st, w.partials, w.counters, 1};
+      int rc = mg_apply(mg, r, z, s, done, nullptr, &fuse, pl.red_blocks);
       if (rc) return rc;
-      launch(k_cg_zsum, gr, kBlock, s, (const double *)r, (const double *)z,
-             n, 1, st, w.partials, w.counters);
     }
     launch(k_cg_pinit, ge, kBlock, s, a, r, (const double *)z, p, n, st);
     // events: 0 start | 1 spmv | 2 update | 3..8 mg level-0 marks | 9 zsum |
@@ -1201,10 +1168,11 @@ extern "C" int pf_cg_profile(const pf_plan *plan, const double *a,
              w.counters);
       PF_CUDA(cudaEventRecord(ev[2], s));
       if (precond == 2) {
-        int rc = mg_apply(mg, r, z, s, done, ev + 3);
+        // as in production: the z-sums ride in the last smoothing pass, so
+        // the zsum slot measures ~0
+        const CgFuse fuse{st, w.partials, w.counters, 0};
+        int rc = mg_apply(mg, r, z, s, done, ev + 3, &fuse, pl.red_blocks);
         if (rc) return rc;
-        launch(k_cg_zsum, gr, kBlock, s, (const double *)r,
-               (const double *)z, n, 0, st, w.partials, w.counters);
       } else {
         for (int j = 3; j < 9; ++j) PF_CUDA(cudaEventRecord(ev[j], s));
       }
@@ -1225,6 +1193,26 @@ extern "C" int pf_cg_profile(const pf_plan *plan, const double *a,
       PF_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[10]));
       tot[9] += ms;
     }
+    // [10]: the production path -- iterations replayed from the cached
+    // CUDA graph (multigrid only)
+    double graph_ms = 0.0;
+    if (precond == 2) {
+      cudaGraphExec_t exec;
+      unsigned long long nk = 0;
+      int rc = mg_graph(pl, w, st, &mg, x, &exec, &nk);
+      if (rc) return rc;
+      const int reps = std::max(1, iters / kGraphIters);
+      PF_CUDA(cudaEventRecord(ev[0], s));
+      for (int k = 0; k < reps; ++k) {
+        PF_CUDA(cudaGraphLaunch(exec, s));
+        g_launches += nk;
+      }
+      PF_CUDA(cudaEventRecord(ev[1], s));
+      PF_CUDA(cudaEventSynchronize(ev[1]));
+      float ms = 0.f;
+      PF_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+      graph_ms = ms / (reps * kGraphIters);
+    }
     for (auto &e : ev) cudaEventDestroy(e);
     SolverState hs;
     int rc = read_state(st, &hs, s);
@@ -1234,6 +1222,7 @@ extern "C" int pf_cg_profile(const pf_plan *plan, const double *a,
       return PF_ERR_ARG;
     }
     for (int j = 0; j < 10; ++j) ms_host[j] = tot[j] / iters;
+    ms_host[10] = graph_ms;
     return PF_OK;
   });
 }
