@@ -251,7 +251,21 @@ KERNEL_BYTES = {
     # 1/8 coarse x
     "k_mg_smooth2_cg (level 0)": 57,
     "k_cg_pupdate": 24,           # z, p read; p written
+    # spectral preconditioner: the (Y, kz, kx) work array holds ~n/2
+    # complex values, 8 B per cell per sweep
+    "k_spec_fwd_z": 16,           # r read; spectrum written
+    "k_spec_x (forward)": 16,     # spectrum read + written
+    "k_spec_ysolve": 16,          # minimum: spectrum read + written once
+    "k_spec_x (inverse)": 16,
+    "k_spec_inv_z + CG z-sums": 24,  # spectrum, r read; z written
 }
+
+MG_NAMES = ["k_mg_smooth0 (level 0)", "k_mg_resid_restrict (level 0)",
+            "mg coarse levels", "k_mg_prolong_resid (level 0)",
+            "k_mg_smooth2_cg (level 0)", "zsum (fused into smooth2)"]
+SPEC_NAMES = ["k_spec_fwd_z", "k_spec_x (forward)", "k_spec_ysolve",
+              "k_spec_x (inverse)", "k_spec_inv_z + CG z-sums",
+              "zsum (fused into inv_z)"]
 
 
 def measure_roofline(args, dom, plan, state, nu, dt, dev):
@@ -275,12 +289,8 @@ def measure_roofline(args, dom, plan, state, nu, dt, dev):
               args.profile_iters, 2 if mg else 1, _lib.ptr(plan.workspace),
               _lib.ptr(plan.mg_workspace if mg else None), ms, plan.stream)
     names = (["k_cg_spmv_faces" if mg else "k_cg_spmv", "k_cg_update"]
-             + (["k_mg_smooth0 (level 0)",
-                 "k_mg_resid_restrict (level 0)",
-                 "mg coarse levels", "k_mg_prolong_resid (level 0)",
-                 "k_mg_smooth2_cg (level 0)", "zsum (fused into smooth2)"]
-                if mg else
-                [None] * 6) + ["k_cg_pupdate"])
+             + ((SPEC_NAMES if plan.geom_kind == "spectral" else MG_NAMES)
+                if mg else [None] * 6) + ["k_cg_pupdate"])
     idx = [0, 1, 2, 3, 4, 5, 6, 7, 8]
     per = {}
     for j, nm in zip(idx, names):
@@ -312,7 +322,7 @@ def measure_roofline(args, dom, plan, state, nu, dt, dev):
             "peak_source": peak_src, "bytes_per_cell": KERNEL_BYTES[top],
             "cells_per_launch": n, "ms_per_launch": cand[top],
             "pressure_cg_iteration": {
-                "preconditioner": "multigrid" if mg else "jacobi",
+                "preconditioner": plan.geom_kind if mg else "jacobi",
                 "ms": it_ms, "ms_graph_replay": float(ms[10]),
                 "level0_and_cg_ms": fine_ms,
                 "level0_and_cg_bytes_per_cell": it_bytes,

@@ -60,6 +60,10 @@ extern "C" {
 #define PF_PRECOND_JACOBI 1
 #define PF_PRECOND_MG 2
 
+#define PF_GEOM_NONE (-1)
+#define PF_GEOM_MULTIGRID 0
+#define PF_GEOM_SPECTRAL 1
+
 #define PF_BKIND_DIRICHLET 0
 #define PF_BKIND_OUTFLOW 1
 
@@ -99,6 +103,11 @@ typedef struct pf_plan_desc {
                                 tangential-terms active, axis, side, 0    */
   int32_t nfaces;
   int32_t has_cross;         /* cell cross terms active                   */
+  /* PF_GEOM_MULTIGRID (0) or PF_GEOM_SPECTRAL: the pressure preconditioner
+   * of a box plan.  SPECTRAL asserts that the periodic X / Z axes are
+   * uniformly spaced; it falls back to multigrid where the topology does
+   * not allow it. */
+  int32_t geom_precond;
 } pf_plan_desc;
 
 typedef struct pf_plan pf_plan;
@@ -191,16 +200,22 @@ PF_API int pf_cg_solve(const pf_plan *plan, const double *a, const double *b,
                        void *workspace, void *mg_workspace,
                        pf_solver_report *report_host, void *stream);
 
-/* Geometric multigrid for the pressure operator of a box plan (the GPU
- * replacement of the reference's ILU(0) preconditioner, S/linalg.py:88-108):
- * Y-line block-Jacobi smoothing, X/Z semi-coarsening with Galerkin
- * aggregation, exact singular coarsest line solve.  pf_cg_solve with
- * precond == PF_PRECOND_MG uses the hierarchy last built by pf_mg_setup on
- * the same mg_workspace.  pf_mg_workspace_bytes returns 0 (and pf_mg_levels
- * 0) when the plan does not support it (gather topology, periodic line
- * axis). */
+/* Geometric preconditioner for the pressure operator of a box plan (the GPU
+ * replacement of the reference's ILU(0) preconditioner, S/linalg.py:88-108),
+ * one of:
+ *  - PF_GEOM_MULTIGRID: V(1,1) cycle, Y-line block-Jacobi smoothing, 2x
+ *    coarsening with Galerkin aggregation, exact singular coarsest line
+ *    solve;
+ *  - PF_GEOM_SPECTRAL (desc.geom_precond == PF_GEOM_SPECTRAL and periodic
+ *    power-of-two X / Z): exact inverse of the XZ-plane-averaged operator,
+ *    Fourier in X and Z, tridiagonal in Y.
+ * pf_cg_solve with precond == PF_PRECOND_MG uses the preconditioner last
+ * built by pf_mg_setup on the same mg_workspace.  pf_mg_workspace_bytes
+ * returns 0 (pf_mg_levels 0, pf_mg_kind PF_GEOM_NONE) when the plan supports
+ * neither (gather topology, periodic line axis). */
 PF_API int64_t pf_mg_workspace_bytes(const pf_plan *plan);
 PF_API int pf_mg_levels(const pf_plan *plan);
+PF_API int pf_mg_kind(const pf_plan *plan);
 PF_API int pf_mg_setup(const pf_plan *plan, const double *k,
                        void *mg_workspace, void *stream);
 
@@ -219,8 +234,9 @@ PF_API int pf_bicgstab_solve(const pf_plan *plan, const double *a, int32_t trans
  * on `stream`; average ms per iteration of:
  *   ms_host[0] SpMV + p.Ap   [1] x/r update + sums
  *   [2..6] multigrid level 0: line smooth | residual+restrict | all coarse
- *          levels | prolong+residual | line smooth with correction
- *          (precond == PF_PRECOND_MG; zero otherwise)
+ *          levels | prolong+residual | line smooth with correction; or
+ *          spectral: Z transform | X transform | Y solve | inverse X |
+ *          inverse Z (precond == PF_PRECOND_MG; zero otherwise)
  *   [7] z sums   [8] direction update   [9] whole iteration
  *   [10] whole iteration replayed from the cached CUDA graph (MG only).
  * Used by bench.py for the roofline figure. */

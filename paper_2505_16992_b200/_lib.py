@@ -20,6 +20,9 @@ c_ptr = ctypes.c_void_p
 
 PF_TOPO_GATHER = 0
 PF_TOPO_BOX = 1
+PF_GEOM_NONE = -1
+PF_GEOM_MULTIGRID = 0
+PF_GEOM_SPECTRAL = 1
 PF_BKIND_DIRICHLET = 0
 PF_BKIND_OUTFLOW = 1
 
@@ -35,6 +38,7 @@ class PlanDesc(ctypes.Structure):
         ("bt", c_ptr), ("balpha", c_ptr),
         ("alpha_full", c_ptr), ("balpha_row", c_ptr), ("bfid", c_ptr),
         ("finfo", c_ptr), ("nfaces", c_int), ("has_cross", c_int),
+        ("geom_precond", c_int),
     ]
 
 
@@ -67,6 +71,7 @@ _SIGS = {
                     c_ptr],
     "pf_mg_workspace_bytes": [c_ptr],
     "pf_mg_levels": [c_ptr],
+    "pf_mg_kind": [c_ptr],
     "pf_mg_setup": [c_ptr, c_ptr, c_ptr, c_ptr],
     "pf_bicgstab_solve": [c_ptr, c_ptr, c_int, c_int, c_ptr, c_ptr, c_int,
                           c_dbl, c_int, c_int, c_ptr,

@@ -56,11 +56,26 @@ struct MgLevel {
   double *r, *x, *t;     // level rhs, solution, scratch
 };
 
+// Spectral preconditioner of a box with periodic, uniformly spaced X and Z
+// (see spectral.cuh): exact inverse of the XZ-plane-averaged operator.
+struct SpecPlan {
+  int32_t sx, sy, sz;  // canonical dims (sx == 1 in 2D)
+  int32_t nkz;         // sz / 2 + 1 retained Z wavenumbers
+  int32_t lpx, lpz;    // lines per CTA of the X / Z transforms
+  double2 *s;          // (sy, nkz, sx) spectral work array
+  double *cw;          // (sy, nkz * sx) Thomas c' scratch
+  double *ax, *ay, *az;  // (sy) plane-mean face weights
+  double2 *twx, *twz;    // exp(-2 pi i k / N), N = sx, sz
+  double *lx, *lz;       // 2 - 2 cos(2 pi k / N)
+};
+
 struct MgHierarchy {
   int nlev;
   int ax_of[3];  // physical axis of canonical X, Y, Z (-1: absent)
   MgLevel lv[kMgMaxLevels];
   double omega;   // damping of the block-Jacobi line smoother
+  int spectral;   // level 0 only, preconditioned by the spectral solve
+  SpecPlan sp;
 };
 
 

@@ -7,6 +7,7 @@
 
 #include "cgstate.cuh"
 #include "mg.cuh"
+#include "spectral.cuh"
 
 namespace pf {
 
@@ -374,9 +375,15 @@ __global__ void __launch_bounds__(kBlock)
 // ---------------------------------------------------------------------------
 // host side
 
+// level-0 face weights of the spectral mode, padded for the arrays after it
+static int64_t spec_level0_bytes(int64_t n) {
+  return (3 * n * 8 + 255) / 256 * 256;
+}
+
 bool mg_plan(const Plan &p, MgHierarchy &h, int64_t *bytes) {
   h.nlev = 0;
   h.omega = 0.85;
+  h.spectral = 0;
   *bytes = 0;
   if (p.d.topo != PF_TOPO_BOX) return false;
   const int d = p.d.dim;
@@ -403,6 +410,24 @@ bool mg_plan(const Plan &p, MgHierarchy &h, int64_t *bytes) {
     if (p.d.box_periodic[0]) return false;
   }
   if (sy < 2 || (sx <= 1 && sz <= 1)) return false;
+  h.spectral = 0;
+  if (p.d.geom_precond == PF_GEOM_SPECTRAL && spec_ok(d, sx, sy, sz, px, pz)) {
+    // level 0 face weights + the spectral solve, no coarse levels
+    MgLevel &L = h.lv[0];
+    L = MgLevel{};
+    L.sx = sx;
+    L.sy = sy;
+    L.sz = sz;
+    L.px = px;
+    L.pz = pz;
+    L.n = (int64_t)sx * sy * sz;
+    L.fx = L.fy = L.fz = 1;
+    h.nlev = 1;
+    h.spectral = 1;
+    spec_plan(h.sp, sx, sy, sz);
+    *bytes = spec_level0_bytes(L.n) + spec_bytes(h.sp);
+    return true;
+  }
   int64_t total = 0;
   for (;;) {
     MgLevel &L = h.lv[h.nlev];
@@ -434,6 +459,15 @@ bool mg_plan(const Plan &p, MgHierarchy &h, int64_t *bytes) {
 
 void mg_bind(MgHierarchy &h, void *base) {
   double *q = static_cast<double *>(base);
+  if (h.spectral) {
+    MgLevel &L = h.lv[0];
+    L.wx = q;
+    L.wy = q + L.n;
+    L.wz = q + 2 * L.n;
+    L.cp = L.ivd = L.t = L.r = L.x = nullptr;
+    spec_bind(h.sp, static_cast<char *>(base) + spec_level0_bytes(L.n));
+    return;
+  }
   for (int k = 0; k < h.nlev; ++k) {
     MgLevel &L = h.lv[k];
     L.wx = q;
@@ -467,6 +501,7 @@ int mg_setup(const MgHierarchy &h, const double *k, int64_t n, cudaStream_t s,
              const int *done) {
   launch(k_mg_faces0, grid_for(n), kBlock, s, h.lv[0], k, n, h.ax_of[0],
          h.ax_of[1], h.ax_of[2], done);
+  if (h.spectral) return spec_setup(h.lv[0], h.sp, s, done);
   for (int l = 0; l + 1 < h.nlev; ++l)
     launch(k_mg_aggregate, grid_for(h.lv[l + 1].n), kBlock, s, h.lv[l],
            h.lv[l + 1], done);
@@ -525,6 +560,8 @@ int mg_apply(const MgHierarchy &h, const double *r, double *z, cudaStream_t s,
   MgHierarchy hh = h;
   hh.lv[0].r = const_cast<double *>(r);
   hh.lv[0].x = z;
+  if (hh.spectral)
+    return spec_apply(hh.lv[0], hh.sp, r, z, s, done, ev, fuse, red_blocks);
   int fused_from = hh.nlev;
   for (int l = 1; l < hh.nlev; ++l)
     if (hh.lv[l].n <= kFusedCoarseMax) {

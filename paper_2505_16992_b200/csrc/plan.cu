@@ -115,6 +115,13 @@ extern "C" int pf_mg_levels(const pf_plan *plan) {
   return p.has_mg ? p.mg.nlev : 0;
 }
 
+extern "C" int pf_mg_kind(const pf_plan *plan) {
+  if (!plan) return PF_GEOM_NONE;
+  const Plan &p = *reinterpret_cast<const Plan *>(plan);
+  if (!p.has_mg) return PF_GEOM_NONE;
+  return p.mg.spectral ? PF_GEOM_SPECTRAL : PF_GEOM_MULTIGRID;
+}
+
 extern "C" int pf_mg_setup(const pf_plan *plan, const double *k,
                            void *mg_workspace, void *stream) {
   if (!plan || !k || !mg_workspace) {

@@ -1,0 +1,443 @@
+// spectral.cu -- FFT / tridiagonal preconditioner (see spectral.cuh).
+#include <algorithm>
+
+#include "mg.cuh"
+#include "spectral.cuh"
+
+namespace pf {
+
+constexpr int kFftThreads = 256;
+constexpr int kFftElems = 1024;  // complex elements per CTA buffer (16 KB)
+constexpr int kYThreads = 128;
+
+#define SPEC_DONE_RETURN \
+  if (done && *done) return
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) {
+  return make_double2(a.x - b.x, a.y - b.y);
+}
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+template <bool kInv>
+__device__ __forceinline__ double2 twiddle(const double2 *tw, int k) {
+  double2 w = __ldg(tw + k);
+  if (kInv) w.y = -w.y;
+  return w;
+}
+
+// Stockham autosort FFT (radix 4, a final radix-2 stage when log2 N is odd)
+// of `nl` lines of length N held in shared memory, line stride N; b is
+// scratch of the same size.  Returns the buffer holding the natural-order
+// result.  Forward: exp(-2 pi i jk / N); inverse: exp(+...), unnormalised.
+template <bool kInv>
+__device__ double2 *fft_lines(double2 *a, double2 *b, int N, int nl,
+                              const double2 *tw) {
+  const int q4 = N >> 2;
+  int n = N, ls = 0;  // current length, log2 of the stride
+  while (n >= 4) {
+    const int n1 = n >> 2, s = 1 << ls;
+    for (int t = threadIdx.x; t < nl * q4; t += blockDim.x) {
+      const int line = t / q4;
+      const int k = t - line * q4;
+      const int q = k & (s - 1), p = k >> ls;
+      const double2 *x = a + line * N;
+      double2 *y = b + line * N;
+      const double2 x0 = x[q + s * p], x1 = x[q + s * (p + n1)];
+      const double2 x2 = x[q + s * (p + 2 * n1)];
+      const double2 x3 = x[q + s * (p + 3 * n1)];
+      const double2 apc = cadd(x0, x2), amc = csub(x0, x2);
+      const double2 bpd = cadd(x1, x3), bmd = csub(x1, x3);
+      // forward: j (b - d) with j = i; the inverse flips its sign
+      const double2 jb = kInv ? make_double2(bmd.y, -bmd.x)
+                              : make_double2(-bmd.y, bmd.x);
+      const int ps = p << ls;
+      y[q + s * (4 * p)] = cadd(apc, bpd);
+      y[q + s * (4 * p + 1)] = cmul(twiddle<kInv>(tw, ps), csub(amc, jb));
+      y[q + s * (4 * p + 2)] = cmul(twiddle<kInv>(tw, 2 * ps), csub(apc, bpd));
+      y[q + s * (4 * p + 3)] = cmul(twiddle<kInv>(tw, 3 * ps), cadd(amc, jb));
+    }
+    __syncthreads();
+    double2 *tmp = a;
+    a = b;
+    b = tmp;
+    n >>= 2;
+    ls += 2;
+  }
+  if (n == 2) {
+    const int s = N >> 1;
+    for (int t = threadIdx.x; t < nl * s; t += blockDim.x) {
+      const int line = t / s;
+      const int q = t - line * s;
+      const double2 *x = a + line * N;
+      double2 *y = b + line * N;
+      const double2 x0 = x[q], x1 = x[q + s];
+      y[q] = cadd(x0, x1);
+      y[q + s] = csub(x0, x1);
+    }
+    __syncthreads();
+    a = b;
+  }
+  return a;
+}
+
+// first element of the Z line number l (lines enumerated X fastest, then Y)
+__device__ __forceinline__ int64_t zline_base(const SpecPlan &sp, int64_t l) {
+  const int64_t x = l % sp.sx, y = l / sp.sx;
+  return (x * sp.sy + y) * sp.sz;
+}
+
+__device__ __forceinline__ int64_t spec_index(const SpecPlan &sp, int64_t l,
+                                              int kz) {
+  const int64_t x = l % sp.sx, y = l / sp.sx;
+  return (y * sp.nkz + kz) * sp.sx + x;
+}
+
+// pass 1: real FFT along Z, two real lines per complex transform
+__global__ void __launch_bounds__(kFftThreads)
+    k_spec_fwd_z(SpecPlan sp, const double *__restrict__ r, const int *done) {
+  SPEC_DONE_RETURN;
+  extern __shared__ double2 sm[];
+  const int N = sp.sz, LP = sp.lpz, nk = sp.nkz;
+  const int64_t npairs = (int64_t)sp.sx * sp.sy / 2;
+  const int64_t ntiles = (npairs + LP - 1) / LP;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t g0 = tile * LP;
+    for (int e = threadIdx.x; e < LP * N; e += blockDim.x) {
+      const int j = e / N, z = e - j * N;
+      const int64_t g = g0 + j;
+      double2 v = make_double2(0.0, 0.0);
+      if (g < npairs) {
+        v.x = r[zline_base(sp, 2 * g) + z];
+        v.y = r[zline_base(sp, 2 * g + 1) + z];
+      }
+      sm[e] = v;
+    }
+    __syncthreads();
+    const double2 *f = fft_lines<false>(sm, sm + LP * N, N, LP, sp.twz);
+    for (int e = threadIdx.x; e < 2 * LP * nk; e += blockDim.x) {
+      const int kz = e / (2 * LP), jj = e - kz * 2 * LP;
+      const int j = jj >> 1, side = jj & 1;
+      const int64_t g = g0 + j;
+      if (g >= npairs) continue;
+      const double2 zk = f[j * N + kz];
+      const double2 zm = f[j * N + ((N - kz) & (N - 1))];
+      // Z = A + iB with A, B the transforms of the two real lines
+      const double2 o =
+          side == 0 ? make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y))
+                    : make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+      sp.s[spec_index(sp, 2 * g + side, kz)] = o;
+    }
+    __syncthreads();
+  }
+}
+
+// passes 2 / 4: complex FFT along X, in place on the work array
+template <bool kInv>
+__global__ void __launch_bounds__(kFftThreads)
+    k_spec_x(SpecPlan sp, const int *done) {
+  SPEC_DONE_RETURN;
+  extern __shared__ double2 sm[];
+  const int N = sp.sx, LP = sp.lpx;
+  const int64_t nlines = (int64_t)sp.sy * sp.nkz;
+  const int64_t ntiles = (nlines + LP - 1) / LP;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t l0 = tile * LP;
+    const int64_t nl = nlines - l0 < LP ? nlines - l0 : LP;
+    double2 *src = sp.s + l0 * N;
+    for (int e = threadIdx.x; e < LP * N; e += blockDim.x)
+      sm[e] = e < nl * N ? src[e] : make_double2(0.0, 0.0);
+    __syncthreads();
+    const double2 *f = fft_lines<kInv>(sm, sm + LP * N, N, LP, sp.twx);
+    for (int e = threadIdx.x; e < nl * N; e += blockDim.x) src[e] = f[e];
+    __syncthreads();
+  }
+}
+
+// pass 3: per wavenumber pair (kx, kz) the tridiagonal Y system
+//   (ax lx + az lz + ay- + ay+) z_y - ay- z_{y-1} - ay+ z_{y+1} = rhs_y,
+// one thread per real / imaginary part (the coefficients are real); the
+// forward sweep overwrites the work array in place, the real lane keeps c'.
+// The 1 / (sx sz) normalisation of the transforms is folded in here.
+__global__ void __launch_bounds__(kYThreads)
+    k_spec_ysolve(SpecPlan sp, const int *done) {
+  SPEC_DONE_RETURN;
+  extern __shared__ double sh[];
+  const int sy = sp.sy;
+  double *ax = sh, *ay = sh + sy, *az = sh + 2 * sy;
+  for (int y = threadIdx.x; y < sy; y += blockDim.x) {
+    ax[y] = sp.ax[y];
+    ay[y] = y + 1 < sy ? sp.ay[y] : 0.0;
+    az[y] = sp.az[y];
+  }
+  __syncthreads();
+  const int64_t ncol = (int64_t)sp.nkz * sp.sx;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = t < 2 * ncol;
+  const int64_t col = t >> 1;
+  const int comp = (int)(t & 1);
+  const int kx = (int)(col % sp.sx), kz = (int)(col / sp.sx);
+  const double lxv = active ? sp.lx[kx] : 0.0;
+  const double lzv = active ? sp.lz[kz] : 0.0;
+  const bool pinned = col == 0;
+  const double scale = 1.0 / ((double)sp.sx * sp.sz);
+  double *sv = reinterpret_cast<double *>(sp.s);
+  const int64_t ystride = 2 * ncol;
+  constexpr int C = 8;
+  if (active) {
+    double dp = 0.0, cprev = 0.0;
+    for (int y0 = 0; y0 < sy; y0 += C) {
+      double rr[C];
+#pragma unroll
+      for (int k = 0; k < C; ++k)
+        if (y0 + k < sy) rr[k] = sv[(int64_t)(y0 + k) * ystride + t];
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        const int y = y0 + k;
+        if (y >= sy) break;
+        const double lo = y > 0 ? ay[y - 1] : 0.0, up = ay[y];
+        double c = 0.0;
+        if (pinned && y == sy - 1) {
+          dp = 0.0;
+        } else {
+          const double den = ax[y] * lxv + az[y] * lzv + lo + up + lo * cprev;
+          const double iv = 1.0 / den;
+          c = -up * iv;
+          dp = (rr[k] * scale + lo * dp) * iv;
+        }
+        cprev = c;
+        sv[(int64_t)y * ystride + t] = dp;
+        if (comp == 0) sp.cw[(int64_t)y * ncol + col] = c;
+      }
+    }
+  }
+  __syncwarp();
+  if (active) {
+    double zn = 0.0;
+    for (int y0 = sy - 1; y0 >= 0; y0 -= C) {
+      double dd[C], cc[C];
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        const int y = y0 - k;
+        if (y >= 0) {
+          dd[k] = sv[(int64_t)y * ystride + t];
+          cc[k] = sp.cw[(int64_t)y * ncol + col];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        const int y = y0 - k;
+        if (y < 0) break;
+        zn = dd[k] - cc[k] * zn;
+        sv[(int64_t)y * ystride + t] = zn;
+      }
+    }
+  }
+}
+
+// pass 5: inverse real FFT along Z (two lines per complex transform), z
+// written in the cell layout; optionally the CG z-sums and beta
+template <bool kSums>
+__global__ void __launch_bounds__(kFftThreads)
+    k_spec_inv_z(SpecPlan sp, const double *__restrict__ r,
+                 double *__restrict__ z, CgFuse fz, const int *done) {
+  SPEC_DONE_RETURN;
+  extern __shared__ double2 sm[];
+  const int N = sp.sz, LP = sp.lpz, half = N >> 1;
+  const int64_t npairs = (int64_t)sp.sx * sp.sy / 2;
+  const int64_t ntiles = (npairs + LP - 1) / LP;
+  double sums[3] = {0.0, 0.0, 0.0};
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t g0 = tile * LP;
+    for (int e = threadIdx.x; e < LP * N; e += blockDim.x) {
+      const int k = e / LP, j = e - k * LP;
+      const int64_t g = g0 + j;
+      double2 v = make_double2(0.0, 0.0);
+      if (g < npairs) {
+        const int kk = k <= half ? k : N - k;
+        const double2 a = sp.s[spec_index(sp, 2 * g, kk)];
+        const double2 b = sp.s[spec_index(sp, 2 * g + 1, kk)];
+        v = k <= half ? make_double2(a.x - b.y, a.y + b.x)
+                      : make_double2(a.x + b.y, b.x - a.y);
+      }
+      sm[j * N + k] = v;
+    }
+    __syncthreads();
+    const double2 *f = fft_lines<true>(sm, sm + LP * N, N, LP, sp.twz);
+    for (int e = threadIdx.x; e < LP * N; e += blockDim.x) {
+      const int j = e / N, zz = e - j * N;
+      const int64_t g = g0 + j;
+      if (g >= npairs) continue;
+      const double2 v = f[e];
+      const int64_t i0 = zline_base(sp, 2 * g) + zz;
+      const int64_t i1 = zline_base(sp, 2 * g + 1) + zz;
+      z[i0] = v.x;
+      z[i1] = v.y;
+      if (kSums) {
+        const double r0 = r[i0], r1 = r[i1];
+        sums[0] += v.x + v.y;
+        sums[1] += r0 * v.x + r1 * v.y;
+        sums[2] += r0 + r1;
+      }
+    }
+    __syncthreads();
+  }
+  if (kSums) {
+    double tot[3];
+    if (grid_reduce<3>(sums, fz.partials, fz.counter, tot))
+      cg_fin_z(fz.st, tot[0], tot[1], tot[2], sp.sx * sp.sy * sp.sz,
+               fz.initial != 0);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// setup
+
+__global__ void __launch_bounds__(kBlock) k_spec_tables(SpecPlan sp) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  double s, c;
+  if (t < sp.sx) {
+    sincospi(2.0 * t / sp.sx, &s, &c);
+    sp.twx[t] = make_double2(c, -s);
+    sp.lx[t] = sp.sx > 1 ? 2.0 - 2.0 * c : 0.0;
+  }
+  if (t < sp.sz) {
+    sincospi(2.0 * t / sp.sz, &s, &c);
+    sp.twz[t] = make_double2(c, -s);
+    if (t < sp.nkz) sp.lz[t] = 2.0 - 2.0 * c;
+  }
+}
+
+// plane means of the level-0 face weights, one CTA per Y plane
+__global__ void __launch_bounds__(kBlock)
+    k_spec_planes(MgLevel L, SpecPlan sp, const int *done) {
+  SPEC_DONE_RETURN;
+  const int y = blockIdx.x;
+  double v[3] = {0.0, 0.0, 0.0};
+  const int64_t m = (int64_t)L.sx * L.sz;
+  for (int64_t e = threadIdx.x; e < m; e += blockDim.x) {
+    const int64_t x = e / L.sz, zz = e - x * L.sz;
+    const int64_t i = (x * L.sy + y) * L.sz + zz;
+    v[0] += L.wx[i];
+    v[1] += L.wy[i];
+    v[2] += L.wz[i];
+  }
+  block_reduce<3>(v);
+  if (threadIdx.x == 0) {
+    sp.ax[y] = v[0] / m;
+    sp.ay[y] = v[1] / m;
+    sp.az[y] = v[2] / m;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+static bool pow2_in(int n, int lo, int hi) {
+  return n >= lo && n <= hi && (n & (n - 1)) == 0;
+}
+
+bool spec_ok(int dim, int sx, int sy, int sz, int px, int pz) {
+  if (!pz || !pow2_in(sz, 4, kFftElems) || sy < 2) return false;
+  if (dim == 3) return px && pow2_in(sx, 2, kFftElems);
+  return sx == 1 && sy % 2 == 0;
+}
+
+void spec_plan(SpecPlan &sp, int sx, int sy, int sz) {
+  sp = SpecPlan{};
+  sp.sx = sx;
+  sp.sy = sy;
+  sp.sz = sz;
+  sp.nkz = sz / 2 + 1;
+  sp.lpx = std::max(1, kFftElems / sx);
+  sp.lpz = std::max(1, kFftElems / sz);
+}
+
+static int64_t al(int64_t b) { return (b + 255) / 256 * 256; }
+
+int64_t spec_bytes(const SpecPlan &sp) {
+  const int64_t ns = (int64_t)sp.sy * sp.nkz * sp.sx;
+  return al(ns * 16) + al(ns * 8) + 3 * al(sp.sy * 8) + al(sp.sx * 16) +
+         al(sp.sz * 16) + al(sp.sx * 8) + al(sp.nkz * 8);
+}
+
+char *spec_bind(SpecPlan &sp, char *q) {
+  const int64_t ns = (int64_t)sp.sy * sp.nkz * sp.sx;
+  sp.s = reinterpret_cast<double2 *>(q);
+  q += al(ns * 16);
+  sp.cw = reinterpret_cast<double *>(q);
+  q += al(ns * 8);
+  sp.ax = reinterpret_cast<double *>(q);
+  q += al(sp.sy * 8);
+  sp.ay = reinterpret_cast<double *>(q);
+  q += al(sp.sy * 8);
+  sp.az = reinterpret_cast<double *>(q);
+  q += al(sp.sy * 8);
+  sp.twx = reinterpret_cast<double2 *>(q);
+  q += al(sp.sx * 16);
+  sp.twz = reinterpret_cast<double2 *>(q);
+  q += al(sp.sz * 16);
+  sp.lx = reinterpret_cast<double *>(q);
+  q += al(sp.sx * 8);
+  sp.lz = reinterpret_cast<double *>(q);
+  q += al(sp.nkz * 8);
+  return q;
+}
+
+int spec_setup(const MgLevel &l0, const SpecPlan &sp, cudaStream_t s,
+               const int *done) {
+  launch(k_spec_tables, grid_for(std::max(sp.sx, sp.sz)), kBlock, s, sp);
+  launch(k_spec_planes, sp.sy, kBlock, s, l0, sp, done);
+  PF_LAUNCH_CHECK("spec_setup");
+  return PF_OK;
+}
+
+template <typename... KArgs, typename... Args>
+static void launch_smem(void (*kernel)(KArgs...), int grid, int block,
+                        size_t smem, cudaStream_t stream, Args... args) {
+  ++g_launches;
+  kernel<<<grid, block, smem, stream>>>(args...);
+}
+
+int spec_apply(const MgLevel &l0, const SpecPlan &sp, const double *r,
+               double *z, cudaStream_t s, const int *done, cudaEvent_t *ev,
+               const CgFuse *fuse, int red_blocks) {
+  (void)l0;
+  auto mark = [&](int k) {
+    if (ev) cudaEventRecord(ev[k], s);
+  };
+  const int64_t npairs = (int64_t)sp.sx * sp.sy / 2;
+  const int zt = (int)std::min<int64_t>((npairs + sp.lpz - 1) / sp.lpz,
+                                        1 << 20);
+  const size_t zsm = 2 * sizeof(double2) * sp.lpz * sp.sz;
+  const int64_t xlines = (int64_t)sp.sy * sp.nkz;
+  const int xt = (int)std::min<int64_t>((xlines + sp.lpx - 1) / sp.lpx,
+                                        1 << 20);
+  const size_t xsm = 2 * sizeof(double2) * sp.lpx * sp.sx;
+  const int64_t ncol2 = 2 * (int64_t)sp.nkz * sp.sx;
+  mark(0);
+  launch_smem(k_spec_fwd_z, zt, kFftThreads, zsm, s, sp, r, done);
+  mark(1);
+  if (sp.sx > 1) launch_smem(k_spec_x<false>, xt, kFftThreads, xsm, s, sp, done);
+  mark(2);
+  launch_smem(k_spec_ysolve, grid_for(ncol2, kYThreads), kYThreads,
+              3 * sizeof(double) * sp.sy, s, sp, done);
+  mark(3);
+  if (sp.sx > 1) launch_smem(k_spec_x<true>, xt, kFftThreads, xsm, s, sp, done);
+  mark(4);
+  if (fuse && fuse->st)
+    launch_smem(k_spec_inv_z<true>, std::min(zt, red_blocks), kFftThreads,
+                zsm, s, sp, r, z, *fuse, done);
+  else
+    launch_smem(k_spec_inv_z<false>, zt, kFftThreads, zsm, s, sp, r, z,
+                CgFuse{nullptr, nullptr, nullptr, 0}, done);
+  mark(5);
+  PF_LAUNCH_CHECK("spec_apply");
+  return PF_OK;
+}
+
+}  // namespace pf

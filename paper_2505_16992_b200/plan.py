@@ -24,8 +24,28 @@ import torch
 from . import _lib
 
 
+def _spectral_allowed(domain, box, sep):
+    """The spectral pressure preconditioner needs a single box whose
+    non-line axes (all but the first in 2D, X and Z in 3D) are periodic and
+    uniformly spaced; the C library checks the topology (power-of-two
+    periodic X / Z), the spacing is asserted here."""
+    if box is None or sep is None:
+        return False
+    shape, periodic = box
+    axes = [1] if domain.dim == 2 else [0, 2]
+    for a in axes:
+        h = np.asarray(sep[a], dtype=np.float64)
+        if not periodic[a] or np.ptp(h) > 1e-12 * np.abs(h).max():
+            return False
+    return True
+
+
 class DevicePlan:
-    def __init__(self, domain, device):
+    """``geom_precond``: "auto" (spectral where the box allows it, else
+    multigrid), "multigrid" or "spectral" (falls back to multigrid when the
+    box does not allow it)."""
+
+    def __init__(self, domain, device, geom_precond="auto"):
         _lib.require_cuda(device)
         self.domain = domain
         self.device = device
@@ -151,6 +171,12 @@ class DevicePlan:
                 desc.bfid = self.bfid.data_ptr()
                 desc.finfo = self.finfo.data_ptr()
                 desc.nfaces = len(faces)
+        if geom_precond not in ("auto", "multigrid", "spectral"):
+            raise ValueError(f"geom_precond {geom_precond!r}")
+        desc.geom_precond = (
+            _lib.PF_GEOM_SPECTRAL
+            if geom_precond != "multigrid" and _spectral_allowed(domain, box, sep)
+            else _lib.PF_GEOM_MULTIGRID)
         self._desc = desc
         handle = ctypes.c_void_p()
         with torch.cuda.device(device):
@@ -161,6 +187,9 @@ class DevicePlan:
                                          device=device)
             self.mg_bytes = int(_lib.load().pf_mg_workspace_bytes(handle))
             self.mg_levels = int(_lib.load().pf_mg_levels(handle))
+            kind = int(_lib.load().pf_mg_kind(handle))
+        self.geom_kind = {_lib.PF_GEOM_MULTIGRID: "multigrid",
+                          _lib.PF_GEOM_SPECTRAL: "spectral"}.get(kind)
         self.mg_workspace = None
         self._mg_key = None
 
