@@ -260,6 +260,13 @@ KERNEL_BYTES = {
     "k_spec_inv_z + CG z-sums": 24,  # spectrum, r read; z written
 }
 
+# batched BiCGStab (3 components sharing the 7-row stencil C, Jacobi):
+# pv: C rows 56 + per comp r, p, v, rhat read, p', v' written (48)
+# st: C rows 56 + per comp r, v read, t written (24)
+# xr: diag 8 + per comp x r/w, p, r, v, t, rhat read, r written (64)
+BI_BYTES = {"k_bi_pv": 56 + 3 * 48, "k_bi_st": 56 + 3 * 24,
+            "k_bi_xr": 8 + 3 * 64}
+
 MG_NAMES = ["k_mg_smooth0 (level 0)", "k_mg_resid_restrict (level 0)",
             "mg coarse levels", "k_mg_prolong_resid (level 0)",
             "k_mg_smooth2_cg (level 0)", "zsum (fused into smooth2)"]
@@ -268,10 +275,22 @@ SPEC_NAMES = ["k_spec_fwd_z", "k_spec_x (forward)", "k_spec_ysolve",
               "zsum (fused into inv_z)"]
 
 
-def measure_roofline(args, dom, plan, state, nu, dt, dev):
-    """Per-kernel live timing of the production pressure-CG iteration on this
-    step's operator (CUDA events on the launching stream, pf_cg_profile);
-    the roofline entry is the kernel with the largest time share."""
+def _lockstep(reports, prefix, d):
+    """Lock-step iterations of the batched BiCGStab solves whose stage
+    label starts with `prefix` (the d components of one solve run
+    together, so a solve costs max over its components)."""
+    its = [r.iterations for r in reports if r.stage.startswith(prefix)]
+    return sum(max(its[k:k + d]) for k in range(0, len(its), d))
+
+
+def measure_roofline(args, dom, plan, state, nu, dt, dev, per_step):
+    """Live per-kernel timing (CUDA events on the launching stream) of the
+    two solver iterations that make up most of the step -- the batched
+    BiCGStab of the momentum predictor and its adjoint (pf_bicgstab_profile)
+    and the preconditioned pressure CG (pf_cg_profile) -- on this step's
+    operators.  Each kernel's share of the step is its per-launch time x
+    launches per step (from the step's own iteration counts) / step time;
+    the roofline entry is the kernel with the largest share."""
     import ctypes
     import torch
     from paper_2505_16992_b200 import _lib
@@ -291,11 +310,19 @@ def measure_roofline(args, dom, plan, state, nu, dt, dev):
     names = (["k_cg_spmv_faces" if mg else "k_cg_spmv", "k_cg_update"]
              + ((SPEC_NAMES if plan.geom_kind == "spectral" else MG_NAMES)
                 if mg else [None] * 6) + ["k_cg_pupdate"])
-    idx = [0, 1, 2, 3, 4, 5, 6, 7, 8]
-    per = {}
-    for j, nm in zip(idx, names):
-        if nm is not None:
-            per[nm] = float(ms[j])
+    cg = {}
+    for j, nm in enumerate(names):
+        if nm is not None and nm in KERNEL_BYTES and ms[j] > 0:
+            cg[nm] = float(ms[j])
+    d = dom.dim
+    bb = torch.randn((d, dom.n), dtype=torch.float64, device=dev)
+    bi = {}
+    for trans, tag in ((0, ""), (1, " (adjoint)")):
+        bm = (ctypes.c_double * 4)()
+        _lib.call("pf_bicgstab_profile", plan.handle, _lib.ptr(c), trans, d,
+                  _lib.ptr(bb), 8, _lib.ptr(plan.workspace), bm, plan.stream)
+        for j, nm in enumerate(("k_bi_pv", "k_bi_st", "k_bi_xr")):
+            bi[nm + tag] = float(bm[j])
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -304,12 +331,20 @@ def measure_roofline(args, dom, plan, state, nu, dt, dev):
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
     n = dom.n
-    cand = {k: v for k, v in per.items() if k in KERNEL_BYTES and v > 0}
-    top = max(cand, key=cand.get)
-    top_gbs = KERNEL_BYTES[top] * n / (cand[top] * 1e-3) / 1e9
-    it_ms = float(ms[9])
-    it_bytes = sum(KERNEL_BYTES[k] for k in cand)
-    fine_ms = sum(cand.values())
+    launches = {}
+    for nm in bi:
+        launches[nm] = per_step["bi_adj" if "adjoint" in nm else "bi_fwd"]
+    for nm in cg:
+        launches[nm] = per_step["cg"]
+    allk = dict(cg)
+    allk.update(bi)
+
+    def nbytes(nm):
+        return BI_BYTES.get(nm.replace(" (adjoint)", ""), KERNEL_BYTES.get(nm))
+
+    share = {nm: allk[nm] * launches[nm] / per_step["ms"] for nm in allk}
+    top = max(share, key=share.get)
+    gbs = {nm: nbytes(nm) * n / (allk[nm] * 1e-3) / 1e9 for nm in allk}
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -317,18 +352,22 @@ def measure_roofline(args, dom, plan, state, nu, dt, dev):
             traffic = json.load(open(tpath)).get(args.config, {}).get(top)
         except (OSError, ValueError, AttributeError):
             traffic = None
-    return {"bound": "hbm", "kernel": top, "achieved": top_gbs, "peak": peak,
-            "unit": "GB/s", "frac": top_gbs / peak, "traffic": traffic,
-            "peak_source": peak_src, "bytes_per_cell": KERNEL_BYTES[top],
-            "cells_per_launch": n, "ms_per_launch": cand[top],
+    it_ms = float(ms[9])
+    return {"bound": "hbm", "kernel": top, "achieved": gbs[top], "peak": peak,
+            "unit": "GB/s", "frac": gbs[top] / peak, "traffic": traffic,
+            "peak_source": peak_src, "bytes_per_cell": nbytes(top),
+            "cells_per_launch": n, "ms_per_launch": allk[top],
+            "share_of_step": share[top],
+            "kernels": {nm: {"ms_per_launch": allk[nm],
+                             "launches_per_step": launches[nm],
+                             "share_of_step": share[nm],
+                             "bytes_per_cell": nbytes(nm),
+                             "achieved_gbs": gbs[nm],
+                             "frac": gbs[nm] / peak}
+                        for nm in sorted(allk, key=lambda x: -share[x])},
             "pressure_cg_iteration": {
                 "preconditioner": plan.geom_kind if mg else "jacobi",
-                "ms": it_ms, "ms_graph_replay": float(ms[10]),
-                "level0_and_cg_ms": fine_ms,
-                "level0_and_cg_bytes_per_cell": it_bytes,
-                "level0_and_cg_achieved_gbs":
-                    it_bytes * n / (fine_ms * 1e-3) / 1e9,
-                "ms_per_kernel": per}}
+                "ms": it_ms, "ms_graph_replay": float(ms[10])}}
 
 
 def run_c5train(args, world, rank, local, dev):
@@ -442,7 +481,8 @@ def main():
     cot = adjoint.GradState(u=w, p=torch.zeros(dom.n, dtype=torch.float64,
                                                device=dev))
     ws = piso.PisoWorkspace(dom)
-    stats = {"mom": 0, "p": 0, "adj": 0, "steps": 0}
+    stats = {"mom": 0, "p": 0, "adj": 0, "steps": 0, "bi_fwd": 0,
+             "bi_adj": 0, "cg": 0}
 
     def step(state):
         cfg = piso.StepConfig(dt=dt, nu=nu, source=forcing(state.u, nu),
@@ -453,6 +493,12 @@ def main():
         stats["mom"] += dg.momentum_iterations
         stats["p"] += dg.pressure_iterations
         stats["adj"] += g.solve_iterations
+        stats["bi_fwd"] += _lockstep(dg.reports, "momentum[", dom.dim)
+        stats["bi_adj"] += _lockstep(g.reports or [], "adjoint_momentum",
+                                     dom.dim)
+        stats["cg"] += (dg.pressure_iterations
+                        + sum(r.iterations for r in (g.reports or [])
+                              if r.stage.startswith("adjoint_pressure")))
         stats["steps"] += 1
         return new, g
 
@@ -487,7 +533,7 @@ def main():
     ms_step = ms / args.steps
     value = world * dom.n * args.steps / (ms / 1e3) / 1e6
     it_per_step = {k: stats[k] / max(stats["steps"], 1)
-                   for k in ("mom", "p", "adj")}
+                   for k in ("mom", "p", "adj", "bi_fwd", "bi_adj", "cg")}
 
     # end to end through the public API with host buffers
     u_host = state.u.detach().cpu().pin_memory()
@@ -518,7 +564,11 @@ def main():
         ms_e2e = float(t.item())
     e2e_value = world * dom.n * args.steps / (ms_e2e / 1e3) / 1e6
 
-    roofline = measure_roofline(args, dom, plan, state, nu, dt, dev)
+    per_step = {k: stats[k] / max(stats["steps"], 1)
+                for k in ("bi_fwd", "bi_adj", "cg")}
+    per_step["ms"] = ms_step
+    roofline = measure_roofline(args, dom, plan, state, nu, dt, dev,
+                                per_step)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

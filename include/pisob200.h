@@ -245,6 +245,16 @@ PF_API int pf_cg_profile(const pf_plan *plan, const double *a,
                          void *workspace, void *mg_workspace,
                          double *ms_host, void *stream);
 
+/* Live per-pass timing of the batched BiCGStab iteration (bench.py roofline):
+ * `iters` Jacobi-preconditioned iterations on `ncomp` right-hand sides of the
+ * operator a (transposed if `transpose`), each pass bracketed by CUDA events
+ * on `stream`.  ms_host[0..3] = mean ms of pass pv, pass st, pass xr and the
+ * whole iteration.  Not part of the reference interface. */
+PF_API int pf_bicgstab_profile(const pf_plan *plan, const double *a,
+                               int32_t transpose, int32_t ncomp,
+                               const double *b, int32_t iters,
+                               void *workspace, double *ms_host, void *stream);
+
 /* ---- adjoint stage kernels (S/adjoint.py) --------------------------------- */
 
 /* backward_correct_velocity, S/adjoint.py:78-91: dA += (cu . T^t g)/A^2,

@@ -78,6 +78,8 @@ _SIGS = {
                           ctypes.POINTER(SolverReportC), c_ptr],
     "pf_cg_profile": [c_ptr, c_ptr, c_ptr, c_int, c_int, c_ptr, c_ptr,
                       ctypes.POINTER(c_dbl), c_ptr],
+    "pf_bicgstab_profile": [c_ptr, c_ptr, c_int, c_int, c_ptr, c_int, c_ptr,
+                            ctypes.POINTER(c_dbl), c_ptr],
     "pf_bwd_correct_velocity": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
                                 c_ptr, c_ptr, c_ptr],
     "pf_bwd_pressure_outer": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],

@@ -65,6 +65,7 @@ class GradState:
     source: object = None
     bc: list = None
     solve_iterations: int = 0
+    reports: list = None     # SolverReports of the adjoint solves
 
     @classmethod
     def zeros(cls, domain, device=None):
@@ -219,7 +220,8 @@ def backward_step(domain, tape, cot, path=GradientPath.FULL, tol=None,
     iters = sum(r.iterations for r in reports)
     return GradState(u=du_n.t(), p=torch.zeros(n, dtype=F64, device=dev),
                      nu=float(dnu.item()), source=dsource.t(),
-                     bc=bc_views(plan, dbc), solve_iterations=iters)
+                     bc=bc_views(plan, dbc), solve_iterations=iters,
+                     reports=reports)
 
 
 def backward_rollout(domain, tapes, cots, path=GradientPath.FULL, tol=None,

@@ -20,7 +20,7 @@ namespace pf {
 
 constexpr int kBlock = 256;      // threads per CTA for streaming kernels
 constexpr int kMaxRedBlocks = 1184;  // 148 SMs x 8 resident CTAs
-constexpr int kMaxK = 8;         // values per fused reduction
+constexpr int kMaxK = 12;        // values per fused reduction
 
 void set_error(const std::string &msg);
 int cuda_check(cudaError_t e, const char *what);

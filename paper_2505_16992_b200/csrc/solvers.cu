@@ -358,9 +358,22 @@ __global__ void __launch_bounds__(kBlock)
 
 // ===========================================================================
 // BiCGStab on ncomp right-hand sides sharing one matrix
+//
+// Three fused passes per iteration (S/linalg.py:183-211 restated):
+//   pv: p = r + beta (p - omega v) and v = A M^-1 p in one sweep -- the
+//       stencil gathers the neighbours' r, p, v and forms their p on the fly,
+//       so neither p nor phat makes a separate trip through HBM; r^.v -> alpha
+//   st: s = r - alpha v (on the fly again) and t = A M^-1 s;
+//       |s|, t.t, t.s -> early exit / omega
+//   xr: x += M^-1 (alpha p + omega s); r = s - omega t; |r|, r^.r -> beta
+// p and v are ping-ponged by iteration parity (the stencil of cell i reads
+// its neighbours' old p while i writes its new one).  M is Jacobi: M^-1 y is
+// y_j / A_jj, evaluated where the value is gathered.
 
 struct BiVecs {
-  double *r, *rhat, *p, *v, *phat, *s, *shat, *t;  // each (ncomp, n)
+  double *r, *rhat, *t;   // each (ncomp, n)
+  double *p[2], *v[2];    // ping-pong by iteration parity
+  double *dinv;           // (n) Jacobi: 1 / A_ii (ones when unpreconditioned)
 };
 
 __global__ void k_bi_reset(SolverState *st, int ncomp, int maxiter,
@@ -420,7 +433,7 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
-// r = b - A x; rhat = r; p = v = 0
+// r = b - A x; rhat = r; p = v = 0 (parity-0 buffers)
 template <class V, bool kTrans>
 __global__ void __launch_bounds__(kBlock)
     k_bi_init(V v, const double *__restrict__ a, const double *__restrict__ b,
@@ -432,17 +445,19 @@ __global__ void __launch_bounds__(kBlock)
   int act[3];
   for (int q = 0; q < 3; ++q) act[q] = q < nc && !st->c[q].done;
   double acc[3] = {0.0, 0.0, 0.0};
+  const int pc = st->precond;
   GRID_LOOP(i, v.n) {
     Face fc[2 * V::kDim];
     load_faces(v, i, fc);
+    w.dinv[i] = pc ? 1.0 / a[i] : 1.0;
     for (int q = 0; q < nc; ++q) {
       if (!act[q]) continue;
       const int64_t o = q * n;
       const double ri = b[o + i] - apply_row<V, kTrans>(v, i, fc, a, x + o);
       w.r[o + i] = ri;
       w.rhat[o + i] = ri;
-      w.p[o + i] = 0.0;
-      w.v[o + i] = 0.0;
+      w.p[0][o + i] = 0.0;
+      w.v[0][o + i] = 0.0;
       acc[q] += ri * ri;
     }
   }
@@ -474,51 +489,79 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
-// p = r + beta (p - omega v); phat = M p
-__global__ void __launch_bounds__(kBlock)
-    k_bi_p(const double *__restrict__ a, BiVecs w, int32_t n,
-           const SolverState *st) {
-  if (st->all_done) return;
-  const int nc = st->ncomp, pc = st->precond;
-  for (int q = 0; q < nc; ++q) {
-    const CompState &c = st->c[q];
-    if (c.done) continue;
-    const double beta = c.beta, omega = c.omega;
-    const int64_t o = (int64_t)q * n;
-    GRID_LOOP(i, n) {
-      const double pi = w.r[o + i] + beta * (w.p[o + i] - omega * w.v[o + i]);
-      w.p[o + i] = pi;
-      w.phat[o + i] = prec(pc, a, i, pi);
-    }
+// y_i = sum_j A_ij g(j) (transposed: A_ji) for NC right-hand sides at once;
+// g(q, j) is the preconditioned input value of component q at cell j.
+template <class V, bool kTrans, class G>
+__device__ __forceinline__ void apply_rows(const V &v, int32_t i,
+                                           const Face (&fc)[2 * V::kDim],
+                                           const double *__restrict__ a,
+                                           const int (&act)[3], int nc,
+                                           G &&g, double (&y)[3]) {
+  constexpr int D = V::kDim;
+  const int64_t n = v.n;
+  const double aii = a[i];
+#pragma unroll
+  for (int q = 0; q < 3; ++q)
+    y[q] = (q < nc && act[q]) ? aii * g(q, i) : 0.0;
+#pragma unroll
+  for (int f = 0; f < 2 * D; ++f) {
+    const int32_t j = fc[f].nb;
+    if (j < 0) continue;
+    const double coef =
+        kTrans ? a[(int64_t)(1 + back_face(fc[f], f & 1)) * n + j]
+               : a[(int64_t)(1 + f) * n + i];
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+      if (q < nc && act[q]) y[q] += coef * g(q, j);
   }
 }
 
-// v = A phat; rhat.v -> alpha
+// pass pv: p' = r + beta (p - omega v); v' = A M^-1 p'; r^.v' -> alpha
 template <class V, bool kTrans>
 __global__ void __launch_bounds__(kBlock)
-    k_bi_v(V v, const double *__restrict__ a, BiVecs w, SolverState *st,
-           double *partials, unsigned *counter) {
+    k_bi_pv(V v, const double *__restrict__ a, BiVecs w, int par,
+            SolverState *st, double *partials, unsigned *counter) {
   if (st->all_done) return;
-  const int nc = st->ncomp;
+  const int nc = st->ncomp, pc = st->precond;
   const int64_t n = v.n;
   int act[3];
-  for (int q = 0; q < 3; ++q) act[q] = q < nc && !st->c[q].done;
+  double beta[3], omega[3];
+  _Pragma("unroll") for (int q = 0; q < 3; ++q) {
+    act[q] = q < nc && !st->c[q].done;
+    beta[q] = q < nc ? st->c[q].beta : 0.0;
+    omega[q] = q < nc ? st->c[q].omega : 0.0;
+  }
+  const double *__restrict__ r = w.r;
+  const double *__restrict__ dinv = w.dinv;
+  const double *__restrict__ p0 = w.p[par];
+  const double *__restrict__ v0 = w.v[par];
+  double *__restrict__ p1 = w.p[par ^ 1];
+  double *__restrict__ v1 = w.v[par ^ 1];
   double acc[3] = {0.0, 0.0, 0.0};
   GRID_LOOP(i, v.n) {
     Face fc[2 * V::kDim];
     load_faces(v, i, fc);
-    for (int q = 0; q < nc; ++q) {
+    auto pnew = [&](int q, int32_t j) {
+      const int64_t o = q * n + j;
+      return r[o] + beta[q] * (p0[o] - omega[q] * v0[o]);
+    };
+    auto g = [&](int q, int32_t j) { return pnew(q, j) * dinv[j]; };
+    double y[3];
+    apply_rows<V, kTrans>(v, i, fc, a, act, nc, g, y);
+    _Pragma("unroll") for (int q = 0; q < 3; ++q) {
+      if (q >= nc) break;
       if (!act[q]) continue;
-      const int64_t o = q * n;
-      const double vi = apply_row<V, kTrans>(v, i, fc, a, w.phat + o);
-      w.v[o + i] = vi;
-      acc[q] += w.rhat[o + i] * vi;
+      const int64_t o = q * n + i;
+      p1[o] = pnew(q, i);
+      v1[o] = y[q];
+      acc[q] += w.rhat[o] * y[q];
     }
   }
   double tot[3];
   if (grid_reduce<3>(acc, partials, counter, tot)) {
     int all = 1;
-    for (int q = 0; q < nc; ++q) {
+    _Pragma("unroll") for (int q = 0; q < 3; ++q) {
+      if (q >= nc) break;
       CompState &c = st->c[q];
       if (act[q]) {
         if (fabs(tot[q]) < DBL_MIN) {
@@ -534,126 +577,110 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
-// s = r - alpha v; shat = M s; |s| -> early exit
+// pass st: s = r - alpha v'; t = A M^-1 s; |s| (early exit), t.t, t.s
+template <class V, bool kTrans>
 __global__ void __launch_bounds__(kBlock)
-    k_bi_s(const double *__restrict__ a, BiVecs w, int32_t n, SolverState *st,
-           double *partials, unsigned *counter) {
+    k_bi_st(V v, const double *__restrict__ a, BiVecs w, int par,
+            SolverState *st, double *partials, unsigned *counter) {
   if (st->all_done) return;
   const int nc = st->ncomp, pc = st->precond;
+  const int64_t n = v.n;
   int act[3];
   double alpha[3];
-  for (int q = 0; q < 3; ++q) {
+  _Pragma("unroll") for (int q = 0; q < 3; ++q) {
     act[q] = q < nc && !st->c[q].done;
     alpha[q] = q < nc ? st->c[q].alpha : 0.0;
   }
-  double acc[3] = {0.0, 0.0, 0.0};
-  GRID_LOOP(i, n) {
-    for (int q = 0; q < nc; ++q) {
+  const double *__restrict__ r = w.r;
+  const double *__restrict__ dinv = w.dinv;
+  const double *__restrict__ v1 = w.v[par ^ 1];
+  double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  GRID_LOOP(i, v.n) {
+    Face fc[2 * V::kDim];
+    load_faces(v, i, fc);
+    auto sval = [&](int q, int32_t j) {
+      const int64_t o = q * n + j;
+      return r[o] - alpha[q] * v1[o];
+    };
+    auto g = [&](int q, int32_t j) { return sval(q, j) * dinv[j]; };
+    double y[3];
+    apply_rows<V, kTrans>(v, i, fc, a, act, nc, g, y);
+    _Pragma("unroll") for (int q = 0; q < 3; ++q) {
+      if (q >= nc) break;
       if (!act[q]) continue;
-      const int64_t o = (int64_t)q * n;
-      const double si = w.r[o + i] - alpha[q] * w.v[o + i];
-      w.s[o + i] = si;
-      w.shat[o + i] = prec(pc, a, i, si);
-      acc[q] += si * si;
+      const double si = sval(q, i);
+      w.t[q * n + i] = y[q];
+      acc[3 * q] += si * si;
+      acc[3 * q + 1] += y[q] * y[q];
+      acc[3 * q + 2] += y[q] * si;
     }
   }
-  double tot[3];
-  if (grid_reduce<3>(acc, partials, counter, tot)) {
-    // all_done is deliberately left alone: k_bi_t must still run to apply
+  double tot[9];
+  if (grid_reduce<9>(acc, partials, counter, tot)) {
+    // all_done is deliberately left alone: k_bi_xr must still run to apply
     // the early-exit update x += alpha phat
-    for (int q = 0; q < nc; ++q) {
+    _Pragma("unroll") for (int q = 0; q < 3; ++q) {
+      if (q >= nc) break;
       CompState &c = st->c[q];
       if (!act[q]) continue;
-      c.res = sqrt(tot[q]);
+      c.res = sqrt(tot[3 * q]);
       if (c.res <= c.tol_abs) {
         c.converged = 1;
         c.done = 1;
         c.pending = 1;
+      } else if (tot[3 * q + 1] < DBL_MIN) {
+        c.fail = 1;
+        c.done = 1;
+      } else {
+        c.omega = tot[3 * q + 2] / tot[3 * q + 1];
       }
     }
   }
 }
 
-// pending comps: x += alpha phat.  active comps: t = A shat; t.t, t.s -> omega
-template <class V, bool kTrans>
+// pass xr: pending comps: x += alpha phat.  active comps:
+// x += alpha phat + omega shat; r = s - omega t; |r|, r^.r -> next beta
 __global__ void __launch_bounds__(kBlock)
-    k_bi_t(V v, const double *__restrict__ a, BiVecs w, double *__restrict__ x,
-           SolverState *st, double *partials, unsigned *counter) {
+    k_bi_xr(const double *__restrict__ a, BiVecs w, int par,
+            double *__restrict__ x, int32_t n, SolverState *st,
+            double *partials, unsigned *counter) {
   if (st->all_done) return;
-  const int nc = st->ncomp;
-  const int64_t n = v.n;
+  const int nc = st->ncomp, pc = st->precond;
   int act[3], pend[3];
-  double alpha[3];
-  for (int q = 0; q < 3; ++q) {
+  double alpha[3], omega[3];
+  _Pragma("unroll") for (int q = 0; q < 3; ++q) {
     act[q] = q < nc && !st->c[q].done;
     pend[q] = q < nc && st->c[q].pending;
     alpha[q] = q < nc ? st->c[q].alpha : 0.0;
-  }
-  double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  GRID_LOOP(i, v.n) {
-    Face fc[2 * V::kDim];
-    load_faces(v, i, fc);
-    for (int q = 0; q < nc; ++q) {
-      const int64_t o = q * n;
-      if (pend[q]) x[o + i] += alpha[q] * w.phat[o + i];
-      if (!act[q]) continue;
-      const double ti = apply_row<V, kTrans>(v, i, fc, a, w.shat + o);
-      w.t[o + i] = ti;
-      acc[2 * q] += ti * ti;
-      acc[2 * q + 1] += ti * w.s[o + i];
-    }
-  }
-  double tot[6];
-  if (grid_reduce<6>(acc, partials, counter, tot)) {
-    int all = 1;
-    for (int q = 0; q < nc; ++q) {
-      CompState &c = st->c[q];
-      c.pending = 0;
-      if (act[q]) {
-        const double tt = tot[2 * q];
-        if (tt < DBL_MIN) {
-          c.fail = 1;
-          c.done = 1;
-        } else {
-          c.omega = tot[2 * q + 1] / tt;
-        }
-      }
-      if (!c.done) all = 0;
-    }
-    st->all_done = all;
-  }
-}
-
-// x += alpha phat + omega shat; r = s - omega t; next rho
-__global__ void __launch_bounds__(kBlock)
-    k_bi_x(BiVecs w, double *__restrict__ x, int32_t n, SolverState *st,
-           double *partials, unsigned *counter) {
-  if (st->all_done) return;
-  const int nc = st->ncomp;
-  int act[3];
-  double alpha[3], omega[3];
-  for (int q = 0; q < 3; ++q) {
-    act[q] = q < nc && !st->c[q].done;
-    alpha[q] = q < nc ? st->c[q].alpha : 0.0;
     omega[q] = q < nc ? st->c[q].omega : 0.0;
   }
+  const double *__restrict__ p1 = w.p[par ^ 1];
+  const double *__restrict__ v1 = w.v[par ^ 1];
   double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   GRID_LOOP(i, n) {
-    for (int q = 0; q < nc; ++q) {
+    const double di = w.dinv[i];
+    _Pragma("unroll") for (int q = 0; q < 3; ++q) {
+      if (q >= nc) break;
+      const int64_t o = (int64_t)q * n + i;
+      if (pend[q]) x[o] += alpha[q] * (p1[o] * di);
       if (!act[q]) continue;
-      const int64_t o = (int64_t)q * n;
-      x[o + i] = x[o + i] + alpha[q] * w.phat[o + i] + omega[q] * w.shat[o + i];
-      const double ri = w.s[o + i] - omega[q] * w.t[o + i];
-      w.r[o + i] = ri;
+      const double phat = p1[o] * di;
+      const double si = w.r[o] - alpha[q] * v1[o];
+      const double shat = si * di;
+      x[o] = x[o] + alpha[q] * phat + omega[q] * shat;
+      const double ri = si - omega[q] * w.t[o];
+      w.r[o] = ri;
       acc[2 * q] += ri * ri;
-      acc[2 * q + 1] += w.rhat[o + i] * ri;
+      acc[2 * q + 1] += w.rhat[o] * ri;
     }
   }
   double tot[6];
   if (grid_reduce<6>(acc, partials, counter, tot)) {
     int all = 1;
-    for (int q = 0; q < nc; ++q) {
+    _Pragma("unroll") for (int q = 0; q < 3; ++q) {
+      if (q >= nc) break;
       CompState &c = st->c[q];
+      c.pending = 0;
       if (act[q]) {
         c.res = sqrt(tot[2 * q]);
         if (c.res <= c.tol_abs) {
@@ -982,12 +1009,12 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   double *base = w.vecs;
   bv.r = base;
   bv.rhat = base + len;
-  bv.p = base + 2 * len;
-  bv.v = base + 3 * len;
-  bv.phat = base + 4 * len;
-  bv.s = base + 5 * len;
-  bv.shat = base + 6 * len;
-  bv.t = base + 7 * len;
+  bv.t = base + 2 * len;
+  bv.p[0] = base + 3 * len;
+  bv.p[1] = base + 4 * len;
+  bv.v[0] = base + 5 * len;
+  bv.v[1] = base + 6 * len;
+  bv.dinv = base + 7 * len;
   const int ge = grid_for(n), gr = std::min(grid_for(n), pl.red_blocks);
   launch(k_bi_reset, 1, 1, s, st, ncomp, maxiter, precond, tol, fresh, mask);
   if (fresh) launch(k_bi_bnorm, gr, kBlock, s, b, n, st, w.partials, w.counters);
@@ -1002,13 +1029,13 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     const int bsz = std::min(launched < 4 ? 2 : next_batch(launched, 0),
                              maxiter - launched);
     for (int k = 0; k < bsz; ++k) {
-      launch(k_bi_p, ge, kBlock, s, a, bv, n, st);
-      launch(k_bi_v<V, kTrans>, gr, kBlock, s, v, a, bv, st, w.partials,
-                                              w.counters);
-      launch(k_bi_s, gr, kBlock, s, a, bv, n, st, w.partials, w.counters);
-      launch(k_bi_t<V, kTrans>, gr, kBlock, s, v, a, bv, x, st, w.partials,
-                                              w.counters);
-      launch(k_bi_x, gr, kBlock, s, bv, x, n, st, w.partials, w.counters);
+      const int par = (launched + k) & 1;
+      launch(k_bi_pv<V, kTrans>, gr, kBlock, s, v, a, bv, par, st,
+             w.partials, w.counters);
+      launch(k_bi_st<V, kTrans>, gr, kBlock, s, v, a, bv, par, st,
+             w.partials, w.counters);
+      launch(k_bi_xr, gr, kBlock, s, a, bv, par, x, n, st, w.partials,
+             w.counters);
     }
     PF_LAUNCH_CHECK("bicgstab iterations");
     launched += bsz;
@@ -1223,6 +1250,99 @@ extern "C" int pf_cg_profile(const pf_plan *plan, const double *a,
     }
     for (int j = 0; j < 10; ++j) ms_host[j] = tot[j] / iters;
     ms_host[10] = graph_ms;
+    return PF_OK;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// live per-pass timing of the batched BiCGStab iteration (bench.py roofline)
+
+extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
+                                   int32_t transpose, int32_t ncomp,
+                                   const double *b, int32_t iters,
+                                   void *workspace, double *ms_host,
+                                   void *stream) {
+  if (!plan || !a || !b || !workspace || !ms_host || iters < 1 || ncomp < 1 ||
+      ncomp > 3) {
+    set_error("pf_bicgstab_profile: bad argument");
+    return PF_ERR_ARG;
+  }
+  const Plan &pl = *reinterpret_cast<const Plan *>(plan);
+  if (ncomp > pl.d.dim) {
+    set_error("pf_bicgstab_profile: ncomp exceeds the workspace sizing");
+    return PF_ERR_ARG;
+  }
+  Workspace w = carve(workspace, pl.d.n, pl.d.dim);
+  SolverState *st = reinterpret_cast<SolverState *>(w.solver);
+  cudaStream_t s = S(stream);
+  const int32_t n = (int32_t)pl.d.n;
+  const int64_t len = (int64_t)ncomp * n;
+  // x lives past the seven solver vectors and 1 / diag
+  double *x = w.vecs + 8 * len;
+  return dispatch(pl, [&](auto v) {
+    using V = decltype(v);
+    BiVecs bv;
+    bv.r = w.vecs;
+    bv.rhat = w.vecs + len;
+    bv.t = w.vecs + 2 * len;
+    bv.p[0] = w.vecs + 3 * len;
+    bv.p[1] = w.vecs + 4 * len;
+    bv.v[0] = w.vecs + 5 * len;
+    bv.v[1] = w.vecs + 6 * len;
+    bv.dinv = w.vecs + 7 * len;
+    const int gr = std::min(grid_for(n), pl.red_blocks);
+    PF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * len, s));
+    // tol 0: the recurrence never converges inside the timed iterations
+    launch(k_bi_reset, 1, 1, s, st, ncomp, iters + 1, 1, 0.0, 1, 0x7u);
+    launch(k_bi_bnorm, gr, kBlock, s, b, n, st, w.partials, w.counters);
+    if (transpose)
+      launch(k_bi_init<V, true>, gr, kBlock, s, v, a, b, (const double *)x,
+             bv, st, w.partials, w.counters);
+    else
+      launch(k_bi_init<V, false>, gr, kBlock, s, v, a, b, (const double *)x,
+             bv, st, w.partials, w.counters);
+    cudaEvent_t ev[4];
+    for (auto &e : ev) PF_CUDA(cudaEventCreate(&e));
+    double tot[4] = {0, 0, 0, 0};
+    for (int k = 0; k < iters; ++k) {
+      const int par = k & 1;
+      PF_CUDA(cudaEventRecord(ev[0], s));
+      if (transpose)
+        launch(k_bi_pv<V, true>, gr, kBlock, s, v, a, bv, par, st, w.partials,
+               w.counters);
+      else
+        launch(k_bi_pv<V, false>, gr, kBlock, s, v, a, bv, par, st,
+               w.partials, w.counters);
+      PF_CUDA(cudaEventRecord(ev[1], s));
+      if (transpose)
+        launch(k_bi_st<V, true>, gr, kBlock, s, v, a, bv, par, st, w.partials,
+               w.counters);
+      else
+        launch(k_bi_st<V, false>, gr, kBlock, s, v, a, bv, par, st,
+               w.partials, w.counters);
+      PF_CUDA(cudaEventRecord(ev[2], s));
+      launch(k_bi_xr, gr, kBlock, s, a, bv, par, x, n, st, w.partials,
+             w.counters);
+      PF_CUDA(cudaEventRecord(ev[3], s));
+      PF_CUDA(cudaEventSynchronize(ev[3]));
+      for (int j = 0; j < 3; ++j) {
+        float ms = 0.f;
+        PF_CUDA(cudaEventElapsedTime(&ms, ev[j], ev[j + 1]));
+        tot[j] += ms;
+      }
+      float ms = 0.f;
+      PF_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[3]));
+      tot[3] += ms;
+    }
+    for (auto &e : ev) cudaEventDestroy(e);
+    SolverState hs;
+    int rc = read_state(st, &hs, s);
+    if (rc) return rc;
+    if (hs.all_done) {
+      set_error("pf_bicgstab_profile: iteration stopped early (breakdown)");
+      return PF_ERR_ARG;
+    }
+    for (int j = 0; j < 4; ++j) ms_host[j] = tot[j] / iters;
     return PF_OK;
   });
 }
