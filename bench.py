@@ -11,9 +11,12 @@ perturbation 0.1, seed 0), dt = 0.3 (2 pi/256) / max|u0|, tol 1e-8, fp64,
 per-step wall forcing.  The state advances, warm starts are on (the
 reference's run_rollout setting), inputs (>10 GB working set) exceed L2.
 
-Multi-GPU (torchrun, N>1): every rank advances its own C4 replica (weak
-scaling, no data-path collective); value = all ranks' cell-steps / max-over-
-ranks device time.
+Multi-GPU (torchrun, N>1): C4 is slab-decomposed along its periodic
+streamwise axis, one slab per rank (strong scaling: the job advances the
+one 256x192x256 channel); ghost planes, solver reductions and the spectral
+preconditioner's transposes move over NVLink peer memory (paper_2505_16992_
+b200/slab.py).  value = global cells x steps / max-over-ranks device time.
+The other configs run one replica per rank (weak scaling).
 
 --impl reference runs the reference's own CPU implementation (pisoflow,
 built unmodified into oracle/_ref by oracle/build_ref.py) on rank 0, one
@@ -32,6 +35,10 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# load every kernel at context creation: a lazy load is a context-wide
+# synchronisation, which the spinning cross-rank waits of the slab path
+# must not meet mid-run (and it keeps first-launch costs out of warm-up)
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 METRIC = "Mcell-steps/s fwd+adjoint PISO, 3D channel"
 UNIT = "Mcell-steps/s"
@@ -55,7 +62,7 @@ SAMPLE_SHAPE = (64, 48, 64)
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
@@ -174,7 +181,10 @@ def workload_config(args, sample=False):
             "cells": int(math.prod(shape)), "wall_ratio": ratio,
             "dt_rule": f"{cfl}*(2pi/{shape[0]})/max|u0|", "tol": args.tol,
             "gradient_path": "full",
-            "parallelism": ("replicas" if args.gpus > 1 else "single"),
+            "parallelism": (("single" if args.gpus <= 1 else
+                             f"slab{args.gpus} (x split, NVLink P2P halos)"
+                             if args.config in ("c4", "slab8") else
+                             "replicas")),
             "l2": "inputs larger than L2 (no flush needed)",
             "reference_sample": list(SAMPLE_SHAPE) if sample else None}
 
@@ -184,6 +194,10 @@ def workload_config(args, sample=False):
 
 
 class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms by a reader
+    thread.  start() returns once the first sample has arrived, so the
+    sampler's own start-up (which touches the GPU) is outside the timed
+    region; stop() keeps only the samples taken while the region ran."""
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,"
              "clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,"
@@ -194,27 +208,49 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.lines = []
+        self.t_start = None
+        self.first = threading.Event()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.perf_counter(), line))
+            self.first.set()
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}",
                  f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE,
+                 "-lms", "100"], stdout=subprocess.PIPE,
                 stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+            return
+        threading.Thread(target=self._read, daemon=True).start()
+        self.first.wait(timeout=10)
+
+    def mark(self):
+        """Start of the timed region."""
+        self.t_start = time.perf_counter()
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
                     "samples": 0}
+        t_end = time.perf_counter()
         self.proc.terminate()
-        out, _ = self.proc.communicate(timeout=10)
+        try:
+            self.proc.wait(timeout=10)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        t0 = self.t_start if self.t_start is not None else 0.0
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
                  "sw_power_cap"]
-        for line in out.strip().splitlines():
+        for t, line in list(self.lines):
+            if t < t0 or t > t_end + 0.2:
+                continue
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue
@@ -330,7 +366,9 @@ def measure_roofline(args, dom, plan, state, nu, dt, dev, per_step):
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    n = dom.n
+    # cells one launch processes: the owned cells (a slab's ghost planes are
+    # only read)
+    n = dom.nxl * dom.plane if hasattr(dom, "nxl") else dom.n
     launches = {}
     for nm in bi:
         launches[nm] = per_step["bi_adj" if "adjoint" in nm else "bi_fwd"]
@@ -400,10 +438,11 @@ def run_c5train(args, world, rank, local, dev):
         tstep()
     lib = _lib.load()
     clocks = ClockSampler(local)
+    clocks.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    clocks.mark()
     l0 = lib.pf_launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -437,19 +476,30 @@ def run_c5train(args, world, rank, local, dev):
         dist.destroy_process_group()
 
 
-def build_workload(args, dev):
+def build_workload(args, dev, rank=0, world=1):
+    """The C4 workload; with world > 1 this rank's slab of it (SURVEY §8 e:
+    slab decomposition of the periodic streamwise axis, ghost-plane halos
+    and cross-rank reductions over NVLink peer memory).  The initial field
+    and the cotangent are the single-GPU ones, restricted to the slab."""
     import numpy as np
     import torch
-    from paper_2505_16992_b200 import channel, mesh
+    from paper_2505_16992_b200 import channel, mesh, piso, slab
     shape, ratio, cfl, _ = CONFIGS[args.config]
     dom = mesh.make_channel(shape, ratio=ratio)
-    state, nu, u_tau = channel.reichardt_init(dom, 180.0, perturbation=0.1,
-                                              seed=0, device=dev)
-    dt = cfl * (2 * np.pi / shape[0]) / float(state.u.abs().max())
-    forcing = channel.WallForcing(dom, dev)
+    u0, nu, u_tau = channel.reichardt_velocity(dom, 180.0, perturbation=0.1,
+                                               seed=0, device=dev)
+    dt = cfl * (2 * np.pi / shape[0]) / float(u0.abs().max())
     g = torch.Generator(device="cpu").manual_seed(0)
     w = torch.randn((dom.n, 3), generator=g, dtype=torch.float64).to(dev)
-    return dom, state, nu, dt, forcing, w
+    if world == 1:
+        state = piso.make_state(dom, u0=u0, device=dev)
+        return dom, state, nu, dt, channel.WallForcing(dom, dev), w, None
+    sd = slab.SlabDomain(dom, rank, world)
+    comm = slab.SlabComm.distributed(sd, dev)
+    state = piso.make_state(sd, u0=sd.scatter(u0), device=dev)
+    wl = sd.scatter(w).contiguous()
+    del u0, w
+    return sd, state, nu, dt, slab.SlabWallForcing(sd, dev), wl, comm
 
 
 def main():
@@ -476,7 +526,11 @@ def main():
     if args.config == "c5train":
         return run_c5train(args, world, rank, local, dev)
 
-    dom, state0, nu, dt, forcing, w = build_workload(args, dev)
+    # C4 splits into slabs across the ranks (strong scaling); the other
+    # configs run one replica per rank (weak scaling)
+    slabbed = world > 1 and args.config in ("c4", "slab8")
+    dom, state0, nu, dt, forcing, w, comm = build_workload(
+        args, dev, rank if slabbed else 0, world if slabbed else 1)
     plan = dom.device_plan(dev)
     cot = adjoint.GradState(u=w, p=torch.zeros(dom.n, dtype=torch.float64,
                                                device=dev))
@@ -510,10 +564,11 @@ def main():
 
     lib = _lib.load()
     clocks = ClockSampler(local)
+    clocks.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    clocks.mark()
     l0 = lib.pf_launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -531,7 +586,8 @@ def main():
         dist.barrier()
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = world * dom.n * args.steps / (ms / 1e3) / 1e6
+    cells_job = (dom.global_domain.n if slabbed else world * dom.n)
+    value = cells_job * args.steps / (ms / 1e3) / 1e6
     it_per_step = {k: stats[k] / max(stats["steps"], 1)
                    for k in ("mom", "p", "adj", "bi_fwd", "bi_adj", "cg")}
 
@@ -562,7 +618,7 @@ def main():
         t = torch.tensor([ms_e2e], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
-    e2e_value = world * dom.n * args.steps / (ms_e2e / 1e3) / 1e6
+    e2e_value = cells_job * args.steps / (ms_e2e / 1e3) / 1e6
 
     per_step = {k: stats[k] / max(stats["steps"], 1)
                 for k in ("bi_fwd", "bi_adj", "cg")}
@@ -590,7 +646,8 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if slabbed else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reichardt_init seed 0, random cotangent)",
             "config": workload_config(args),
             "roofline": roofline,

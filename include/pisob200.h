@@ -108,6 +108,18 @@ typedef struct pf_plan_desc {
    * uniformly spaced; it falls back to multigrid where the topology does
    * not allow it. */
   int32_t geom_precond;
+  /* Slab decomposition along axis 0 of a PF_TOPO_BOX plan (0 / 0: not
+   * distributed).  The local box is box_shape[0] = nxl + 2 planes: the nxl
+   * planes this rank owns (global planes slab_x0 .. slab_x0 + nxl - 1 of
+   * slab_nx) between two ghost planes that mirror the neighbouring ranks'
+   * edge planes (axis 0 must be periodic: the ranks form a ring).  Kernels
+   * compute the owned cells only; reductions and solver scalars are global
+   * over all ranks once a communicator is attached (pf_comm_create,
+   * pf_plan_attach_comm). */
+  int32_t slab_world;
+  int32_t slab_rank;
+  int64_t slab_nx;
+  int64_t slab_x0;
 } pf_plan_desc;
 
 typedef struct pf_plan pf_plan;
@@ -355,6 +367,48 @@ PF_API int pf_reduce_dot(const pf_plan *plan, const double *x, const double *y,
                   void *stream);
 PF_API int pf_reduce_maxabs(const pf_plan *plan, const double *x, int64_t len,
                      void *workspace, double *out_host, void *stream);
+
+/* ---- slab decomposition across GPUs (SURVEY.md §8 e) ----------------------
+ * The reference is single-process; these entry points have no reference
+ * counterpart.  A slab plan (pf_plan_desc.slab_world > 0) computes its owned
+ * planes; a communicator links it to the other ranks' plans through peer
+ * memory (NVLink P2P via CUDA IPC across processes, or direct pointers for
+ * several slabs of one process on one device).  Once attached, every entry
+ * point of the plan is COLLECTIVE: all ranks call the same entry points in
+ * the same order, ghost planes of the arrays they read are exchanged inside
+ * the call, and every reduction (solver dot products, means, maxima) is
+ * global and bitwise identical on all ranks.  Ghost planes of every array
+ * passed to a slab plan are owned by the library. */
+typedef struct pf_comm pf_comm;
+
+/* Allocate this rank's symmetric buffer (halo inboxes, reduction slots, the
+ * spectral preconditioner's transposed spectrum) for a slab plan. */
+PF_API int pf_comm_create(const pf_plan *plan, pf_comm **out);
+/* 64-byte cudaIpcMemHandle of the symmetric buffer, for the other ranks. */
+PF_API int pf_comm_ipc_handle(const pf_comm *comm, void *handle_host);
+/* Map rank `peer`'s buffer from its IPC handle (cross-process, NVLink). */
+PF_API int pf_comm_open_peer(pf_comm *comm, int32_t peer, const void *handle_host);
+/* Same-process peer (several slab plans of one process on one device). */
+PF_API int pf_comm_set_local_peer(pf_comm *comm, int32_t peer, const pf_comm *other);
+PF_API int64_t pf_comm_bytes(const pf_comm *comm);
+/* After every peer is mapped: make the plan (and its workspace) use it. */
+PF_API int pf_plan_attach_comm(pf_plan *plan, pf_comm *comm, void *workspace,
+                               void *stream);
+/* PF_ERR_CUDA if a device-side wait for a peer timed out. */
+PF_API int pf_comm_status(const pf_comm *comm, void *stream);
+PF_API int pf_comm_destroy(pf_comm *comm);
+/* Exchange the ghost planes of `count` (ncomp_host[j], n) arrays. */
+PF_API int pf_halo_exchange(const pf_plan *plan, const uint64_t *arrays_host,
+                            const int32_t *ncomp_host, int32_t count,
+                            void *stream);
+/* buf[0..k) <- sum (op 0) or max (op 1) over the ranks, in place. */
+PF_API int pf_comm_allreduce(const pf_plan *plan, double *buf, int32_t k,
+                             int32_t op, void *stream);
+PF_API int pf_comm_barrier(const pf_plan *plan, void *stream);
+/* Sequence numbers of the collectives this rank has completed: allreduce,
+ * halo exchange, barrier, vector allreduce (tests and diagnostics). */
+PF_API int pf_comm_counters(const pf_comm *comm, uint64_t *out4_host,
+                            void *stream);
 
 #ifdef __cplusplus
 }

@@ -39,6 +39,8 @@ class PlanDesc(ctypes.Structure):
         ("alpha_full", c_ptr), ("balpha_row", c_ptr), ("bfid", c_ptr),
         ("finfo", c_ptr), ("nfaces", c_int), ("has_cross", c_int),
         ("geom_precond", c_int),
+        ("slab_world", c_int), ("slab_rank", c_int), ("slab_nx", c_i64),
+        ("slab_x0", c_i64),
     ]
 
 
@@ -78,6 +80,18 @@ _SIGS = {
                           ctypes.POINTER(SolverReportC), c_ptr],
     "pf_cg_profile": [c_ptr, c_ptr, c_ptr, c_int, c_int, c_ptr, c_ptr,
                       ctypes.POINTER(c_dbl), c_ptr],
+    "pf_comm_create": [c_ptr, ctypes.POINTER(c_ptr)],
+    "pf_comm_ipc_handle": [c_ptr, c_ptr],
+    "pf_comm_open_peer": [c_ptr, c_int, c_ptr],
+    "pf_comm_set_local_peer": [c_ptr, c_int, c_ptr],
+    "pf_comm_bytes": [c_ptr],
+    "pf_plan_attach_comm": [c_ptr, c_ptr, c_ptr, c_ptr],
+    "pf_comm_status": [c_ptr, c_ptr],
+    "pf_comm_destroy": [c_ptr],
+    "pf_halo_exchange": [c_ptr, c_ptr, c_ptr, c_int, c_ptr],
+    "pf_comm_allreduce": [c_ptr, c_ptr, c_int, c_int, c_ptr],
+    "pf_comm_barrier": [c_ptr, c_ptr],
+    "pf_comm_counters": [c_ptr, c_ptr, c_ptr],
     "pf_bicgstab_profile": [c_ptr, c_ptr, c_int, c_int, c_ptr, c_int, c_ptr,
                             ctypes.POINTER(c_dbl), c_ptr],
     "pf_bwd_correct_velocity": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
@@ -109,7 +123,8 @@ _SIGS = {
     "pf_reduce_maxabs": [c_ptr, c_ptr, c_i64, c_ptr, ctypes.POINTER(c_dbl),
                          c_ptr],
 }
-_RESTYPES = {"pf_workspace_bytes": c_i64, "pf_mg_workspace_bytes": c_i64, "pf_last_error": ctypes.c_char_p,
+_RESTYPES = {"pf_workspace_bytes": c_i64, "pf_mg_workspace_bytes": c_i64,
+             "pf_comm_bytes": c_i64, "pf_last_error": ctypes.c_char_p,
              "pf_launch_count": ctypes.c_uint64}
 
 EXPORTED = sorted(list(_SIGS) + ["pf_last_error"])

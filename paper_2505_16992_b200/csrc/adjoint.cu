@@ -24,8 +24,8 @@ __global__ void __launch_bounds__(kBlock)
                   const double *__restrict__ c, const double *__restrict__ cu,
                   double *__restrict__ da, double *__restrict__ cot_gp) {
   constexpr int D = V::kDim;
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= v.n) return;
+  const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.i1) return;
   const int64_t n = v.n;
   const auto cell = v.topo.cell(i);
   const double pi = p[i];
@@ -66,8 +66,8 @@ __global__ void __launch_bounds__(kBlock)
     k_bwd_cv_gather(V v, const double *__restrict__ cot_gp,
                     const double *__restrict__ extra, double *__restrict__ dp) {
   constexpr int D = V::kDim;
-  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= v.n) return;
+  const int32_t j = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= v.i1) return;
   const int64_t n = v.n;
   const auto cell = v.topo.cell(j);
   double acc = 0.0;
@@ -98,8 +98,8 @@ __global__ void __launch_bounds__(kBlock)
     k_bwd_p_outer(V v, const double *__restrict__ y,
                   const double *__restrict__ p, double *__restrict__ dkf) {
   constexpr int D = V::kDim;
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= v.n) return;
+  const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.i1) return;
   const int64_t n = v.n;
   const auto cell = v.topo.cell(i);
   const double yi = y[i], pi = p[i];
@@ -116,8 +116,8 @@ __global__ void __launch_bounds__(kBlock)
     k_bwd_p_matrix(V v, const double *__restrict__ c,
                    const double *__restrict__ dkf, double *__restrict__ da) {
   constexpr int D = V::kDim;
-  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= v.n) return;
+  const int32_t j = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= v.i1) return;
   const int64_t n = v.n;
   const auto cell = v.topo.cell(j);
   double g = 0.0;
@@ -142,8 +142,8 @@ __global__ void __launch_bounds__(kBlock)
     k_adj_div(V v, const double *__restrict__ cot_b, double cs,
               double *__restrict__ g_h, double *__restrict__ dbc) {
   constexpr int D = V::kDim;
-  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= v.n) return;
+  const int32_t j = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= v.i1) return;
   const int64_t n = v.n;
   const auto cell = v.topo.cell(j);
   const double cb = cs * cot_b[j];
@@ -192,8 +192,8 @@ __global__ void __launch_bounds__(kBlock)
                  double *__restrict__ g_rhs, double *__restrict__ dc,
                  double *__restrict__ cot_hu) {
   constexpr int D = V::kDim;
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= v.n) return;
+  const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.i1) return;
   const int64_t n = v.n;
   const auto cell = v.topo.cell(i);
   const double ainv = 1.0 / c[i];
@@ -226,8 +226,8 @@ __global__ void __launch_bounds__(kBlock)
     k_bwd_h_gather(V v, const double *__restrict__ c,
                    const double *__restrict__ cot_hu, double *__restrict__ cu) {
   constexpr int D = V::kDim;
-  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= v.n) return;
+  const int32_t j = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= v.i1) return;
   const int64_t n = v.n;
   const auto cell = v.topo.cell(j);
   double acc[D];
@@ -252,8 +252,8 @@ __global__ void __launch_bounds__(kBlock)
     k_bwd_mom_outer(V v, const double *__restrict__ y,
                     const double *__restrict__ us, double *__restrict__ dc) {
   constexpr int D = V::kDim;
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= v.n) return;
+  const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.i1) return;
   const int64_t n = v.n;
   const auto cell = v.topo.cell(i);
   double yi[D];
@@ -283,8 +283,8 @@ __global__ void __launch_bounds__(kBlock)
     k_adj_rhs_cells(V v, const double *__restrict__ cot, double dt,
                     double *__restrict__ du_n) {
   constexpr int D = V::kDim;
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= v.n) return;
+  const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.i1) return;
   const int64_t n = v.n;
 #pragma unroll
   for (int q = 0; q < D; ++q) du_n[q * n + i] += cot[q * n + i] / dt;
@@ -301,6 +301,8 @@ __global__ void __launch_bounds__(kBlock)
   double acc[1] = {0.0};
   GRID_LOOP(e, v.m) {
     const int32_t i = __ldg(v.bcell + e);
+    // slab plans: entries of ghost-plane cells belong to a neighbour rank
+    if (i < v.i0 || i >= v.i1) continue;
     const int bf = __ldg(v.bface + e);
     const int f = bf & 15, kind = bf >> 4;
     const double nsgn = (f & 1) ? 1.0 : -1.0;
@@ -380,7 +382,7 @@ __global__ void __launch_bounds__(kBlock)
   constexpr int D = V::kDim;
   const int64_t n = v.n;
   double acc[1] = {0.0};
-  GRID_LOOP(j, v.n) {
+  RANGE_LOOP(j, v.rng()) {
     const auto cell = v.topo.cell(j);
     const double cdj = dc[j];
     const double invj = 1.0 / v.J(j);
@@ -455,9 +457,12 @@ extern "C" int pf_bwd_correct_velocity(const pf_plan *plan, const double *p,
   Workspace w = carve(workspace, pl.d.n, pl.d.dim);
   return dispatch(pl, [&](auto v) {
     double *cot_gp = w.vecs;
-    launch(k_bwd_cv_cell<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, p, c, cu, da,
+    const int D = decltype(v)::kDim;
+    halo(pl, S(stream), {{const_cast<double *>(p), 1}});
+    launch(k_bwd_cv_cell<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, p, c, cu, da,
                                                            cot_gp);
-    launch(k_bwd_cv_gather<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, cot_gp,
+    halo(pl, S(stream), {{cot_gp, D}});
+    launch(k_bwd_cv_gather<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, cot_gp,
                                                              extra_cot_p, cot_p);
     PF_LAUNCH_CHECK("bwd_correct_velocity");
     return PF_OK;
@@ -469,7 +474,8 @@ extern "C" int pf_bwd_pressure_outer(const pf_plan *plan, const double *y,
                                      void *stream) {
   PF_REQUIRE(plan && y && p && dkf, "pf_bwd_pressure_outer: null argument");
   return dispatch(P(plan), [&](auto v) {
-    launch(k_bwd_p_outer<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, y, p, dkf);
+    halo(P(plan), S(stream), {{const_cast<double *>(p), 1}});
+    launch(k_bwd_p_outer<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, y, p, dkf);
     PF_LAUNCH_CHECK("bwd_pressure_outer");
     return PF_OK;
   });
@@ -480,7 +486,9 @@ extern "C" int pf_bwd_pressure_matrix(const pf_plan *plan, const double *c,
                                       void *stream) {
   PF_REQUIRE(plan && c && dkf && da, "pf_bwd_pressure_matrix: null argument");
   return dispatch(P(plan), [&](auto v) {
-    launch(k_bwd_p_matrix<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, c, dkf, da);
+    halo(P(plan), S(stream),
+         {{const_cast<double *>(dkf), 2 * decltype(v)::kDim}});
+    launch(k_bwd_p_matrix<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, c, dkf, da);
     PF_LAUNCH_CHECK("bwd_pressure_matrix");
     return PF_OK;
   });
@@ -492,7 +500,8 @@ extern "C" int pf_adj_divergence_rhs(const pf_plan *plan, const double *cot_b,
   PF_REQUIRE(plan && cot_b && g_h, "pf_adj_divergence_rhs: null argument");
   PF_REQUIRE(dbc || P(plan).d.m == 0, "pf_adj_divergence_rhs: null dbc");
   return dispatch(P(plan), [&](auto v) {
-    launch(k_adj_div<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, cot_b, cot_scale,
+    halo(P(plan), S(stream), {{const_cast<double *>(cot_b), 1}});
+    launch(k_adj_div<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, cot_b, cot_scale,
                                                        g_h, dbc);
     PF_LAUNCH_CHECK("adj_divergence_rhs");
     return PF_OK;
@@ -511,9 +520,12 @@ extern "C" int pf_bwd_h_stage(const pf_plan *plan, const double *c,
   Workspace w = carve(workspace, pl.d.n, pl.d.dim);
   return dispatch(pl, [&](auto v) {
     double *cot_hu = w.vecs;
-    launch(k_bwd_h_cell<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, c, g_h, h, u_hin,
+    const int D = decltype(v)::kDim;
+    halo(pl, S(stream), {{const_cast<double *>(u_hin), D}});
+    launch(k_bwd_h_cell<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, c, g_h, h, u_hin,
                                                           da, g_rhs, dc, cot_hu);
-    launch(k_bwd_h_gather<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, c, cot_hu,
+    halo(pl, S(stream), {{cot_hu, D}});
+    launch(k_bwd_h_gather<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, c, cot_hu,
                                                             cu_out);
     PF_LAUNCH_CHECK("bwd_h_stage");
     return PF_OK;
@@ -525,7 +537,9 @@ extern "C" int pf_bwd_momentum_outer(const pf_plan *plan, const double *y,
                                      void *stream) {
   PF_REQUIRE(plan && y && u_star && dc, "pf_bwd_momentum_outer: null argument");
   return dispatch(P(plan), [&](auto v) {
-    launch(k_bwd_mom_outer<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, y, u_star, dc);
+    halo(P(plan), S(stream),
+         {{const_cast<double *>(u_star), decltype(v)::kDim}});
+    launch(k_bwd_mom_outer<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, y, u_star, dc);
     PF_LAUNCH_CHECK("bwd_momentum_outer");
     return PF_OK;
   });
@@ -541,7 +555,7 @@ extern "C" int pf_adj_momentum_rhs(const pf_plan *plan, const double *cot_rhs,
   PF_REQUIRE((bc && dbc) || pl.d.m == 0, "pf_adj_momentum_rhs: null bc");
   Workspace w = carve(workspace, pl.d.n, pl.d.dim);
   return dispatch(pl, [&](auto v) {
-    launch(k_adj_rhs_cells<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, cot_rhs, dt,
+    launch(k_adj_rhs_cells<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, cot_rhs, dt,
                                                              du_n);
     if (v.m > 0) {
       const int g = std::min(grid_for(v.m), pl.red_blocks);
@@ -562,7 +576,9 @@ extern "C" int pf_adj_assemble_momentum(const pf_plan *plan, const double *dc,
   const Plan &pl = P(plan);
   Workspace w = carve(workspace, pl.d.n, pl.d.dim);
   return dispatch(pl, [&](auto v) {
-    const int g = std::min(grid_for(v.n), pl.red_blocks);
+    const int g = std::min(grid_for(v.owned()), pl.red_blocks);
+    halo(pl, S(stream),
+         {{const_cast<double *>(dc), 2 * decltype(v)::kDim + 1}});
     launch(k_adj_assemble<decltype(v)>, g, kBlock, S(stream), v, dc, nu, du_n, dnu_dev,
                                                 w.partials, w.counters);
     PF_LAUNCH_CHECK("adj_assemble_momentum");

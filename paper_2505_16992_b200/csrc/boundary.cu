@@ -28,6 +28,9 @@ __global__ void __launch_bounds__(kBlock)
   double acc[3] = {0.0, 0.0, 0.0};
   for (int32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < v.m;
        e += gridDim.x * blockDim.x) {
+    // slab plans: entries of ghost-plane cells belong to a neighbour rank
+    const int32_t ie = __ldg(v.bcell + e);
+    if (ie < v.i0 || ie >= v.i1) continue;
     const int bf = __ldg(v.bface + e);
     const int f = bf & 15, kind = bf >> 4;
     const double nsgn = (f & 1) ? 1.0 : -1.0;
@@ -126,8 +129,8 @@ extern "C" int pf_advective_outflow_update(const pf_plan *plan,
   });
   if (rc) return rc;
   OutflowState hs;
-  PF_CUDA(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
-  PF_CUDA(cudaStreamSynchronize(s));
+  rc = d2h(pl, &hs, st, sizeof(hs), s);
+  if (rc) return rc;
   *scale_host = hs.scale;
   return PF_OK;
 }

@@ -26,7 +26,7 @@ __device__ __forceinline__ bool finite(double x) { return isfinite(x); }
 // z-bar, r.z and beta from the sums (sum z, sum r.z, sum r); `initial`
 // seeds rz for the first direction (S/linalg.py:146-149 / 162-168)
 __device__ __forceinline__ void cg_fin_z(SolverState *st, double sz,
-                                         double srz, double sr, int32_t n,
+                                         double srz, double sr, double n,
                                          bool initial) {
   CompState &c = st->c[0];
   c.zbar = st->zero_mean ? sz / n : 0.0;

@@ -10,11 +10,14 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <initializer_list>
 #include <string>
 
 #include "../../include/pisob200.h"
+#include "comm.cuh"
 
 namespace pf {
 
@@ -59,10 +62,18 @@ struct MgLevel {
 // Spectral preconditioner of a box with periodic, uniformly spaced X and Z
 // (see spectral.cuh): exact inverse of the XZ-plane-averaged operator.
 struct SpecPlan {
-  int32_t sx, sy, sz;  // canonical dims (sx == 1 in 2D)
+  int32_t sx, sy, sz;  // canonical dims (sx == 1 in 2D); sx is GLOBAL
   int32_t nkz;         // sz / 2 + 1 retained Z wavenumbers
   int32_t lpx, lpz;    // lines per CTA of the X / Z transforms
-  double2 *s;          // (sy, nkz, sx) spectral work array
+  // slab decomposition of X (comm.cuh): this rank owns X lines
+  // x0 .. x0 + nxl - 1 (stored at local plane x + xoff) and the Z
+  // wavenumbers kz0[rank] .. kz0[rank + 1] - 1 of the transposed spectrum;
+  // peer_s[q] is rank q's work array (own at [rank]).  Single GPU: nxl = sx,
+  // xoff = x0 = 0, one rank owning every kz.
+  int32_t nxl, xoff, x0, rank, world;
+  int32_t kz0[kMaxRanks + 1];
+  double2 *peer_s[kMaxRanks];
+  double2 *s;          // (sy, kz of this rank, sx) spectral work array
   double *cw;          // (sy, nkz * sx) Thomas c' scratch
   double *ax, *ay, *az;  // (sy) plane-mean face weights
   double2 *twx, *twz;    // exp(-2 pi i k / N), N = sx, sz
@@ -88,6 +99,8 @@ struct GraphCache {
   unsigned long long nkern = 0;
 };
 
+struct CommHost;
+
 // Host-side plan: the immutable device description plus derived launch
 // parameters.
 struct Plan {
@@ -98,7 +111,49 @@ struct Plan {
   MgHierarchy mg;
   int64_t mg_bytes;
   mutable GraphCache graph;
+  // slab decomposition along axis 0 (comm.cuh): owned cells [i0, i1) of the
+  // (nxl + 2)-plane local box; i0 = 0, i1 = n otherwise
+  bool slab = false;
+  int32_t i0 = 0, i1 = 0;
+  double ng = 0.0;  // owned cells summed over all ranks
+  int64_t plane = 0, nxl = 0;
+  CommHost *comm = nullptr;  // attached communicator (slab plans)
+  // pinned staging for the small device-to-host reads (solver state,
+  // scalars): a copy into pageable memory is staged through a buffer the
+  // driver shares between streams, which would serialise slabs that share
+  // a device
+  void *pinned = nullptr;
 };
+
+constexpr size_t kPinnedBytes = 4096;
+// copy `bytes` (<= kPinnedBytes) from device to host through the plan's
+// pinned buffer and wait for it (stream ordered)
+int d2h(const Plan &p, void *host, const void *dev, size_t bytes,
+        cudaStream_t s);
+
+// owned cell range of a plan, for the pointwise kernels
+struct Rng {
+  int32_t i0, i1;
+  double ng;
+};
+inline Rng plan_range(const Plan &p) { return Rng{p.i0, p.i1, p.ng}; }
+#define RANGE_LOOP(i, rg)                                                  \
+  for (int32_t i = (rg).i0 + blockIdx.x * blockDim.x + threadIdx.x;        \
+       i < (rg).i1; i += gridDim.x * blockDim.x)
+
+// halo exchange of the ghost planes of a set of arrays (no-op unless the
+// plan is a slab plan with a communicator), barrier, vector allreduce
+int halo_exchange(const Plan &p, const HaloItem *items, int count,
+                  cudaStream_t s);
+inline int halo(const Plan &p, cudaStream_t s,
+                std::initializer_list<HaloItem> items) {
+  return halo_exchange(p, items.begin(), (int)items.size(), s);
+}
+int comm_barrier(const Plan &p, cudaStream_t s);
+// PF_ERR_CUDA (with the details) once a device-side peer wait timed out
+int comm_check(const Plan &p, cudaStream_t s);
+int comm_vec_allreduce(const Plan &p, double *buf, int k, int op,
+                       cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // face lookup
@@ -209,6 +264,8 @@ struct View {
   Topo topo;
   int32_t n;
   int32_t m;
+  int32_t i0, i1;  // owned cells (the whole range unless a slab plan)
+  double ng;       // owned cells over all ranks (means, zero-mean projection)
   const double *__restrict__ jac;
   const double *__restrict__ tmat;   // (D*D, n)
   const double *__restrict__ alpha;  // (D, n)
@@ -224,6 +281,8 @@ struct View {
   const int32_t *__restrict__ finfo;      // (nfaces, 8)
   int32_t has_cross;
 
+  __device__ __forceinline__ Rng rng() const { return Rng{i0, i1, ng}; }
+  __host__ __device__ __forceinline__ int32_t owned() const { return i1 - i0; }
   __device__ __forceinline__ double AF(int a, int k, int32_t i) const {
     return __ldg(alpha_full + (int64_t)(a * D + k) * n + i);
   }
@@ -261,6 +320,9 @@ View<D, Topo> make_view(const Plan &p, const Topo &topo) {
   v.topo = topo;
   v.n = (int32_t)p.d.n;
   v.m = (int32_t)p.d.m;
+  v.i0 = p.i0;
+  v.i1 = p.i1;
+  v.ng = p.ng;
   v.jac = p.d.jac;
   v.tmat = p.d.tmat;
   v.alpha = p.d.alpha_diag;
@@ -469,13 +531,19 @@ __device__ __forceinline__ bool grid_reduce(double (&v)[K], double *partials,
 #pragma unroll
     for (int k = 0; k < K; ++k) tot[k] = acc[k];
     *counter = 0u;
+    // slab plans: fold the other ranks' totals in (rank order, all ranks
+    // get the same bits)
+    CommDev *c = ws_comm(counter);
+    if (c) comm_allreduce<K, kMax>(c, tot);
     return true;
   }
   return false;
 }
 
 // Workspace layout shared by all entry points (bytes, 256-aligned):
-//   [0, 4096)                 : counters (unsigned) + small scalar block
+//   [0, 4096)                 : counters (unsigned, 64), the plan's
+//                               CommDev* at byte 256 (kWsCommOffset),
+//                               small scalar block from byte 512
 //   partials                  : kMaxRedBlocks * kMaxK doubles
 //   solver scalars            : 4096 doubles
 //   solver vectors            : nvec * (3 * n) doubles

@@ -56,8 +56,8 @@ __global__ void __launch_bounds__(kBlock)
     k_xmom_x(V v, const double *__restrict__ u, double nu,
              double *__restrict__ x) {
   constexpr int D = V::kDim;
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= v.n) return;
+  const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.i1) return;
   const int64_t n = v.n;
   Face fc[2 * D];
   faces_of(v, i, fc);
@@ -86,8 +86,8 @@ template <class V>
 __global__ void __launch_bounds__(kBlock)
     k_xmom_div(V v, const double *__restrict__ x, double *__restrict__ rhs) {
   constexpr int D = V::kDim;
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= v.n) return;
+  const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.i1) return;
   const int64_t n = v.n;
   Face fc[2 * D];
   faces_of(v, i, fc);
@@ -119,8 +119,8 @@ __global__ void __launch_bounds__(kBlock)
     k_xp_x(V v, const double *__restrict__ c, const double *__restrict__ p,
            double *__restrict__ x) {
   constexpr int D = V::kDim;
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= v.n) return;
+  const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.i1) return;
   const int64_t n = v.n;
   Face fc[2 * D];
   faces_of(v, i, fc);
@@ -142,8 +142,8 @@ __global__ void __launch_bounds__(kBlock)
     k_xp_div(V v, const double *__restrict__ x, const double *__restrict__ b0,
              double *__restrict__ b) {
   constexpr int D = V::kDim;
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= v.n) return;
+  const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.i1) return;
   const int64_t n = v.n;
   Face fc[2 * D];
   faces_of(v, i, fc);
@@ -224,8 +224,8 @@ __global__ void __launch_bounds__(kBlock)
                const double *__restrict__ cot_out, double cs,
                double *__restrict__ da, double *__restrict__ cot_g) {
   constexpr int D = V::kDim;
-  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= v.n) return;
+  const int32_t j = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= v.i1) return;
   const int64_t n = v.n;
   Face fc[2 * D];
   faces_of(v, j, fc);
@@ -257,8 +257,8 @@ __global__ void __launch_bounds__(kBlock)
     k_adj_onesided(V v, const double *__restrict__ cot_g, int ncomp,
                    double *__restrict__ out, int accumulate) {
   constexpr int D = V::kDim;
-  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= v.n) return;
+  const int32_t j = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= v.i1) return;
   const int64_t n = v.n;
   Face fc[2 * D];
   faces_of(v, j, fc);
@@ -286,8 +286,7 @@ __global__ void __launch_bounds__(kBlock)
   constexpr int D = V::kDim;
   const int64_t n = v.n;
   double acc[1] = {0.0};
-  for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < v.n;
-       j += gridDim.x * blockDim.x) {
+  RANGE_LOOP(j, v.rng()) {
     Face fc[2 * D];
     faces_of(v, j, fc);
     double cx[D][D];  // cx[a][c]
@@ -367,9 +366,9 @@ extern "C" int pf_momentum_cross_rhs(const pf_plan *plan, const double *u,
   Workspace w = carve(workspace, pl.d.n, pl.d.dim);
   return dispatch(pl, [&](auto v) {
     double *x = w.vecs;  // (d*d, n)
-    launch(k_xmom_x<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, u, nu,
+    launch(k_xmom_x<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, u, nu,
            x);
-    launch(k_xmom_div<decltype(v)>, grid_for(v.n), kBlock, S(stream), v,
+    launch(k_xmom_div<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v,
            (const double *)x, rhs_inout);
     PF_LAUNCH_CHECK("momentum_cross_rhs");
     return PF_OK;
@@ -387,9 +386,9 @@ extern "C" int pf_pressure_cross_rhs(const pf_plan *plan, const double *c,
   Workspace w = carve(workspace, pl.d.n, pl.d.dim);
   return dispatch(pl, [&](auto v) {
     double *x = w.vecs;  // (d, n)
-    launch(k_xp_x<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, c,
+    launch(k_xp_x<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, c,
            p_prev, x);
-    launch(k_xp_div<decltype(v)>, grid_for(v.n), kBlock, S(stream), v,
+    launch(k_xp_div<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v,
            (const double *)x, b0, b_out);
     PF_LAUNCH_CHECK("pressure_cross_rhs");
     return PF_OK;
@@ -408,9 +407,9 @@ extern "C" int pf_adj_pressure_cross(const pf_plan *plan, const double *c,
   Workspace w = carve(workspace, pl.d.n, pl.d.dim);
   return dispatch(pl, [&](auto v) {
     double *cot_g = w.vecs;  // (d, n)
-    launch(k_axp_cell<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, c,
+    launch(k_axp_cell<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, c,
            p_prev, cot_out, cot_scale, da, cot_g);
-    launch(k_adj_onesided<decltype(v)>, grid_for(v.n), kBlock, S(stream), v,
+    launch(k_adj_onesided<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v,
            (const double *)cot_g, 1, dp_prev, 0);
     PF_LAUNCH_CHECK("adj_pressure_cross");
     return PF_OK;
@@ -430,10 +429,10 @@ extern "C" int pf_adj_momentum_cross(const pf_plan *plan, const double *u,
   return dispatch(pl, [&](auto v) {
     constexpr int D = decltype(v)::kDim;
     double *cot_g = w.vecs;  // (d*d, n) at [(k*D + c) * n]
-    const int g = std::min(grid_for(v.n), pl.red_blocks);
+    const int g = std::min(grid_for(v.owned()), pl.red_blocks);
     launch(k_axmom_cell<decltype(v)>, g, kBlock, S(stream), v, u, nu, cot_out,
            cot_g, dnu_dev, w.partials, w.counters);
-    launch(k_adj_onesided<decltype(v)>, grid_for(v.n), kBlock, S(stream), v,
+    launch(k_adj_onesided<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v,
            (const double *)cot_g, D, du_cross, (int)accumulate);
     PF_LAUNCH_CHECK("adj_momentum_cross");
     return PF_OK;

@@ -29,8 +29,8 @@ __global__ void __launch_bounds__(kBlock)
     k_assemble_momentum(V v, const double *__restrict__ flux,
                         double nu, double dt, double *__restrict__ c) {
   constexpr int D = V::kDim;
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= v.n) return;
+  const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.i1) return;
   const auto cell = v.topo.cell(i);
   const double invj = 1.0 / v.J(i);
   double diag = 1.0 / dt;
@@ -73,8 +73,8 @@ __global__ void __launch_bounds__(kBlock)
                    const double *__restrict__ src, int src_uniform, double nu,
                    double dt, double *__restrict__ rhs) {
   constexpr int D = V::kDim;
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= v.n) return;
+  const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.i1) return;
   const int64_t n = v.n;
   const auto cell = v.topo.cell(i);
   double r[D];
@@ -120,8 +120,8 @@ __global__ void __launch_bounds__(kBlock)
     k_assemble_pressure(V v, const double *__restrict__ c, int c_is_a_inv,
                         double *__restrict__ k) {
   constexpr int D = V::kDim;
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= v.n) return;
+  const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.i1) return;
   const int64_t n = v.n;
   const auto cell = v.topo.cell(i);
   const double ainv = c_is_a_inv ? c[i] : 1.0 / c[i];
@@ -152,8 +152,8 @@ __global__ void __launch_bounds__(kBlock)
               const double *__restrict__ u, const double *__restrict__ rhs,
               double *__restrict__ h) {
   constexpr int D = V::kDim;
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= v.n) return;
+  const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.i1) return;
   const int64_t n = v.n;
   const auto cell = v.topo.cell(i);
   double hu[D];
@@ -210,8 +210,8 @@ __global__ void __launch_bounds__(kBlock)
     k_divergence_rhs(V v, const double *__restrict__ flux,
                      const double *__restrict__ bc, double *__restrict__ b) {
   constexpr int D = V::kDim;
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= v.n) return;
+  const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.i1) return;
   b[i] = cell_divergence(v, i, flux, bc);
 }
 
@@ -222,8 +222,7 @@ __global__ void __launch_bounds__(kBlock)
                      unsigned *counter, double *out) {
   constexpr int D = V::kDim;
   double acc[1] = {0.0};
-  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < v.n;
-       i += gridDim.x * blockDim.x)
+  RANGE_LOOP(i, v.rng())
     acc[0] = fmax(acc[0], fabs(cell_divergence(v, i, flux, bc) / v.J(i)));
   double tot[1];
   if (grid_reduce<1, true>(acc, partials, counter, tot)) *out = tot[0];
@@ -255,8 +254,8 @@ __global__ void __launch_bounds__(kBlock)
                        const double *__restrict__ p,
                        const double *__restrict__ c, double *__restrict__ u) {
   constexpr int D = V::kDim;
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= v.n) return;
+  const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.i1) return;
   const int64_t n = v.n;
   const auto cell = v.topo.cell(i);
   double g[D];
@@ -279,8 +278,8 @@ __global__ void __launch_bounds__(kBlock)
     k_stencil_matvec(V v, const double *__restrict__ a, int ncomp,
                      const double *__restrict__ x, double *__restrict__ y) {
   constexpr int D = V::kDim;
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= v.n) return;
+  const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.i1) return;
   const int64_t n = v.n;
   const auto cell = v.topo.cell(i);
   for (int q = 0; q < ncomp; ++q) {
@@ -342,6 +341,7 @@ extern "C" int pf_contravariant_flux(const pf_plan *plan, const double *u,
                                      double *flux, void *stream) {
   PF_REQUIRE(plan && u && flux, "pf_contravariant_flux: null argument");
   return dispatch(P(plan), [&](auto v) {
+    halo(P(plan), S(stream), {{const_cast<double *>(u), decltype(v)::kDim}});
     launch(k_flux<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, u, flux);
     PF_LAUNCH_CHECK("k_flux");
     return PF_OK;
@@ -354,9 +354,16 @@ extern "C" int pf_assemble_momentum(const pf_plan *plan, const double *u_n,
   PF_REQUIRE(plan && u_n && flux_scratch && c_out,
              "pf_assemble_momentum: null argument");
   return dispatch(P(plan), [&](auto v) {
+    constexpr int D = decltype(v)::kDim;
+    // slab plans: the face means need the neighbours' flux, so the flux is
+    // formed on the ghost planes too (from exchanged velocities), and the
+    // assembled stencil's ghost rows are exchanged for the transposed
+    // gathers of the adjoint and the pressure assembly
+    halo(P(plan), S(stream), {{const_cast<double *>(u_n), D}});
     launch(k_flux<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, u_n, flux_scratch);
-    launch(k_assemble_momentum<decltype(v)>, grid_for(v.n), kBlock, S(stream), 
+    launch(k_assemble_momentum<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), 
         v, flux_scratch, nu, dt, c_out);
+    halo(P(plan), S(stream), {{c_out, 2 * D + 1}});
     PF_LAUNCH_CHECK("k_assemble_momentum");
     return PF_OK;
   });
@@ -369,7 +376,7 @@ extern "C" int pf_momentum_rhs(const pf_plan *plan, const double *u_n,
   PF_REQUIRE(plan && u_n && source && rhs_out, "pf_momentum_rhs: null argument");
   PF_REQUIRE(bc || P(plan).d.m == 0, "pf_momentum_rhs: null bc");
   return dispatch(P(plan), [&](auto v) {
-    launch(k_momentum_rhs<decltype(v)>, grid_for(v.n), kBlock, S(stream), 
+    launch(k_momentum_rhs<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), 
         v, u_n, bc, source, source_is_uniform, nu, dt, rhs_out);
     PF_LAUNCH_CHECK("k_momentum_rhs");
     return PF_OK;
@@ -381,8 +388,10 @@ extern "C" int pf_assemble_pressure(const pf_plan *plan, const double *c,
                                     void *stream) {
   PF_REQUIRE(plan && c && k_out, "pf_assemble_pressure: null argument");
   return dispatch(P(plan), [&](auto v) {
-    launch(k_assemble_pressure<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, c, c_is_a_inv,
+    halo(P(plan), S(stream), {{const_cast<double *>(c), 1}});
+    launch(k_assemble_pressure<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, c, c_is_a_inv,
                                                                  k_out);
+    halo(P(plan), S(stream), {{k_out, 2 * decltype(v)::kDim + 1}});
     PF_LAUNCH_CHECK("k_assemble_pressure");
     return PF_OK;
   });
@@ -393,7 +402,9 @@ extern "C" int pf_h_stage(const pf_plan *plan, const double *c,
                           double *h_out, void *stream) {
   PF_REQUIRE(plan && c && u_cur && rhs && h_out, "pf_h_stage: null argument");
   return dispatch(P(plan), [&](auto v) {
-    launch(k_h_stage<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, c, u_cur, rhs, h_out);
+    halo(P(plan), S(stream),
+         {{const_cast<double *>(u_cur), decltype(v)::kDim}});
+    launch(k_h_stage<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, c, u_cur, rhs, h_out);
     PF_LAUNCH_CHECK("k_h_stage");
     return PF_OK;
   });
@@ -406,8 +417,9 @@ extern "C" int pf_divergence_rhs(const pf_plan *plan, const double *h,
              "pf_divergence_rhs: null argument");
   PF_REQUIRE(bc || P(plan).d.m == 0, "pf_divergence_rhs: null bc");
   return dispatch(P(plan), [&](auto v) {
+    halo(P(plan), S(stream), {{const_cast<double *>(h), decltype(v)::kDim}});
     launch(k_flux<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, h, flux_scratch);
-    launch(k_divergence_rhs<decltype(v)>, grid_for(v.n), kBlock, S(stream), 
+    launch(k_divergence_rhs<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), 
         v, flux_scratch, bc, b_out);
     PF_LAUNCH_CHECK("k_divergence_rhs");
     return PF_OK;
@@ -419,7 +431,8 @@ extern "C" int pf_correct_velocity(const pf_plan *plan, const double *h,
                                    double *u_out, void *stream) {
   PF_REQUIRE(plan && h && p && c && u_out, "pf_correct_velocity: null argument");
   return dispatch(P(plan), [&](auto v) {
-    launch(k_correct_velocity<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, h, p, c,
+    halo(P(plan), S(stream), {{const_cast<double *>(p), 1}});
+    launch(k_correct_velocity<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, h, p, c,
                                                                  u_out);
     PF_LAUNCH_CHECK("k_correct_velocity");
     return PF_OK;
@@ -440,17 +453,15 @@ extern "C" int pf_divergence_max(const pf_plan *plan, const double *u,
   const Plan &pl = P(plan);
   Workspace w = carve(workspace, pl.d.n, pl.d.dim);
   int rc = dispatch(pl, [&](auto v) {
+    halo(pl, S(stream), {{const_cast<double *>(u), decltype(v)::kDim}});
     launch(k_flux<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, u, flux_scratch);
-    launch(k_divergence_max<decltype(v)>, red_grid(pl, v.n), kBlock,
+    launch(k_divergence_max<decltype(v)>, red_grid(pl, v.owned()), kBlock,
            S(stream), v, flux_scratch, bc, w.partials, w.counters, w.scalars);
     PF_LAUNCH_CHECK("k_divergence_max");
     return PF_OK;
   });
   if (rc) return rc;
-  PF_CUDA(cudaMemcpyAsync(out_host, w.scalars, sizeof(double),
-                          cudaMemcpyDeviceToHost, S(stream)));
-  PF_CUDA(cudaStreamSynchronize(S(stream)));
-  return PF_OK;
+  return d2h(pl, out_host, w.scalars, sizeof(double), S(stream));
 }
 
 extern "C" int pf_stencil_matvec(const pf_plan *plan, const double *a,
@@ -459,10 +470,13 @@ extern "C" int pf_stencil_matvec(const pf_plan *plan, const double *a,
   PF_REQUIRE(plan && a && x && y && ncomp >= 1, "pf_stencil_matvec: bad argument");
   return dispatch(P(plan), [&](auto v) {
     using V = decltype(v);
+    halo(P(plan), S(stream), {{const_cast<double *>(x), ncomp}});
     if (transpose)
-      launch(k_stencil_matvec<V, true>, grid_for(v.n), kBlock, S(stream), v, a, ncomp, x, y);
+      halo(P(plan), S(stream), {{const_cast<double *>(a), 2 * V::kDim + 1}});
+    if (transpose)
+      launch(k_stencil_matvec<V, true>, grid_for(v.owned()), kBlock, S(stream), v, a, ncomp, x, y);
     else
-      launch(k_stencil_matvec<V, false>, grid_for(v.n), kBlock, S(stream), v, a, ncomp, x, y);
+      launch(k_stencil_matvec<V, false>, grid_for(v.owned()), kBlock, S(stream), v, a, ncomp, x, y);
     PF_LAUNCH_CHECK("k_stencil_matvec");
     return PF_OK;
   });
@@ -477,10 +491,7 @@ static int reduce_common(const pf_plan *plan, const double *x, const double *y,
   launch(k_reduce, red_grid(pl, len), kBlock, S(stream), x, y, len, mode,
          w.partials, w.counters, w.scalars);
   PF_LAUNCH_CHECK("k_reduce");
-  PF_CUDA(cudaMemcpyAsync(out_host, w.scalars, sizeof(double),
-                          cudaMemcpyDeviceToHost, S(stream)));
-  PF_CUDA(cudaStreamSynchronize(S(stream)));
-  return PF_OK;
+  return d2h(pl, out_host, w.scalars, sizeof(double), S(stream));
 }
 
 extern "C" int pf_reduce_sum(const pf_plan *plan, const double *x, int64_t len,

@@ -411,7 +411,13 @@ bool mg_plan(const Plan &p, MgHierarchy &h, int64_t *bytes) {
   }
   if (sy < 2 || (sx <= 1 && sz <= 1)) return false;
   h.spectral = 0;
-  if (p.d.geom_precond == PF_GEOM_SPECTRAL && spec_ok(d, sx, sy, sz, px, pz)) {
+  // slab plans: the spectral solve transforms the global X axis (all-to-all
+  // over the ranks); the coarse levels of the multigrid are not distributed
+  const int sxg = p.slab ? (int)p.d.slab_nx : sx;
+  if (p.slab && (d != 3 || p.d.geom_precond != PF_GEOM_SPECTRAL ||
+                 !spec_ok(d, sxg, sy, sz, px, pz) || (p.nxl * sy) % 2))
+    return false;
+  if (p.d.geom_precond == PF_GEOM_SPECTRAL && spec_ok(d, sxg, sy, sz, px, pz)) {
     // level 0 face weights + the spectral solve, no coarse levels
     MgLevel &L = h.lv[0];
     L = MgLevel{};
@@ -424,7 +430,10 @@ bool mg_plan(const Plan &p, MgHierarchy &h, int64_t *bytes) {
     L.fx = L.fy = L.fz = 1;
     h.nlev = 1;
     h.spectral = 1;
-    spec_plan(h.sp, sx, sy, sz);
+    spec_plan(h.sp, sxg, sy, sz);
+    if (p.slab)
+      spec_slab_plan(h.sp, (int)p.nxl, (int)p.d.slab_x0, p.d.slab_rank,
+                     p.d.slab_world);
     *bytes = spec_level0_bytes(L.n) + spec_bytes(h.sp);
     return true;
   }
@@ -498,10 +507,10 @@ static int lines_grid(const MgLevel &L) {
 }
 
 int mg_setup(const MgHierarchy &h, const double *k, int64_t n, cudaStream_t s,
-             const int *done) {
+             const int *done, const Plan *pl) {
   launch(k_mg_faces0, grid_for(n), kBlock, s, h.lv[0], k, n, h.ax_of[0],
          h.ax_of[1], h.ax_of[2], done);
-  if (h.spectral) return spec_setup(h.lv[0], h.sp, s, done);
+  if (h.spectral) return spec_setup(h.lv[0], h.sp, s, done, pl);
   for (int l = 0; l + 1 < h.nlev; ++l)
     launch(k_mg_aggregate, grid_for(h.lv[l + 1].n), kBlock, s, h.lv[l],
            h.lv[l + 1], done);
@@ -556,12 +565,13 @@ static void vcycle(const MgHierarchy &h, int l, const double *r, double *x,
 
 int mg_apply(const MgHierarchy &h, const double *r, double *z, cudaStream_t s,
              const int *done, cudaEvent_t *ev, const CgFuse *fuse,
-             int red_blocks) {
+             int red_blocks, const Plan *pl) {
   MgHierarchy hh = h;
   hh.lv[0].r = const_cast<double *>(r);
   hh.lv[0].x = z;
   if (hh.spectral)
-    return spec_apply(hh.lv[0], hh.sp, r, z, s, done, ev, fuse, red_blocks);
+    return spec_apply(hh.lv[0], hh.sp, r, z, s, done, ev, fuse, red_blocks,
+                      pl);
   int fused_from = hh.nlev;
   for (int l = 1; l < hh.nlev; ++l)
     if (hh.lv[l].n <= kFusedCoarseMax) {

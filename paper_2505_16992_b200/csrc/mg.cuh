@@ -88,7 +88,7 @@ void mg_bind(MgHierarchy &h, void *base);
 // Setup for operator K (2d+1 stencil, K = -P): level-0 faces, coarse
 // aggregation, line factorisations.
 int mg_setup(const MgHierarchy &h, const double *k_stencil, int64_t n,
-             cudaStream_t s, const int *all_done);
+             cudaStream_t s, const int *all_done, const Plan *pl = nullptr);
 // z = V(r) on the fine level; every kernel returns at once when *all_done.
 // `ev` (optional, 6 events) is recorded around the level-0 kernels:
 // smooth | restrict | coarse levels | prolong | smooth.  `fuse` (optional)
@@ -96,6 +96,7 @@ int mg_setup(const MgHierarchy &h, const double *k_stencil, int64_t n,
 // separate z-sum kernel); it needs red_blocks.
 int mg_apply(const MgHierarchy &h, const double *r, double *z,
              cudaStream_t s, const int *all_done, cudaEvent_t *ev = nullptr,
-             const CgFuse *fuse = nullptr, int red_blocks = 0);
+             const CgFuse *fuse = nullptr, int red_blocks = 0,
+             const Plan *pl = nullptr);
 
 }  // namespace pf

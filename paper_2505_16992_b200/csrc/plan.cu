@@ -21,6 +21,18 @@ int cuda_check(cudaError_t e, const char *what) {
   return PF_ERR_CUDA;
 }
 
+int d2h(const Plan &p, void *host, const void *dev, size_t bytes,
+        cudaStream_t s) {
+  if (bytes > kPinnedBytes || !p.pinned) {
+    set_error("d2h: read too large for the plan's staging buffer");
+    return PF_ERR_ARG;
+  }
+  PF_CUDA(cudaMemcpyAsync(p.pinned, dev, bytes, cudaMemcpyDeviceToHost, s));
+  PF_CUDA(cudaStreamSynchronize(s));
+  std::memcpy(host, p.pinned, bytes);
+  return PF_OK;
+}
+
 }  // namespace pf
 
 using namespace pf;
@@ -75,6 +87,22 @@ extern "C" int pf_plan_create(const pf_plan_desc *desc, pf_plan **out) {
     set_error("pf_plan_create: unknown topology");
     return PF_ERR_ARG;
   }
+  const bool slab = d.slab_world > 0;
+  if (slab) {
+    if (d.topo != PF_TOPO_BOX || !d.box_periodic[0] || d.box_shape[0] < 3 ||
+        d.slab_world > kMaxRanks || d.slab_rank < 0 ||
+        d.slab_rank >= d.slab_world || d.slab_x0 < 0 ||
+        d.slab_x0 + d.box_shape[0] - 2 > d.slab_nx) {
+      set_error("pf_plan_create: a slab plan needs a box periodic along axis "
+                "0 with nxl + 2 planes, 0 <= slab_rank < slab_world <= 16 and "
+                "slab_x0 + nxl <= slab_nx");
+      return PF_ERR_ARG;
+    }
+    if (d.has_cross) {
+      set_error("pf_plan_create: slab plans support orthogonal grids only");
+      return PF_ERR_UNSUPPORTED;
+    }
+  }
   int dev = 0, sms = 148;
   PF_CUDA(cudaGetDevice(&dev));
   PF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -82,7 +110,26 @@ extern "C" int pf_plan_create(const pf_plan_desc *desc, pf_plan **out) {
   p->d = d;
   p->num_sms = sms;
   p->red_blocks = sms * 8 < kMaxRedBlocks ? sms * 8 : kMaxRedBlocks;
+  p->slab = slab;
+  if (slab) {
+    p->plane = d.n / d.box_shape[0];
+    p->nxl = d.box_shape[0] - 2;
+    p->i0 = (int32_t)p->plane;
+    p->i1 = (int32_t)(p->plane * (p->nxl + 1));
+    p->ng = (double)d.slab_nx * (double)p->plane;
+  } else {
+    p->i0 = 0;
+    p->i1 = (int32_t)d.n;
+    p->ng = (double)d.n;
+  }
   p->has_mg = mg_plan(*p, p->mg, &p->mg_bytes);
+  {
+    const cudaError_t e = cudaMallocHost(&p->pinned, kPinnedBytes);
+    if (e != cudaSuccess) {
+      delete p;
+      return cuda_check(e, "cudaMallocHost(plan staging)");
+    }
+  }
   *out = reinterpret_cast<pf_plan *>(p);
   return PF_OK;
 }
@@ -92,6 +139,7 @@ extern "C" int pf_plan_destroy(pf_plan *plan) {
   if (p) {
     if (p->graph.exec) cudaGraphExecDestroy(p->graph.exec);
     if (p->graph.cap) cudaStreamDestroy(p->graph.cap);
+    if (p->pinned) cudaFreeHost(p->pinned);
   }
   delete p;
   return PF_OK;
@@ -135,5 +183,6 @@ extern "C" int pf_mg_setup(const pf_plan *plan, const double *k,
   }
   MgHierarchy h = p.mg;
   mg_bind(h, mg_workspace);
-  return mg_setup(h, k, p.d.n, static_cast<cudaStream_t>(stream), nullptr);
+  return mg_setup(h, k, p.d.n, static_cast<cudaStream_t>(stream), nullptr,
+                  &p);
 }

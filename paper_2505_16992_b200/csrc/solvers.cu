@@ -14,6 +14,7 @@
 // state block.  The host only polls that block every few iterations, so the
 // GPU never waits on a host round trip per iteration.
 #include <algorithm>
+#include <cstdlib>
 
 #include "cgstate.cuh"
 #include "common.cuh"
@@ -88,22 +89,22 @@ __global__ void k_cg_reset(SolverState *st, int maxiter, int precond,
 }
 
 __global__ void __launch_bounds__(kBlock)
-    k_cg_bsum(const double *__restrict__ b, double bs, int32_t n,
+    k_cg_bsum(const double *__restrict__ b, double bs, Rng rg,
               SolverState *st, double *partials, unsigned *counter) {
   double acc[1] = {0.0};
-  GRID_LOOP(i, n) acc[0] += bs * b[i];
+  RANGE_LOOP(i, rg) acc[0] += bs * b[i];
   double tot[1];
   if (grid_reduce<1>(acc, partials, counter, tot))
-    st->c[0].bmean = st->zero_mean ? tot[0] / n : 0.0;
+    st->c[0].bmean = st->zero_mean ? tot[0] / rg.ng : 0.0;
 }
 
 __global__ void __launch_bounds__(kBlock)
     k_cg_bproj(const double *__restrict__ b, double bs,
-               double *__restrict__ bp, int32_t n, SolverState *st,
+               double *__restrict__ bp, Rng rg, SolverState *st,
                double *partials, unsigned *counter) {
   const double mean = st->c[0].bmean;
   double acc[1] = {0.0};
-  GRID_LOOP(i, n) {
+  RANGE_LOOP(i, rg) {
     const double x = bs * b[i] - mean;
     bp[i] = x;
     acc[0] += x * x;
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(kBlock)
                SolverState *st, double *partials, unsigned *counter) {
   if (st->all_done) return;
   double acc[1] = {0.0};
-  GRID_LOOP(i, v.n) {
+  RANGE_LOOP(i, v.rng()) {
     Face fc[2 * V::kDim];
     load_faces(v, i, fc);
     const double ri = bp[i] - apply_row<V, false>(v, i, fc, a, x);
@@ -139,7 +140,7 @@ __global__ void __launch_bounds__(kBlock)
   }
   double tot[1];
   if (grid_reduce<1>(acc, partials, counter, tot))
-    st->c[0].rmean = st->zero_mean ? tot[0] / v.n : 0.0;
+    st->c[0].rmean = st->zero_mean ? tot[0] / v.ng : 0.0;
 }
 
 // z value of cell i: the multigrid output vector, or M r pointwise
@@ -151,13 +152,13 @@ __device__ __forceinline__ double zval(int pc, const double *__restrict__ a,
 
 // r -= mean(r); |r|; (pointwise preconditioners) z sums
 __global__ void __launch_bounds__(kBlock)
-    k_cg_rproj(const double *__restrict__ a, double *__restrict__ r, int32_t n,
+    k_cg_rproj(const double *__restrict__ a, double *__restrict__ r, Rng rg,
                SolverState *st, double *partials, unsigned *counter) {
   if (st->all_done) return;
   const double rmean = st->c[0].rmean;
   const int pc = st->precond;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  GRID_LOOP(i, n) {
+  RANGE_LOOP(i, rg) {
     const double ri = r[i] - rmean;
     r[i] = ri;
     acc[0] += ri * ri;
@@ -178,18 +179,18 @@ __global__ void __launch_bounds__(kBlock)
       st->all_done = 1;
       return;
     }
-    if (pc != 2) cg_fin_z(st, tot[1], tot[2], tot[3], n, true);
+    if (pc != 2) cg_fin_z(st, tot[1], tot[2], tot[3], rg.ng, true);
   }
 }
 
 // z sums for a stored z (multigrid), then beta
 __global__ void __launch_bounds__(kBlock)
     k_cg_zsum(const double *__restrict__ r, const double *__restrict__ z,
-              int32_t n, int initial, SolverState *st, double *partials,
+              Rng rg, int initial, SolverState *st, double *partials,
               unsigned *counter) {
   if (st->all_done) return;
   double acc[3] = {0.0, 0.0, 0.0};
-  GRID_LOOP(i, n) {
+  RANGE_LOOP(i, rg) {
     const double ri = r[i], zi = z[i];
     acc[0] += zi;
     acc[1] += ri * zi;
@@ -197,17 +198,17 @@ __global__ void __launch_bounds__(kBlock)
   }
   double tot[3];
   if (grid_reduce<3>(acc, partials, counter, tot))
-    cg_fin_z(st, tot[0], tot[1], tot[2], n, initial != 0);
+    cg_fin_z(st, tot[0], tot[1], tot[2], rg.ng, initial != 0);
 }
 
 __global__ void __launch_bounds__(kBlock)
     k_cg_pinit(const double *__restrict__ a, const double *__restrict__ r,
                const double *__restrict__ z, double *__restrict__ p,
-               int32_t n, const SolverState *st) {
+               Rng rg, const SolverState *st) {
   if (st->all_done) return;
   const double zbar = st->c[0].zbar;
   const int pc = st->precond;
-  GRID_LOOP(i, n) p[i] = zval(pc, a, z, i, r[i]) - zbar;
+  RANGE_LOOP(i, rg) p[i] = zval(pc, a, z, i, r[i]) - zbar;
 }
 
 // q = A p; p.q -> alpha
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(kBlock)
               unsigned *counter) {
   if (st->all_done) return;
   double acc[1] = {0.0};
-  GRID_LOOP(i, v.n) {
+  RANGE_LOOP(i, v.rng()) {
     Face fc[2 * V::kDim];
     load_faces(v, i, fc);
     const double qi = apply_row<V, false>(v, i, fc, a, p);
@@ -244,12 +245,12 @@ __global__ void __launch_bounds__(kBlock)
 // diagonal as their sum): 40 B/cell in 3D instead of the 72 B/cell of the
 // (2d+1)-row stencil
 __global__ void __launch_bounds__(kBlock)
-    k_cg_spmv_faces(MgLevel L, const double *__restrict__ p,
+    k_cg_spmv_faces(MgLevel L, Rng rg, const double *__restrict__ p,
                     double *__restrict__ q, SolverState *st, double *partials,
                     unsigned *counter) {
   if (st->all_done) return;
   double acc[1] = {0.0};
-  GRID_LOOP(i, (int32_t)L.n) {
+  RANGE_LOOP(i, rg) {
     const Cell3 c = decode(L, i);
     const Nbhd b = nbhd(L, c);
     const double qi = kx(b, i, p);
@@ -275,13 +276,13 @@ __global__ void __launch_bounds__(kBlock)
 __global__ void __launch_bounds__(kBlock)
     k_cg_update(const double *__restrict__ a, const double *__restrict__ p,
                 const double *__restrict__ q, double *__restrict__ x,
-                double *__restrict__ r, int32_t n, SolverState *st,
+                double *__restrict__ r, Rng rg, SolverState *st,
                 double *partials, unsigned *counter) {
   if (st->all_done) return;
   const double alpha = st->c[0].alpha;
   const int pc = st->precond;
   double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  GRID_LOOP(i, n) {
+  RANGE_LOOP(i, rg) {
     const double xi = x[i] + alpha * p[i];
     const double ri = r[i] - alpha * q[i];
     x[i] = xi;
@@ -303,32 +304,32 @@ __global__ void __launch_bounds__(kBlock)
       c.converged = 1;
       c.done = 1;
       c.project_x = st->zero_mean;
-      c.xmean = st->zero_mean ? tot[4] / n : 0.0;
+      c.xmean = st->zero_mean ? tot[4] / rg.ng : 0.0;
       st->all_done = 1;
       return;
     }
-    if (pc != 2) cg_fin_z(st, tot[1], tot[2], tot[3], n, false);
+    if (pc != 2) cg_fin_z(st, tot[1], tot[2], tot[3], rg.ng, false);
   }
 }
 
 __global__ void __launch_bounds__(kBlock)
     k_cg_pupdate(const double *__restrict__ a, const double *__restrict__ r,
                  const double *__restrict__ z, double *__restrict__ p,
-                 int32_t n, const SolverState *st) {
+                 Rng rg, const SolverState *st) {
   if (st->all_done) return;
   const double beta = st->c[0].beta, zbar = st->c[0].zbar;
   const int pc = st->precond;
-  GRID_LOOP(i, n) p[i] = beta * p[i] + (zval(pc, a, z, i, r[i]) - zbar);
+  RANGE_LOOP(i, rg) p[i] = beta * p[i] + (zval(pc, a, z, i, r[i]) - zbar);
 }
 
 __global__ void __launch_bounds__(kBlock)
-    k_cg_finish(double *__restrict__ x, int32_t n, const SolverState *st) {
+    k_cg_finish(double *__restrict__ x, Rng rg, const SolverState *st) {
   const CompState &c = st->c[0];
   if (c.zero_rhs) {
-    GRID_LOOP(i, n) x[i] = 0.0;
+    RANGE_LOOP(i, rg) x[i] = 0.0;
   } else if (c.project_x) {
     const double m = c.xmean;
-    GRID_LOOP(i, n) x[i] -= m;
+    RANGE_LOOP(i, rg) x[i] -= m;
   }
 }
 
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(kBlock)
                SolverState *st, double *partials, unsigned *counter) {
   double acc[3] = {0.0, 0.0, 0.0};
   const int64_t n = v.n;
-  GRID_LOOP(i, v.n) {
+  RANGE_LOOP(i, v.rng()) {
     Face fc[2 * V::kDim];
     load_faces(v, i, fc);
     for (int q = 0; q < ncomp; ++q) {
@@ -405,11 +406,11 @@ __global__ void k_bi_reset(SolverState *st, int ncomp, int maxiter,
 }
 
 __global__ void __launch_bounds__(kBlock)
-    k_bi_bnorm(const double *__restrict__ b, int32_t n, SolverState *st,
+    k_bi_bnorm(const double *__restrict__ b, int32_t n, Rng rg, SolverState *st,
                double *partials, unsigned *counter) {
   const int nc = st->ncomp;
   double acc[3] = {0.0, 0.0, 0.0};
-  GRID_LOOP(i, n) {
+  RANGE_LOOP(i, rg) {
     for (int q = 0; q < nc; ++q) {
       const double x = b[(int64_t)q * n + i];
       acc[q] += x * x;
@@ -446,7 +447,7 @@ __global__ void __launch_bounds__(kBlock)
   for (int q = 0; q < 3; ++q) act[q] = q < nc && !st->c[q].done;
   double acc[3] = {0.0, 0.0, 0.0};
   const int pc = st->precond;
-  GRID_LOOP(i, v.n) {
+  RANGE_LOOP(i, v.rng()) {
     Face fc[2 * V::kDim];
     load_faces(v, i, fc);
     w.dinv[i] = pc ? 1.0 / a[i] : 1.0;
@@ -538,7 +539,7 @@ __global__ void __launch_bounds__(kBlock)
   double *__restrict__ p1 = w.p[par ^ 1];
   double *__restrict__ v1 = w.v[par ^ 1];
   double acc[3] = {0.0, 0.0, 0.0};
-  GRID_LOOP(i, v.n) {
+  RANGE_LOOP(i, v.rng()) {
     Face fc[2 * V::kDim];
     load_faces(v, i, fc);
     auto pnew = [&](int q, int32_t j) {
@@ -595,7 +596,7 @@ __global__ void __launch_bounds__(kBlock)
   const double *__restrict__ dinv = w.dinv;
   const double *__restrict__ v1 = w.v[par ^ 1];
   double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  GRID_LOOP(i, v.n) {
+  RANGE_LOOP(i, v.rng()) {
     Face fc[2 * V::kDim];
     load_faces(v, i, fc);
     auto sval = [&](int q, int32_t j) {
@@ -642,7 +643,7 @@ __global__ void __launch_bounds__(kBlock)
 // x += alpha phat + omega shat; r = s - omega t; |r|, r^.r -> next beta
 __global__ void __launch_bounds__(kBlock)
     k_bi_xr(const double *__restrict__ a, BiVecs w, int par,
-            double *__restrict__ x, int32_t n, SolverState *st,
+            double *__restrict__ x, int32_t n, Rng rg, SolverState *st,
             double *partials, unsigned *counter) {
   if (st->all_done) return;
   const int nc = st->ncomp, pc = st->precond;
@@ -657,7 +658,7 @@ __global__ void __launch_bounds__(kBlock)
   const double *__restrict__ p1 = w.p[par ^ 1];
   const double *__restrict__ v1 = w.v[par ^ 1];
   double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  GRID_LOOP(i, n) {
+  RANGE_LOOP(i, rg) {
     const double di = w.dinv[i];
     _Pragma("unroll") for (int q = 0; q < 3; ++q) {
       if (q >= nc) break;
@@ -707,10 +708,10 @@ __global__ void __launch_bounds__(kBlock)
 }
 
 __global__ void __launch_bounds__(kBlock)
-    k_bi_finish(double *__restrict__ x, int32_t n, const SolverState *st) {
+    k_bi_finish(double *__restrict__ x, int32_t n, Rng rg, const SolverState *st) {
   for (int q = 0; q < st->ncomp; ++q) {
     if (!st->c[q].zero_rhs) continue;
-    GRID_LOOP(i, n) x[(int64_t)q * n + i] = 0.0;
+    RANGE_LOOP(i, rg) x[(int64_t)q * n + i] = 0.0;
   }
 }
 
@@ -723,18 +724,24 @@ using namespace pf;
 
 static cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
 
-static int read_state(SolverState *dev, SolverState *host, cudaStream_t s) {
-  PF_CUDA(cudaMemcpyAsync(host, dev, sizeof(SolverState),
-                          cudaMemcpyDeviceToHost, s));
-  PF_CUDA(cudaStreamSynchronize(s));
-  return PF_OK;
+static int read_state(const Plan &pl, SolverState *dev, SolverState *host,
+                      cudaStream_t s) {
+  return d2h(pl, host, dev, sizeof(SolverState), s);
 }
 
 namespace {
 
 // iterations to launch before the next host poll
 int next_batch(int done_iters, int hint) {
-  int b = std::max(4, std::min(64, done_iters / 2));
+  // PF_MAX_BATCH caps the iterations in flight between host polls (the
+  // in-process slab tests: several slabs' launch queues share one context,
+  // and a host thread blocked on a full queue must not starve a peer slab)
+  static const int cap = [] {
+    const char *e = getenv("PF_MAX_BATCH");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v : 64;
+  }();
+  int b = std::max(std::min(4, cap), std::min(cap, done_iters / 2));
   if (hint > done_iters) b = std::max(2, std::min(b, hint - done_iters));
   return b;
 }
@@ -745,27 +752,29 @@ void mg_iteration(const Plan &pl, Workspace &w, SolverState *st,
   const int32_t n = (int32_t)pl.d.n;
   double *r = w.vecs, *p = w.vecs + n, *q = w.vecs + 2 * (int64_t)n;
   double *z = w.vecs + 4 * (int64_t)n;
-  const int ge = grid_for(n), gr = std::min(grid_for(n), pl.red_blocks);
-  launch(k_cg_spmv_faces, gr, kBlock, s, mg->lv[0], (const double *)p, q, st,
+  const int ge = grid_for(pl.i1 - pl.i0), gr = std::min(ge, pl.red_blocks);
+  const Rng rg = plan_range(pl);
+  halo(pl, s, {{p, 1}});
+  launch(k_cg_spmv_faces, gr, kBlock, s, mg->lv[0], rg, (const double *)p, q, st,
          w.partials, w.counters);
   launch(k_cg_update, gr, kBlock, s, (const double *)nullptr,
-         (const double *)p, (const double *)q, x, r, n, st, w.partials,
+         (const double *)p, (const double *)q, x, r, rg, st, w.partials,
          w.counters);
   // the V-cycle's last smoothing pass also forms the z-sums and beta
   const CgFuse fuse{st, w.partials, w.counters, 0};
-  mg_apply(*mg, r, z, s, &st->all_done, nullptr, &fuse, pl.red_blocks);
+  mg_apply(*mg, r, z, s, &st->all_done, nullptr, &fuse, pl.red_blocks, &pl);
   launch(k_cg_pupdate, ge, kBlock, s, (const double *)nullptr,
-         (const double *)r, (const double *)z, p, n, st);
+         (const double *)r, (const double *)z, p, rg, st);
 }
 
 // r = bp - K x on the multigrid level-0 face form
 __global__ void __launch_bounds__(kBlock)
-    k_cg_resid_faces(MgLevel L, const double *__restrict__ bp,
+    k_cg_resid_faces(MgLevel L, Rng rg, const double *__restrict__ bp,
                      const double *__restrict__ x, double *__restrict__ r,
                      SolverState *st, double *partials, unsigned *counter) {
   if (st->all_done) return;
   double acc[1] = {0.0};
-  GRID_LOOP(i, (int32_t)L.n) {
+  RANGE_LOOP(i, rg) {
     const Cell3 c = decode(L, i);
     const double ri = bp[i] - kx(nbhd(L, c), i, x);
     r[i] = ri;
@@ -773,7 +782,7 @@ __global__ void __launch_bounds__(kBlock)
   }
   double tot[1];
   if (grid_reduce<1>(acc, partials, counter, tot))
-    st->c[0].rmean = st->zero_mean ? tot[0] / L.n : 0.0;
+    st->c[0].rmean = st->zero_mean ? tot[0] / rg.ng : 0.0;
 }
 
 constexpr int kGraphIters = 4;  // MG-PCG iterations per graph launch
@@ -822,37 +831,54 @@ int cg_core_mg(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   double *r = w.vecs, *p = w.vecs + n;
   double *z = w.vecs + 4 * (int64_t)n;
   const int *done = &st->all_done;
-  const int ge = grid_for(n), gr = std::min(grid_for(n), pl.red_blocks);
+  const int ge = grid_for(pl.i1 - pl.i0), gr = std::min(ge, pl.red_blocks);
+  const Rng rg = plan_range(pl);
   (void)a;
   launch(k_cg_reset, 1, 1, s, st, maxiter, 2, zero_mean, tol, 0);
-  launch(k_cg_resid_faces, gr, kBlock, s, mg->lv[0], bp, (const double *)x,
+  halo(pl, s, {{x, 1}});
+  launch(k_cg_resid_faces, gr, kBlock, s, mg->lv[0], rg, bp, (const double *)x,
          r, st, w.partials, w.counters);
-  launch(k_cg_rproj, gr, kBlock, s, (const double *)nullptr, r, n, st,
+  launch(k_cg_rproj, gr, kBlock, s, (const double *)nullptr, r, rg, st,
          w.partials, w.counters);
   const CgFuse fuse{st, w.partials, w.counters, 1};
-  int rc = mg_apply(*mg, r, z, s, done, nullptr, &fuse, pl.red_blocks);
+  int rc = mg_apply(*mg, r, z, s, done, nullptr, &fuse, pl.red_blocks, &pl);
   if (rc) return rc;
   launch(k_cg_pinit, ge, kBlock, s, (const double *)nullptr, r,
-         (const double *)z, p, n, st);
+         (const double *)z, p, rg, st);
   PF_LAUNCH_CHECK("mg-cg setup");
-  cudaGraphExec_t exec;
+  // PF_NO_GRAPHS=1: launch the iterations directly (the in-process slab
+  // tests: instantiating a graph may wait for the whole device while other
+  // slabs' kernels spin on this one)
+  static const bool no_graphs = [] {
+    const char *e = getenv("PF_NO_GRAPHS");
+    return e && e[0] == '1';
+  }();
+  cudaGraphExec_t exec = nullptr;
   unsigned long long nk = 0;
-  rc = mg_graph(pl, w, st, mg, x, &exec, &nk);
-  if (rc) return rc;
+  if (!no_graphs) {
+    rc = mg_graph(pl, w, st, mg, x, &exec, &nk);
+    if (rc) return rc;
+  }
   int launched = 0;
   for (;;) {
-    rc = read_state(st, &hs, s);
+    rc = read_state(pl, st, &hs, s);
+    if (!rc) rc = comm_check(pl, s);
     if (rc) return rc;
     if (hs.all_done || launched >= maxiter) break;
     int b = std::min(next_batch(launched, 0), maxiter - launched);
     b = std::max(1, (b + kGraphIters - 1) / kGraphIters);
     for (int k = 0; k < b; ++k) {
-      PF_CUDA(cudaGraphLaunch(exec, s));
-      g_launches += nk;
+      if (exec) {
+        PF_CUDA(cudaGraphLaunch(exec, s));
+        g_launches += nk;
+      } else {
+        for (int j = 0; j < kGraphIters; ++j)
+          mg_iteration(pl, w, st, mg, x, s);
+      }
     }
     launched += b * kGraphIters;
   }
-  launch(k_cg_finish, ge, kBlock, s, x, n, st);
+  launch(k_cg_finish, ge, kBlock, s, x, rg, st);
   PF_LAUNCH_CHECK("mg-cg finish");
   return PF_OK;
 }
@@ -866,7 +892,8 @@ int cg_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   double *r = w.vecs, *p = w.vecs + n, *q = w.vecs + 2 * (int64_t)n;
   double *z = w.vecs + 4 * (int64_t)n;
   const int *done = &st->all_done;
-  const int ge = grid_for(n), gr = std::min(grid_for(n), pl.red_blocks);
+  const int ge = grid_for(pl.i1 - pl.i0), gr = std::min(ge, pl.red_blocks);
+  const Rng rg = plan_range(pl);
   if (precond == 2) {
     // the multigrid iteration runs from a CUDA graph whose buffers are all
     // workspace-resident: iterate on a copy of x, copy the solution back
@@ -875,46 +902,52 @@ int cg_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
                             cudaMemcpyDeviceToDevice, s));
     int rc = cg_core_mg(pl, v, w, st, hs, a, bp, xw, tol, maxiter, zero_mean,
                         mg, s);
-    if (!rc) rc = read_state(st, &hs, s);
+    if (!rc) rc = read_state(pl, st, &hs, s);
     if (rc) return rc;
     PF_CUDA(cudaMemcpyAsync(x, xw, sizeof(double) * n,
                             cudaMemcpyDeviceToDevice, s));
-    if (hs.c[0].converged && !hs.c[0].zero_rhs)
+    if (hs.c[0].converged && !hs.c[0].zero_rhs) {
+      halo(pl, s, {{x, 1}});
       launch(k_true_res<V>, gr, kBlock, s, v, a, 0, 1, bp, (const double *)x,
              st, w.partials, w.counters);
+    }
     PF_LAUNCH_CHECK("mg-cg true residual");
-    return read_state(st, &hs, s);
+    return read_state(pl, st, &hs, s);
   }
   launch(k_cg_reset, 1, 1, s, st, maxiter, precond, zero_mean, tol, 0);
+  halo(pl, s, {{x, 1}});
   launch(k_cg_resid<V>, gr, kBlock, s, v, a, bp, x, r, st, w.partials,
                                       w.counters);
-  launch(k_cg_rproj, gr, kBlock, s, a, r, n, st, w.partials, w.counters);
+  launch(k_cg_rproj, gr, kBlock, s, a, r, rg, st, w.partials, w.counters);
   (void)done;
-  launch(k_cg_pinit, ge, kBlock, s, a, r, (const double *)z, p, n, st);
+  launch(k_cg_pinit, ge, kBlock, s, a, r, (const double *)z, p, rg, st);
   PF_LAUNCH_CHECK("cg setup");
   int launched = 0;
   for (;;) {
-    int rc = read_state(st, &hs, s);
+    int rc = read_state(pl, st, &hs, s);
+    if (!rc) rc = comm_check(pl, s);
     if (rc) return rc;
     if (hs.all_done || launched >= maxiter) break;
     const int b = std::min(next_batch(launched, 0), maxiter - launched);
     for (int k = 0; k < b; ++k) {
+      halo(pl, s, {{p, 1}});
       launch(k_cg_spmv<V>, gr, kBlock, s, v, a, p, q, st, w.partials,
              w.counters);
-      launch(k_cg_update, gr, kBlock, s, a, p, q, x, r, n, st, w.partials,
+      launch(k_cg_update, gr, kBlock, s, a, p, q, x, r, rg, st, w.partials,
                                         w.counters);
-      launch(k_cg_pupdate, ge, kBlock, s, a, r, (const double *)z, p, n, st);
+      launch(k_cg_pupdate, ge, kBlock, s, a, r, (const double *)z, p, rg, st);
     }
     PF_LAUNCH_CHECK("cg iterations");
     launched += b;
   }
-  launch(k_cg_finish, ge, kBlock, s, x, n, st);
+  launch(k_cg_finish, ge, kBlock, s, x, rg, st);
   if (hs.c[0].converged && !hs.c[0].zero_rhs) {
+    halo(pl, s, {{x, 1}});
     launch(k_true_res<V>, gr, kBlock, s, v, a, 0, 1, bp, x, st, w.partials,
                                         w.counters);
   }
   PF_LAUNCH_CHECK("cg finish");
-  return read_state(st, &hs, s);
+  return read_state(pl, st, &hs, s);
 }
 
 }  // namespace
@@ -949,13 +982,14 @@ extern "C" int pf_cg_solve(const pf_plan *plan, const double *a,
   double *bp = w.vecs + 3 * (int64_t)n;
   return dispatch(pl, [&](auto v) {
     using V = decltype(v);
-    const int gr = std::min(grid_for(n), pl.red_blocks);
+    const int gr = std::min(grid_for(pl.i1 - pl.i0), pl.red_blocks);
+    const Rng rg = plan_range(pl);
     SolverState hs;
     if (!has_x0) PF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
     launch(k_cg_reset, 1, 1, s, st, maxiter, precond, zero_mean, tol, 1);
-    launch(k_cg_bsum, gr, kBlock, s, b, b_scale, n, st, w.partials,
+    launch(k_cg_bsum, gr, kBlock, s, b, b_scale, rg, st, w.partials,
                                     w.counters);
-    launch(k_cg_bproj, gr, kBlock, s, b, b_scale, bp, n, st, w.partials,
+    launch(k_cg_bproj, gr, kBlock, s, b, b_scale, bp, rg, st, w.partials,
                                      w.counters);
     PF_LAUNCH_CHECK("cg rhs");
     int rc = cg_core<V>(pl, v, w, st, hs, a, bp, x, tol, maxiter, precond,
@@ -1015,36 +1049,45 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   bv.v[0] = base + 5 * len;
   bv.v[1] = base + 6 * len;
   bv.dinv = base + 7 * len;
-  const int ge = grid_for(n), gr = std::min(grid_for(n), pl.red_blocks);
+  const int ge = grid_for(pl.i1 - pl.i0), gr = std::min(ge, pl.red_blocks);
+  const Rng rg = plan_range(pl);
   launch(k_bi_reset, 1, 1, s, st, ncomp, maxiter, precond, tol, fresh, mask);
-  if (fresh) launch(k_bi_bnorm, gr, kBlock, s, b, n, st, w.partials, w.counters);
+  if (fresh) launch(k_bi_bnorm, gr, kBlock, s, b, n, rg, st, w.partials, w.counters);
+  halo(pl, s, {{x, ncomp}});
   launch(k_bi_init<V, kTrans>, gr, kBlock, s, v, a, b, x, bv, st, w.partials,
                                              w.counters);
+  // slab plans: the stencil passes gather r, p, v and 1 / A_jj of the
+  // neighbours (v[0] = 0 and dinv are exchanged once here)
+  halo(pl, s, {{bv.v[0], ncomp}, {bv.dinv, 1}});
   PF_LAUNCH_CHECK("bicgstab setup");
   int launched = 0;
   for (;;) {
-    int rc = read_state(st, &hs, s);
+    int rc = read_state(pl, st, &hs, s);
+    if (!rc) rc = comm_check(pl, s);
     if (rc) return rc;
     if (hs.all_done || launched >= maxiter) break;
     const int bsz = std::min(launched < 4 ? 2 : next_batch(launched, 0),
                              maxiter - launched);
     for (int k = 0; k < bsz; ++k) {
       const int par = (launched + k) & 1;
+      halo(pl, s, {{bv.r, ncomp}, {bv.p[par], ncomp}});
       launch(k_bi_pv<V, kTrans>, gr, kBlock, s, v, a, bv, par, st,
              w.partials, w.counters);
+      halo(pl, s, {{bv.v[par ^ 1], ncomp}});
       launch(k_bi_st<V, kTrans>, gr, kBlock, s, v, a, bv, par, st,
              w.partials, w.counters);
-      launch(k_bi_xr, gr, kBlock, s, a, bv, par, x, n, st, w.partials,
+      launch(k_bi_xr, gr, kBlock, s, a, bv, par, x, n, rg, st, w.partials,
              w.counters);
     }
     PF_LAUNCH_CHECK("bicgstab iterations");
     launched += bsz;
   }
-  launch(k_bi_finish, ge, kBlock, s, x, n, st);
+  launch(k_bi_finish, ge, kBlock, s, x, n, rg, st);
+  halo(pl, s, {{x, ncomp}});
   launch(k_true_res<V>, gr, kBlock, s, v, a, kTrans ? 1 : 0, ncomp, b, x, st,
                                       w.partials, w.counters);
   PF_LAUNCH_CHECK("bicgstab finish");
-  return read_state(st, &hs, s);
+  return read_state(pl, st, &hs, s);
 }
 
 }  // namespace
@@ -1160,51 +1203,53 @@ extern "C" int pf_cg_profile(const pf_plan *plan, const double *a,
   const int *done = &st->all_done;
   return dispatch(pl, [&](auto v) {
     using V = decltype(v);
-    const int ge = grid_for(n), gr = std::min(grid_for(n), pl.red_blocks);
+    const int ge = grid_for(pl.i1 - pl.i0), gr = std::min(ge, pl.red_blocks);
+  const Rng rg = plan_range(pl);
     PF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
     // room for the timed iterations plus the graph-replay measurement
     launch(k_cg_reset, 1, 1, s, st, 2 * iters + 2 * kGraphIters + 1, precond,
            1, 0.0, 1);
-    launch(k_cg_bsum, gr, kBlock, s, b, 1.0, n, st, w.partials, w.counters);
-    launch(k_cg_bproj, gr, kBlock, s, b, 1.0, bp, n, st, w.partials,
+    launch(k_cg_bsum, gr, kBlock, s, b, 1.0, rg, st, w.partials, w.counters);
+    launch(k_cg_bproj, gr, kBlock, s, b, 1.0, bp, rg, st, w.partials,
            w.counters);
     launch(k_cg_resid<V>, gr, kBlock, s, v, a, bp, x, r, st, w.partials,
            w.counters);
-    launch(k_cg_rproj, gr, kBlock, s, a, r, n, st, w.partials, w.counters);
+    launch(k_cg_rproj, gr, kBlock, s, a, r, rg, st, w.partials, w.counters);
     if (precond == 2) {
       const CgFuse fuse{st, w.partials, w.counters, 1};
-      int rc = mg_apply(mg, r, z, s, done, nullptr, &fuse, pl.red_blocks);
+      int rc = mg_apply(mg, r, z, s, done, nullptr, &fuse, pl.red_blocks, &pl);
       if (rc) return rc;
     }
-    launch(k_cg_pinit, ge, kBlock, s, a, r, (const double *)z, p, n, st);
+    launch(k_cg_pinit, ge, kBlock, s, a, r, (const double *)z, p, rg, st);
     // events: 0 start | 1 spmv | 2 update | 3..8 mg level-0 marks | 9 zsum |
     // 10 pupdate
     cudaEvent_t ev[11];
     for (auto &e : ev) PF_CUDA(cudaEventCreate(&e));
     double tot[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     for (int k = 0; k < iters; ++k) {
+      halo(pl, s, {{p, 1}});
       PF_CUDA(cudaEventRecord(ev[0], s));
       if (precond == 2)
-        launch(k_cg_spmv_faces, gr, kBlock, s, mg.lv[0], (const double *)p,
+        launch(k_cg_spmv_faces, gr, kBlock, s, mg.lv[0], rg, (const double *)p,
                q, st, w.partials, w.counters);
       else
         launch(k_cg_spmv<V>, gr, kBlock, s, v, a, p, q, st, w.partials,
                w.counters);
       PF_CUDA(cudaEventRecord(ev[1], s));
-      launch(k_cg_update, gr, kBlock, s, a, p, q, x, r, n, st, w.partials,
+      launch(k_cg_update, gr, kBlock, s, a, p, q, x, r, rg, st, w.partials,
              w.counters);
       PF_CUDA(cudaEventRecord(ev[2], s));
       if (precond == 2) {
         // as in production: the z-sums ride in the last smoothing pass, so
         // the zsum slot measures ~0
         const CgFuse fuse{st, w.partials, w.counters, 0};
-        int rc = mg_apply(mg, r, z, s, done, ev + 3, &fuse, pl.red_blocks);
+        int rc = mg_apply(mg, r, z, s, done, ev + 3, &fuse, pl.red_blocks, &pl);
         if (rc) return rc;
       } else {
         for (int j = 3; j < 9; ++j) PF_CUDA(cudaEventRecord(ev[j], s));
       }
       PF_CUDA(cudaEventRecord(ev[9], s));
-      launch(k_cg_pupdate, ge, kBlock, s, a, r, (const double *)z, p, n, st);
+      launch(k_cg_pupdate, ge, kBlock, s, a, r, (const double *)z, p, rg, st);
       PF_CUDA(cudaEventRecord(ev[10], s));
       PF_CUDA(cudaEventSynchronize(ev[10]));
       // spmv, update, [mg: smooth0, restrict, coarse, prolong, smooth2],
@@ -1242,7 +1287,8 @@ extern "C" int pf_cg_profile(const pf_plan *plan, const double *a,
     }
     for (auto &e : ev) cudaEventDestroy(e);
     SolverState hs;
-    int rc = read_state(st, &hs, s);
+    int rc = read_state(pl, st, &hs, s);
+    if (!rc) rc = comm_check(pl, s);
     if (rc) return rc;
     if (hs.all_done) {
       set_error("pf_cg_profile: iteration stopped early (breakdown)");
@@ -1290,22 +1336,26 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
     bv.v[0] = w.vecs + 5 * len;
     bv.v[1] = w.vecs + 6 * len;
     bv.dinv = w.vecs + 7 * len;
-    const int gr = std::min(grid_for(n), pl.red_blocks);
+    const int gr = std::min(grid_for(pl.i1 - pl.i0), pl.red_blocks);
+    const Rng rg = plan_range(pl);
     PF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * len, s));
     // tol 0: the recurrence never converges inside the timed iterations
     launch(k_bi_reset, 1, 1, s, st, ncomp, iters + 1, 1, 0.0, 1, 0x7u);
-    launch(k_bi_bnorm, gr, kBlock, s, b, n, st, w.partials, w.counters);
+    launch(k_bi_bnorm, gr, kBlock, s, b, n, rg, st, w.partials, w.counters);
+    halo(pl, s, {{x, ncomp}});
     if (transpose)
       launch(k_bi_init<V, true>, gr, kBlock, s, v, a, b, (const double *)x,
              bv, st, w.partials, w.counters);
     else
       launch(k_bi_init<V, false>, gr, kBlock, s, v, a, b, (const double *)x,
              bv, st, w.partials, w.counters);
+    halo(pl, s, {{bv.v[0], ncomp}, {bv.dinv, 1}});
     cudaEvent_t ev[4];
     for (auto &e : ev) PF_CUDA(cudaEventCreate(&e));
     double tot[4] = {0, 0, 0, 0};
     for (int k = 0; k < iters; ++k) {
       const int par = k & 1;
+      halo(pl, s, {{bv.r, ncomp}, {bv.p[par], ncomp}});
       PF_CUDA(cudaEventRecord(ev[0], s));
       if (transpose)
         launch(k_bi_pv<V, true>, gr, kBlock, s, v, a, bv, par, st, w.partials,
@@ -1313,6 +1363,7 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
       else
         launch(k_bi_pv<V, false>, gr, kBlock, s, v, a, bv, par, st,
                w.partials, w.counters);
+      halo(pl, s, {{bv.v[par ^ 1], ncomp}});
       PF_CUDA(cudaEventRecord(ev[1], s));
       if (transpose)
         launch(k_bi_st<V, true>, gr, kBlock, s, v, a, bv, par, st, w.partials,
@@ -1321,7 +1372,7 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
         launch(k_bi_st<V, false>, gr, kBlock, s, v, a, bv, par, st,
                w.partials, w.counters);
       PF_CUDA(cudaEventRecord(ev[2], s));
-      launch(k_bi_xr, gr, kBlock, s, a, bv, par, x, n, st, w.partials,
+      launch(k_bi_xr, gr, kBlock, s, a, bv, par, x, n, rg, st, w.partials,
              w.counters);
       PF_CUDA(cudaEventRecord(ev[3], s));
       PF_CUDA(cudaEventSynchronize(ev[3]));
@@ -1336,7 +1387,8 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
     }
     for (auto &e : ev) cudaEventDestroy(e);
     SolverState hs;
-    int rc = read_state(st, &hs, s);
+    int rc = read_state(pl, st, &hs, s);
+    if (!rc) rc = comm_check(pl, s);
     if (rc) return rc;
     if (hs.all_done) {
       set_error("pf_bicgstab_profile: iteration stopped early (breakdown)");

@@ -85,16 +85,28 @@ __device__ double2 *fft_lines(double2 *a, double2 *b, int N, int nl,
   return a;
 }
 
-// first element of the Z line number l (lines enumerated X fastest, then Y)
+// first element of the owned Z line number l (lines enumerated X fastest,
+// then Y; slab plans skip the ghost plane at local X = 0)
 __device__ __forceinline__ int64_t zline_base(const SpecPlan &sp, int64_t l) {
-  const int64_t x = l % sp.sx, y = l / sp.sx;
-  return (x * sp.sy + y) * sp.sz;
+  const int64_t x = l % sp.nxl, y = l / sp.nxl;
+  return ((x + sp.xoff) * sp.sy + y) * sp.sz;
 }
 
-__device__ __forceinline__ int64_t spec_index(const SpecPlan &sp, int64_t l,
-                                              int kz) {
-  const int64_t x = l % sp.sx, y = l / sp.sx;
-  return (y * sp.nkz + kz) * sp.sx + x;
+// rank holding wavenumber kz of the transposed spectrum
+__device__ __forceinline__ int kz_owner(const SpecPlan &sp, int kz) {
+  int q = 0;
+  while (kz >= sp.kz0[q + 1]) ++q;
+  return q;
+}
+
+// address of (line l, wavenumber kz) in the owner's transposed spectrum
+// (Y, kz - kz0[q], global X): a peer address when another rank owns kz
+__device__ __forceinline__ double2 *spec_at(const SpecPlan &sp, int64_t l,
+                                            int kz) {
+  const int64_t x = l % sp.nxl, y = l / sp.nxl;
+  const int q = kz_owner(sp, kz);
+  const int nkq = sp.kz0[q + 1] - sp.kz0[q];
+  return sp.peer_s[q] + (y * nkq + (kz - sp.kz0[q])) * sp.sx + sp.x0 + x;
 }
 
 // pass 1: real FFT along Z, two real lines per complex transform
@@ -103,7 +115,7 @@ __global__ void __launch_bounds__(kFftThreads)
   SPEC_DONE_RETURN;
   extern __shared__ double2 sm[];
   const int N = sp.sz, LP = sp.lpz, nk = sp.nkz;
-  const int64_t npairs = (int64_t)sp.sx * sp.sy / 2;
+  const int64_t npairs = (int64_t)sp.nxl * sp.sy / 2;
   const int64_t ntiles = (npairs + LP - 1) / LP;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t g0 = tile * LP;
@@ -130,7 +142,9 @@ __global__ void __launch_bounds__(kFftThreads)
       const double2 o =
           side == 0 ? make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y))
                     : make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
-      sp.s[spec_index(sp, 2 * g + side, kz)] = o;
+      // slab plans: the transpose to the kz owner happens here, as a
+      // store into the peer's spectrum over NVLink
+      *spec_at(sp, 2 * g + side, kz) = o;
     }
     __syncthreads();
   }
@@ -143,14 +157,15 @@ __global__ void __launch_bounds__(kFftThreads)
   SPEC_DONE_RETURN;
   extern __shared__ double2 sm[];
   const int N = sp.sx, LP = sp.lpx;
-  const int64_t nlines = (int64_t)sp.sy * sp.nkz;
+  const int64_t nlines =
+      (int64_t)sp.sy * (sp.kz0[sp.rank + 1] - sp.kz0[sp.rank]);
   const int64_t ntiles = (nlines + LP - 1) / LP;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t l0 = tile * LP;
     const int64_t nl = nlines - l0 < LP ? nlines - l0 : LP;
     double2 *src = sp.s + l0 * N;
     for (int e = threadIdx.x; e < LP * N; e += blockDim.x)
-      sm[e] = e < nl * N ? src[e] : make_double2(0.0, 0.0);
+      sm[e] = e < nl * N ? __ldcg(src + e) : make_double2(0.0, 0.0);
     __syncthreads();
     const double2 *f = fft_lines<kInv>(sm, sm + LP * N, N, LP, sp.twx);
     for (int e = threadIdx.x; e < nl * N; e += blockDim.x) src[e] = f[e];
@@ -175,15 +190,16 @@ __global__ void __launch_bounds__(kYThreads)
     az[y] = sp.az[y];
   }
   __syncthreads();
-  const int64_t ncol = (int64_t)sp.nkz * sp.sx;
+  const int kzb = sp.kz0[sp.rank];
+  const int64_t ncol = (int64_t)(sp.kz0[sp.rank + 1] - kzb) * sp.sx;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = t < 2 * ncol;
   const int64_t col = t >> 1;
   const int comp = (int)(t & 1);
-  const int kx = (int)(col % sp.sx), kz = (int)(col / sp.sx);
+  const int kx = (int)(col % sp.sx), kz = kzb + (int)(col / sp.sx);
   const double lxv = active ? sp.lx[kx] : 0.0;
   const double lzv = active ? sp.lz[kz] : 0.0;
-  const bool pinned = col == 0;
+  const bool pinned = kz == 0 && kx == 0;
   const double scale = 1.0 / ((double)sp.sx * sp.sz);
   double *sv = reinterpret_cast<double *>(sp.s);
   const int64_t ystride = 2 * ncol;
@@ -194,7 +210,7 @@ __global__ void __launch_bounds__(kYThreads)
       double rr[C];
 #pragma unroll
       for (int k = 0; k < C; ++k)
-        if (y0 + k < sy) rr[k] = sv[(int64_t)(y0 + k) * ystride + t];
+        if (y0 + k < sy) rr[k] = __ldcg(sv + (int64_t)(y0 + k) * ystride + t);
 #pragma unroll
       for (int k = 0; k < C; ++k) {
         const int y = y0 + k;
@@ -248,7 +264,7 @@ __global__ void __launch_bounds__(kFftThreads)
   SPEC_DONE_RETURN;
   extern __shared__ double2 sm[];
   const int N = sp.sz, LP = sp.lpz, half = N >> 1;
-  const int64_t npairs = (int64_t)sp.sx * sp.sy / 2;
+  const int64_t npairs = (int64_t)sp.nxl * sp.sy / 2;
   const int64_t ntiles = (npairs + LP - 1) / LP;
   double sums[3] = {0.0, 0.0, 0.0};
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -259,8 +275,9 @@ __global__ void __launch_bounds__(kFftThreads)
       double2 v = make_double2(0.0, 0.0);
       if (g < npairs) {
         const int kk = k <= half ? k : N - k;
-        const double2 a = sp.s[spec_index(sp, 2 * g, kk)];
-        const double2 b = sp.s[spec_index(sp, 2 * g + 1, kk)];
+        // slab plans: the inverse transpose, loads from the kz owner
+        const double2 a = __ldcg(spec_at(sp, 2 * g, kk));
+        const double2 b = __ldcg(spec_at(sp, 2 * g + 1, kk));
         v = k <= half ? make_double2(a.x - b.y, a.y + b.x)
                       : make_double2(a.x + b.y, b.x - a.y);
       }
@@ -318,9 +335,9 @@ __global__ void __launch_bounds__(kBlock)
   SPEC_DONE_RETURN;
   const int y = blockIdx.x;
   double v[3] = {0.0, 0.0, 0.0};
-  const int64_t m = (int64_t)L.sx * L.sz;
+  const int64_t m = (int64_t)sp.nxl * L.sz;
   for (int64_t e = threadIdx.x; e < m; e += blockDim.x) {
-    const int64_t x = e / L.sz, zz = e - x * L.sz;
+    const int64_t x = e / L.sz + sp.xoff, zz = e - (x - sp.xoff) * L.sz;
     const int64_t i = (x * L.sy + y) * L.sz + zz;
     v[0] += L.wx[i];
     v[1] += L.wy[i];
@@ -328,10 +345,16 @@ __global__ void __launch_bounds__(kBlock)
   }
   block_reduce<3>(v);
   if (threadIdx.x == 0) {
-    sp.ax[y] = v[0] / m;
-    sp.ay[y] = v[1] / m;
-    sp.az[y] = v[2] / m;
+    sp.ax[y] = v[0];
+    sp.ay[y] = v[1];
+    sp.az[y] = v[2];
   }
+}
+
+// plane sums (over all ranks) -> plane means
+__global__ void __launch_bounds__(kBlock) k_spec_plane_mean(SpecPlan sp) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < 3 * sp.sy) sp.ax[t] /= (double)sp.sx * sp.sz;
 }
 
 // ---------------------------------------------------------------------------
@@ -355,28 +378,67 @@ void spec_plan(SpecPlan &sp, int sx, int sy, int sz) {
   sp.nkz = sz / 2 + 1;
   sp.lpx = std::max(1, kFftElems / sx);
   sp.lpz = std::max(1, kFftElems / sz);
+  sp.nxl = sx;
+  sp.xoff = sp.x0 = sp.rank = 0;
+  sp.world = 1;
+  sp.kz0[0] = 0;
+  sp.kz0[1] = sp.nkz;
 }
+
+void spec_slab_plan(SpecPlan &sp, int nxl, int x0, int rank, int world) {
+  sp.nxl = nxl;
+  sp.xoff = 1;
+  sp.x0 = x0;
+  sp.rank = rank;
+  sp.world = world;
+  const int base = sp.nkz / world, rem = sp.nkz % world;
+  sp.kz0[0] = 0;
+  for (int q = 0; q < world; ++q)
+    sp.kz0[q + 1] = sp.kz0[q] + base + (q < rem ? 1 : 0);
+}
+
+static int nkz_max(const SpecPlan &sp) {
+  int m = 0;
+  for (int q = 0; q < sp.world; ++q)
+    m = std::max(m, sp.kz0[q + 1] - sp.kz0[q]);
+  return m;
+}
+
+static bool spec_is_slab(const SpecPlan &sp) { return sp.xoff != 0; }
 
 static int64_t al(int64_t b) { return (b + 255) / 256 * 256; }
 
+int64_t spec_slab_bytes(const SpecPlan &sp) {
+  return al((int64_t)sp.sy * nkz_max(sp) * sp.sx * 16);
+}
+
+void spec_slab_bind(SpecPlan &sp, const CommHost &c) {
+  for (int q = 0; q < sp.world; ++q)
+    sp.peer_s[q] = reinterpret_cast<double2 *>(c.host.peer[q] + c.spec_off);
+  sp.s = sp.peer_s[sp.rank];
+}
+
 int64_t spec_bytes(const SpecPlan &sp) {
-  const int64_t ns = (int64_t)sp.sy * sp.nkz * sp.sx;
-  return al(ns * 16) + al(ns * 8) + 3 * al(sp.sy * 8) + al(sp.sx * 16) +
-         al(sp.sz * 16) + al(sp.sx * 8) + al(sp.nkz * 8);
+  // the work array of a slab plan lives in the comm's symmetric buffer
+  const int64_t ns = (int64_t)sp.sy * nkz_max(sp) * sp.sx;
+  return (spec_is_slab(sp) ? 0 : al(ns * 16)) + al(ns * 8) +
+         al(3 * sp.sy * 8) + al(sp.sx * 16) + al(sp.sz * 16) +
+         al(sp.sx * 8) + al(sp.nkz * 8);
 }
 
 char *spec_bind(SpecPlan &sp, char *q) {
-  const int64_t ns = (int64_t)sp.sy * sp.nkz * sp.sx;
-  sp.s = reinterpret_cast<double2 *>(q);
-  q += al(ns * 16);
+  const int64_t ns = (int64_t)sp.sy * nkz_max(sp) * sp.sx;
+  if (!spec_is_slab(sp)) {
+    sp.s = reinterpret_cast<double2 *>(q);
+    sp.peer_s[0] = sp.s;
+    q += al(ns * 16);
+  }
   sp.cw = reinterpret_cast<double *>(q);
   q += al(ns * 8);
   sp.ax = reinterpret_cast<double *>(q);
-  q += al(sp.sy * 8);
-  sp.ay = reinterpret_cast<double *>(q);
-  q += al(sp.sy * 8);
-  sp.az = reinterpret_cast<double *>(q);
-  q += al(sp.sy * 8);
+  sp.ay = sp.ax + sp.sy;
+  sp.az = sp.ax + 2 * sp.sy;
+  q += al(3 * sp.sy * 8);
   sp.twx = reinterpret_cast<double2 *>(q);
   q += al(sp.sx * 16);
   sp.twz = reinterpret_cast<double2 *>(q);
@@ -389,9 +451,19 @@ char *spec_bind(SpecPlan &sp, char *q) {
 }
 
 int spec_setup(const MgLevel &l0, const SpecPlan &sp, cudaStream_t s,
-               const int *done) {
+               const int *done, const Plan *pl) {
+  if (spec_is_slab(sp) && (!pl || !pl->comm)) {
+    set_error("spectral preconditioner of a slab plan: no communicator "
+              "attached (pf_plan_attach_comm)");
+    return PF_ERR_ARG;
+  }
   launch(k_spec_tables, grid_for(std::max(sp.sx, sp.sz)), kBlock, s, sp);
   launch(k_spec_planes, sp.sy, kBlock, s, l0, sp, done);
+  if (pl) {
+    int rc = comm_vec_allreduce(*pl, sp.ax, 3 * sp.sy, 0, s);
+    if (rc) return rc;
+  }
+  launch(k_spec_plane_mean, grid_for(3 * sp.sy), kBlock, s, sp);
   PF_LAUNCH_CHECK("spec_setup");
   return PF_OK;
 }
@@ -405,22 +477,34 @@ static void launch_smem(void (*kernel)(KArgs...), int grid, int block,
 
 int spec_apply(const MgLevel &l0, const SpecPlan &sp, const double *r,
                double *z, cudaStream_t s, const int *done, cudaEvent_t *ev,
-               const CgFuse *fuse, int red_blocks) {
+               const CgFuse *fuse, int red_blocks, const Plan *pl) {
   (void)l0;
+  if (spec_is_slab(sp) && (!pl || !pl->comm)) {
+    set_error("spectral preconditioner of a slab plan: no communicator");
+    return PF_ERR_ARG;
+  }
+  // slab plans: the forward Z pass stores into the kz owners' spectra and
+  // the inverse Z pass loads from them; barriers separate the all-to-all
+  // from the owner-local X / Y passes (no-ops on a single GPU)
+  auto barrier = [&]() {
+    if (pl) comm_barrier(*pl, s);
+  };
   auto mark = [&](int k) {
     if (ev) cudaEventRecord(ev[k], s);
   };
-  const int64_t npairs = (int64_t)sp.sx * sp.sy / 2;
+  const int64_t npairs = (int64_t)sp.nxl * sp.sy / 2;
   const int zt = (int)std::min<int64_t>((npairs + sp.lpz - 1) / sp.lpz,
                                         1 << 20);
   const size_t zsm = 2 * sizeof(double2) * sp.lpz * sp.sz;
-  const int64_t xlines = (int64_t)sp.sy * sp.nkz;
+  const int nkl = sp.kz0[sp.rank + 1] - sp.kz0[sp.rank];
+  const int64_t xlines = (int64_t)sp.sy * nkl;
   const int xt = (int)std::min<int64_t>((xlines + sp.lpx - 1) / sp.lpx,
                                         1 << 20);
   const size_t xsm = 2 * sizeof(double2) * sp.lpx * sp.sx;
-  const int64_t ncol2 = 2 * (int64_t)sp.nkz * sp.sx;
+  const int64_t ncol2 = 2 * (int64_t)nkl * sp.sx;
   mark(0);
   launch_smem(k_spec_fwd_z, zt, kFftThreads, zsm, s, sp, r, done);
+  barrier();
   mark(1);
   if (sp.sx > 1) launch_smem(k_spec_x<false>, xt, kFftThreads, xsm, s, sp, done);
   mark(2);
@@ -428,13 +512,18 @@ int spec_apply(const MgLevel &l0, const SpecPlan &sp, const double *r,
               3 * sizeof(double) * sp.sy, s, sp, done);
   mark(3);
   if (sp.sx > 1) launch_smem(k_spec_x<true>, xt, kFftThreads, xsm, s, sp, done);
+  barrier();
   mark(4);
-  if (fuse && fuse->st)
+  if (fuse && fuse->st) {
+    // the fused z-sums end in a cross-rank allreduce, which no rank leaves
+    // before every rank's loads are done: it doubles as the closing barrier
     launch_smem(k_spec_inv_z<true>, std::min(zt, red_blocks), kFftThreads,
                 zsm, s, sp, r, z, *fuse, done);
-  else
+  } else {
     launch_smem(k_spec_inv_z<false>, zt, kFftThreads, zsm, s, sp, r, z,
                 CgFuse{nullptr, nullptr, nullptr, 0}, done);
+    barrier();
+  }
   mark(5);
   PF_LAUNCH_CHECK("spec_apply");
   return PF_OK;

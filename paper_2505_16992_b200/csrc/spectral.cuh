@@ -22,6 +22,7 @@
 #pragma once
 
 #include "cgstate.cuh"
+#include "comm.h"
 #include "common.cuh"
 
 namespace pf {
@@ -32,15 +33,21 @@ bool spec_ok(int dim, int sx, int sy, int sz, int px, int pz);
 // bytes of the spectral arrays (beyond level 0's face weights)
 int64_t spec_bytes(const SpecPlan &sp);
 void spec_plan(SpecPlan &sp, int sx, int sy, int sz);
+// slab decomposition of the X axis over `world` ranks (see SpecPlan)
+void spec_slab_plan(SpecPlan &sp, int nxl, int x0, int rank, int world);
+// bytes of this rank's transposed spectrum (lives in the comm's symmetric
+// buffer so peers can store / load it), and its binding after attach
+int64_t spec_slab_bytes(const SpecPlan &sp);
+void spec_slab_bind(SpecPlan &sp, const CommHost &c);
 // carve the arrays from `base`; returns the first byte past them
 char *spec_bind(SpecPlan &sp, char *base);
 // plane means of the level-0 face weights, twiddles, eigenvalues
 int spec_setup(const MgLevel &l0, const SpecPlan &sp, cudaStream_t s,
-               const int *done);
+               const int *done, const Plan *pl);
 // z = M^-1 r; `ev` (6 events) brackets the five passes; `fuse` folds the CG
 // z-sums into the last pass
 int spec_apply(const MgLevel &l0, const SpecPlan &sp, const double *r,
                double *z, cudaStream_t s, const int *done, cudaEvent_t *ev,
-               const CgFuse *fuse, int red_blocks);
+               const CgFuse *fuse, int red_blocks, const Plan *pl);
 
 }  // namespace pf

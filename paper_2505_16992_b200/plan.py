@@ -177,6 +177,14 @@ class DevicePlan:
             _lib.PF_GEOM_SPECTRAL
             if geom_precond != "multigrid" and _spectral_allowed(domain, box, sep)
             else _lib.PF_GEOM_MULTIGRID)
+        info = getattr(domain, "slab_info", None)
+        if info is not None:
+            # slab of a larger box (slab.SlabDomain): owned planes between
+            # two ghost planes along axis 0
+            desc.slab_world, desc.slab_rank = int(info[0]), int(info[1])
+            desc.slab_nx, desc.slab_x0 = int(info[2]), int(info[3])
+        self.slab = info is not None
+        self.comm = None
         self._desc = desc
         handle = ctypes.c_void_p()
         with torch.cuda.device(device):
@@ -255,6 +263,13 @@ class DevicePlan:
     @property
     def stream(self):
         return _lib.stream_of(self.device)
+
+    def attach_comm(self, comm):
+        """Link this slab plan to the other ranks (slab.SlabComm): from now
+        on every entry point on the plan is collective."""
+        _lib.call("pf_plan_attach_comm", self.handle, comm.handle,
+                  _lib.ptr(self.workspace), self.stream)
+        self.comm = comm
 
     def __del__(self):
         h = getattr(self, "handle", None)
