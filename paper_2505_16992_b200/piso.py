@@ -28,10 +28,11 @@ face-f neighbour coupling) instead of CSR ``data`` arrays; the tape holds
 K = -P (the operator the pressure CG runs on) and exposes ``p_data = -K``.
 
 Non-orthogonal grids (alpha with off-diagonal entries, e.g. the distorted
-Poiseuille duct) need the lagged cross fluxes of S/piso.py:322-353,431-449;
-they are not implemented on the device yet, and ``piso_step`` raises
-``NotImplementedError`` for such domains instead of computing a different
-discretisation.  None of the BASELINE grids is non-orthogonal (SURVEY §8 a).
+Poiseuille duct) run the lagged cross fluxes of S/piso.py:322-353,431-449
+and the ``nonortho_correctors`` loops on the device (csrc/cross.cu).
+
+Slab domains (slab.SlabDomain, one per GPU) run this same code: the library
+exchanges ghost planes and reduces across the ranks inside its entry points.
 """
 
 from dataclasses import dataclass, field

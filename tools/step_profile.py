@@ -25,7 +25,7 @@ def main():
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     bargs = argparse.Namespace(config=args.config)
-    dom, state, nu, dt, forcing, w = bench.build_workload(bargs, dev)
+    dom, state, nu, dt, forcing, w, _ = bench.build_workload(bargs, dev)
     cot = adjoint.GradState(u=w, p=torch.zeros(dom.n, dtype=torch.float64,
                                                device=dev))
     ws = piso.PisoWorkspace(dom)
