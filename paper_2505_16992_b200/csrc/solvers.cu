@@ -640,13 +640,15 @@ __global__ void __launch_bounds__(kBlock)
 }
 
 // pass xr: pending comps: x += alpha phat.  active comps:
-// x += alpha phat + omega shat; r = s - omega t; |r|, r^.r -> next beta
+// x += alpha phat + omega shat; r = s - omega t; |r|, r^.r -> next beta.
+// Two cells per thread with 128-bit loads and stores (the owned range is
+// split into an even-aligned vector part and scalar edges).
 __global__ void __launch_bounds__(kBlock)
     k_bi_xr(const double *__restrict__ a, BiVecs w, int par,
             double *__restrict__ x, int32_t n, Rng rg, SolverState *st,
             double *partials, unsigned *counter) {
   if (st->all_done) return;
-  const int nc = st->ncomp, pc = st->precond;
+  const int nc = st->ncomp;
   int act[3], pend[3];
   double alpha[3], omega[3];
   _Pragma("unroll") for (int q = 0; q < 3; ++q) {
@@ -658,7 +660,7 @@ __global__ void __launch_bounds__(kBlock)
   const double *__restrict__ p1 = w.p[par ^ 1];
   const double *__restrict__ v1 = w.v[par ^ 1];
   double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  RANGE_LOOP(i, rg) {
+  auto cell = [&](int32_t i) {
     const double di = w.dinv[i];
     _Pragma("unroll") for (int q = 0; q < 3; ++q) {
       if (q >= nc) break;
@@ -674,12 +676,50 @@ __global__ void __launch_bounds__(kBlock)
       acc[2 * q] += ri * ri;
       acc[2 * q + 1] += w.rhat[o] * ri;
     }
+  };
+  // n even: component bases stay 16-byte aligned
+  const int32_t v0 = (n & 1) ? rg.i1 : ((rg.i0 + 1) & ~1);
+  const int32_t v1e = (n & 1) ? rg.i1 : (rg.i1 & ~1);
+  const int32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int32_t nth = gridDim.x * blockDim.x;
+  for (int32_t k = v0 + 2 * tid; k + 1 < v1e; k += 2 * nth) {
+    const double2 di = *reinterpret_cast<const double2 *>(w.dinv + k);
+    _Pragma("unroll") for (int q = 0; q < 3; ++q) {
+      if (q >= nc) break;
+      const int64_t o = (int64_t)q * n + k;
+      const double2 pp = *reinterpret_cast<const double2 *>(p1 + o);
+      double2 xx = *reinterpret_cast<const double2 *>(x + o);
+      if (pend[q]) {
+        xx.x += alpha[q] * (pp.x * di.x);
+        xx.y += alpha[q] * (pp.y * di.y);
+      }
+      if (act[q]) {
+        const double2 rr = *reinterpret_cast<const double2 *>(w.r + o);
+        const double2 vv = *reinterpret_cast<const double2 *>(v1 + o);
+        const double2 tt = *reinterpret_cast<const double2 *>(w.t + o);
+        const double2 rh = *reinterpret_cast<const double2 *>(w.rhat + o);
+        const double s0 = rr.x - alpha[q] * vv.x, s1 = rr.y - alpha[q] * vv.y;
+        xx.x = xx.x + alpha[q] * (pp.x * di.x) + omega[q] * (s0 * di.x);
+        xx.y = xx.y + alpha[q] * (pp.y * di.y) + omega[q] * (s1 * di.y);
+        const double r0 = s0 - omega[q] * tt.x, r1 = s1 - omega[q] * tt.y;
+        *reinterpret_cast<double2 *>(w.r + o) = make_double2(r0, r1);
+        acc[2 * q] += r0 * r0;
+        acc[2 * q] += r1 * r1;
+        acc[2 * q + 1] += rh.x * r0;
+        acc[2 * q + 1] += rh.y * r1;
+      }
+      if (pend[q] || act[q]) *reinterpret_cast<double2 *>(x + o) = xx;
+    }
+  }
+  // scalar edges of the owned range
+  if (tid == 0) {
+    for (int32_t i = rg.i0; i < v0; ++i) cell(i);
+    for (int32_t i = v1e; i < rg.i1; ++i) cell(i);
   }
   double tot[6];
   if (grid_reduce<6>(acc, partials, counter, tot)) {
     int all = 1;
-    _Pragma("unroll") for (int q = 0; q < 3; ++q) {
-      if (q >= nc) break;
+    for (int q = 0; q < nc; ++q) {
       CompState &c = st->c[q];
       c.pending = 0;
       if (act[q]) {
@@ -704,6 +744,301 @@ __global__ void __launch_bounds__(kBlock)
       if (!c.done) all = 0;
     }
     st->all_done = all;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tiled stencil passes for 3D boxes (2.5D blocking).
+//
+// A CTA owns a TY x TZ column tile of the (Y, Z) plane and marches along X
+// through a chunk of planes.  The preconditioned input g = M^-1 (r + beta
+// (p - omega v)) (pass pv) or M^-1 (r - alpha v') (pass st) of every cell is
+// formed ONCE: the centre column in registers for planes x-1, x, x+1, the
+// current plane with its one-cell Y / Z halo in shared memory.  Every input
+// array is then read from HBM once per cell (plus the thin halo and the two
+// prologue planes of a chunk, from L2), instead of once per stencil point.
+
+constexpr int kTZ = 32, kTY = 8, kTileThreads = kTZ * kTY;
+constexpr int kXChunk = 32;
+
+struct TileGeo {
+  int32_t X, Y, Z;          // local box
+  int32_t px, py, pz;       // periodic flags
+  int32_t x0, x1;           // owned planes [x0, x1)
+  int32_t ty_tiles, tz_tiles, chunks, ntiles;
+};
+
+__device__ __forceinline__ int32_t wrap(int32_t c, int32_t L, int32_t per,
+                                        bool &ok) {
+  if (c >= 0 && c < L) {
+    ok = true;
+    return c;
+  }
+  ok = per != 0;
+  return c < 0 ? c + L : c - L;
+}
+
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// Shared memory of the tiled passes: the raw inputs of two planes (tile +
+// halo, filled by cp.async one plane ahead) and the preconditioned values
+// g of two planes (double buffered, so a plane step needs one barrier).
+constexpr int kRawArrays = 10;  // r x3, p x3, v x3, 1/A (pass st: r, v, 1/A)
+constexpr int kTP = (kTY + 2) * (kTZ + 2);
+struct TileSmem {
+  double raw[2][kRawArrays][kTY + 2][kTZ + 2];
+  double g[2][3][kTY + 2][kTZ + 2];
+};
+constexpr size_t kTileSmem = sizeof(TileSmem);
+
+// MODE 0 (pass pv): g = (r + beta (p0 - omega v0)) / A, outputs p' (the
+//                   undivided value), v' = A g, sums r^.v'
+// MODE 1 (pass st): g = (r - alpha v') / A, outputs t = A g, sums s.s, t.t,
+//                   t.s
+template <bool kTrans, int MODE, int kMinB = 1>
+__global__ void __launch_bounds__(kTileThreads, kMinB)
+    k_bi_tiled(TileGeo tg, const double *__restrict__ a, BiVecs w, int par,
+               int64_t n, SolverState *st, double *partials,
+               unsigned *counter) {
+  if (st->all_done) return;
+  constexpr int K = MODE == 0 ? 3 : 9;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem &sm = *reinterpret_cast<TileSmem *>(smem_raw);
+  const int nc = st->ncomp;
+  int act[3];
+  double c0[3], c1[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    act[q] = q < nc && !st->c[q].done;
+    if (MODE == 0) {
+      c0[q] = q < nc ? st->c[q].beta : 0.0;
+      c1[q] = q < nc ? st->c[q].omega : 0.0;
+    } else {
+      c0[q] = q < nc ? st->c[q].alpha : 0.0;
+      c1[q] = 0.0;
+    }
+  }
+  const double *__restrict__ r = w.r;
+  const double *__restrict__ dinv = w.dinv;
+  const double *__restrict__ pin = MODE == 0 ? w.p[par] : nullptr;
+  const double *__restrict__ vin = MODE == 0 ? w.v[par] : w.v[par ^ 1];
+  double *__restrict__ pout = w.p[par ^ 1];
+  double *__restrict__ vout = MODE == 0 ? w.v[par ^ 1] : w.t;
+  const int64_t sX = (int64_t)tg.Y * tg.Z, sY = tg.Z;
+  const int tz = threadIdx.x % kTZ, ty = threadIdx.x / kTZ;
+
+  // async copy of the raw inputs of cell (x, y, z) into slot (sy, sz) of
+  // raw buffer b; zeros outside a walled box
+  auto issue = [&](int b, int32_t x, int32_t y, int32_t z, int sy, int sz) {
+    bool okx, oky, okz;
+    x = wrap(x, tg.X, tg.px, okx);
+    y = wrap(y, tg.Y, tg.py, oky);
+    z = wrap(z, tg.Z, tg.pz, okz);
+    const bool ok = okx && oky && okz;
+    const int64_t j = (int64_t)x * sX + (int64_t)y * sY + z;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      if (q >= nc || !act[q]) continue;
+      const int64_t o = q * n + j;
+      if (ok) {
+        cp_async8(&sm.raw[b][q][sy][sz], r + o);
+        cp_async8(&sm.raw[b][3 + q][sy][sz], vin + o);
+        if (MODE == 0) cp_async8(&sm.raw[b][6 + q][sy][sz], pin + o);
+      } else {
+        sm.raw[b][q][sy][sz] = 0.0;
+        sm.raw[b][3 + q][sy][sz] = 0.0;
+        if (MODE == 0) sm.raw[b][6 + q][sy][sz] = 0.0;
+      }
+    }
+    if (ok)
+      cp_async8(&sm.raw[b][9][sy][sz], dinv + j);
+    else
+      sm.raw[b][9][sy][sz] = 0.0;
+  };
+  // g (and the undivided value) of slot (sy, sz) of raw buffer b
+  auto G = [&](int b, int sy, int sz, double (&g)[3], double (&pv)[3]) {
+    const double dj = sm.raw[b][9][sy][sz];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      g[q] = pv[q] = 0.0;
+      if (q >= nc || !act[q]) continue;
+      const double rr = sm.raw[b][q][sy][sz], vv = sm.raw[b][3 + q][sy][sz];
+      const double val = MODE == 0
+                             ? rr + c0[q] * (sm.raw[b][6 + q][sy][sz] -
+                                             c1[q] * vv)
+                             : rr - c0[q] * vv;
+      pv[q] = val;
+      g[q] = val * dj;
+    }
+  };
+
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = 0.0;
+
+  for (int tile = blockIdx.x; tile < tg.ntiles; tile += gridDim.x) {
+    const int tzt = tile % tg.tz_tiles;
+    const int rest = tile / tg.tz_tiles;
+    const int tyt = rest % tg.ty_tiles;
+    const int ch = rest / tg.ty_tiles;
+    const int32_t y = tyt * kTY + ty, z = tzt * kTZ + tz;
+    const int32_t xs = tg.x0 + ch * kXChunk;
+    const int32_t xe = min(xs + kXChunk, tg.x1);
+    // the halo slot this thread fills (64 along Y, 16 along Z)
+    bool halo_cell = true;
+    int hy = 0, hz = 0, sy_ = 0, sz_ = 0;
+    if (threadIdx.x < 2 * kTZ) {
+      const int side = threadIdx.x / kTZ;
+      hy = tyt * kTY + (side ? kTY : -1);
+      hz = z;
+      sy_ = side ? kTY + 1 : 0;
+      sz_ = tz + 1;
+    } else if (threadIdx.x < 2 * kTZ + 2 * kTY) {
+      const int k = threadIdx.x - 2 * kTZ;
+      const int side = k / kTY;
+      hy = tyt * kTY + (k % kTY);
+      hz = tzt * kTZ + (side ? kTZ : -1);
+      sy_ = (k % kTY) + 1;
+      sz_ = side ? kTZ + 1 : 0;
+    } else {
+      halo_cell = false;
+    }
+    auto issue_plane = [&](int32_t x) {
+      const int b = x & 1;
+      issue(b, x, y, z, ty + 1, tz + 1);
+      if (halo_cell) issue(b, x, hy, hz, sy_, sz_);
+      cp_async_commit();
+    };
+    // g of plane x (tile + halo) from its raw buffer into g buffer x & 1
+    auto convert = [&](int32_t x, double (&gcen)[3], double (&pcen)[3]) {
+      const int b = x & 1;
+      G(b, ty + 1, tz + 1, gcen, pcen);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) sm.g[b][q][ty + 1][tz + 1] = gcen[q];
+      if (halo_cell) {
+        double hg[3], tmp[3];
+        G(b, sy_, sz_, hg, tmp);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) sm.g[b][q][sy_][sz_] = hg[q];
+      }
+    };
+
+    double gm[3], gc[3], gn[3], pc[3], pn[3], tmp[3];
+    __syncthreads();  // the previous tile is done with both buffers
+    issue_plane(xs - 1);
+    issue_plane(xs);
+    cp_async_wait_all();
+    __syncthreads();
+    G((xs - 1) & 1, ty + 1, tz + 1, gm, tmp);
+    convert(xs, gc, pc);
+    __syncthreads();  // raw buffer (xs - 1) & 1 is free again
+    issue_plane(xs + 1);
+    for (int32_t x = xs; x < xe; ++x) {
+      const int64_t i = (int64_t)x * sX + (int64_t)y * sY + z;
+      // this plane's coefficients (and r^): plain loads, consumed after the
+      // barrier and the conversion of plane x + 1
+      double cf[6];
+      if (kTrans) {
+        // the neighbour's coefficient across its back face
+        bool ok;
+        const int32_t xm = wrap(x - 1, tg.X, tg.px, ok);
+        cf[0] = ok ? a[(int64_t)2 * n + xm * sX + (int64_t)y * sY + z] : 0.0;
+        const int32_t xp = wrap(x + 1, tg.X, tg.px, ok);
+        cf[1] = ok ? a[(int64_t)1 * n + xp * sX + (int64_t)y * sY + z] : 0.0;
+        const int32_t ym = wrap(y - 1, tg.Y, tg.py, ok);
+        cf[2] = ok ? a[(int64_t)4 * n + x * sX + (int64_t)ym * sY + z] : 0.0;
+        const int32_t yp = wrap(y + 1, tg.Y, tg.py, ok);
+        cf[3] = ok ? a[(int64_t)3 * n + x * sX + (int64_t)yp * sY + z] : 0.0;
+        const int32_t zm = wrap(z - 1, tg.Z, tg.pz, ok);
+        cf[4] = ok ? a[(int64_t)6 * n + x * sX + (int64_t)y * sY + zm] : 0.0;
+        const int32_t zp = wrap(z + 1, tg.Z, tg.pz, ok);
+        cf[5] = ok ? a[(int64_t)5 * n + x * sX + (int64_t)y * sY + zp] : 0.0;
+      } else {
+#pragma unroll
+        for (int f = 0; f < 6; ++f) cf[f] = a[(int64_t)(1 + f) * n + i];
+      }
+      const double aii = a[i];
+      double rh[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        rh[q] = (MODE == 0 && q < nc && act[q]) ? w.rhat[q * n + i] : 0.0;
+      cp_async_wait_all();  // my copies of plane x + 1 have landed
+      __syncthreads();      // everyone's have; g of plane x is complete
+      convert(x + 1, gn, pn);
+      if (x + 2 <= xe) issue_plane(x + 2);
+      const int gb = x & 1;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        if (q >= nc || !act[q]) continue;
+        const double yv = aii * gc[q] + cf[0] * gm[q] + cf[1] * gn[q] +
+                          cf[2] * sm.g[gb][q][ty][tz + 1] +
+                          cf[3] * sm.g[gb][q][ty + 2][tz + 1] +
+                          cf[4] * sm.g[gb][q][ty + 1][tz] +
+                          cf[5] * sm.g[gb][q][ty + 1][tz + 2];
+        const int64_t o = q * n + i;
+        vout[o] = yv;
+        if (MODE == 0) {
+          pout[o] = pc[q];
+          acc[q] += rh[q] * yv;
+        } else {
+          acc[3 * q] += pc[q] * pc[q];
+          acc[3 * q + 1] += yv * yv;
+          acc[3 * q + 2] += yv * pc[q];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        gm[q] = gc[q];
+        gc[q] = gn[q];
+        pc[q] = pn[q];
+      }
+    }
+    cp_async_wait_all();
+  }
+  double tot[K];
+  if (!grid_reduce<K>(acc, partials, counter, tot)) return;
+  if (MODE == 0) {
+    int all = 1;
+    for (int q = 0; q < nc; ++q) {
+      CompState &c = st->c[q];
+      if (act[q]) {
+        if (fabs(tot[q]) < DBL_MIN) {
+          c.fail = 1;
+          c.done = 1;
+        } else {
+          c.alpha = c.rho_new / tot[q];
+        }
+      }
+      if (!c.done) all = 0;
+    }
+    st->all_done = all;
+  } else {
+    for (int q = 0; q < nc; ++q) {
+      CompState &c = st->c[q];
+      if (!act[q]) continue;
+      c.res = sqrt(tot[3 * q]);
+      if (c.res <= c.tol_abs) {
+        c.converged = 1;
+        c.done = 1;
+        c.pending = 1;
+      } else if (tot[3 * q + 1] < DBL_MIN) {
+        c.fail = 1;
+        c.done = 1;
+      } else {
+        c.omega = tot[3 * q + 2] / tot[3 * q + 1];
+      }
+    }
   }
 }
 
@@ -1032,6 +1367,59 @@ extern "C" int pf_cg_solve(const pf_plan *plan, const double *a,
 
 namespace {
 
+template <bool kTrans, int MODE>
+void launch_tiled(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
+                  const BiVecs &bv, int par, int64_t n, SolverState *st,
+                  Workspace &w) {
+  // 2 CTAs per SM (<= 128 registers, 2 x 71 KB of shared memory) measured
+  // best on C4: pass pv 5.3 TB/s, pass st 4.3 TB/s (1 CTA: 3.8 / 2.9; 3 CTAs
+  // with the 80-register cap: 3.5 / 3.2).  PF_TILE_MINB overrides.
+  static const int minb = [] {
+    const char *e = getenv("PF_TILE_MINB");
+    return e ? atoi(e) : 2;
+  }();
+  auto go = [&](auto kernel) {
+    static bool attr = false;  // per instantiation
+    if (!attr) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kTileSmem);
+      attr = true;
+    }
+    ++g_launches;
+    kernel<<<grid, kTileThreads, kTileSmem, s>>>(tg, a, bv, par, n, st,
+                                                 w.partials, w.counters);
+  };
+  if (minb >= 3)
+    go(k_bi_tiled<kTrans, MODE, 3>);
+  else if (minb == 2)
+    go(k_bi_tiled<kTrans, MODE, 2>);
+  else
+    go(k_bi_tiled<kTrans, MODE, 1>);
+}
+
+// tiled stencil passes apply to 3D boxes whose Y / Z extents are whole tiles
+template <class V>
+bool tile_geo(const Plan &pl, const V &v, TileGeo &tg) {
+  (void)v;
+  if (V::kDim != 3 || pl.d.topo != PF_TOPO_BOX) return false;
+  if (getenv("PF_NO_TILED")) return false;
+  tg.X = (int32_t)pl.d.box_shape[0];
+  tg.Y = (int32_t)pl.d.box_shape[1];
+  tg.Z = (int32_t)pl.d.box_shape[2];
+  if (tg.Y % kTY || tg.Z % kTZ) return false;
+  tg.px = pl.d.box_periodic[0];
+  tg.py = pl.d.box_periodic[1];
+  tg.pz = pl.d.box_periodic[2];
+  const int64_t plane = (int64_t)tg.Y * tg.Z;
+  tg.x0 = (int32_t)(pl.i0 / plane);
+  tg.x1 = (int32_t)(pl.i1 / plane);
+  tg.ty_tiles = tg.Y / kTY;
+  tg.tz_tiles = tg.Z / kTZ;
+  tg.chunks = (tg.x1 - tg.x0 + kXChunk - 1) / kXChunk;
+  tg.ntiles = tg.ty_tiles * tg.tz_tiles * tg.chunks;
+  return true;
+}
+
 template <class V, bool kTrans>
 int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
             SolverState &hs, const double *a, const double *b, double *x,
@@ -1051,6 +1439,9 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   bv.dinv = base + 7 * len;
   const int ge = grid_for(pl.i1 - pl.i0), gr = std::min(ge, pl.red_blocks);
   const Rng rg = plan_range(pl);
+  TileGeo tg;
+  const bool tiled = tile_geo(pl, v, tg);
+  const int tgrid = tiled ? std::min(tg.ntiles, pl.red_blocks) : 0;
   launch(k_bi_reset, 1, 1, s, st, ncomp, maxiter, precond, tol, fresh, mask);
   if (fresh) launch(k_bi_bnorm, gr, kBlock, s, b, n, rg, st, w.partials, w.counters);
   halo(pl, s, {{x, ncomp}});
@@ -1071,11 +1462,17 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     for (int k = 0; k < bsz; ++k) {
       const int par = (launched + k) & 1;
       halo(pl, s, {{bv.r, ncomp}, {bv.p[par], ncomp}});
-      launch(k_bi_pv<V, kTrans>, gr, kBlock, s, v, a, bv, par, st,
-             w.partials, w.counters);
+      if (tiled)
+        launch_tiled<kTrans, 0>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
+      else
+        launch(k_bi_pv<V, kTrans>, gr, kBlock, s, v, a, bv, par, st,
+               w.partials, w.counters);
       halo(pl, s, {{bv.v[par ^ 1], ncomp}});
-      launch(k_bi_st<V, kTrans>, gr, kBlock, s, v, a, bv, par, st,
-             w.partials, w.counters);
+      if (tiled)
+        launch_tiled<kTrans, 1>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
+      else
+        launch(k_bi_st<V, kTrans>, gr, kBlock, s, v, a, bv, par, st,
+               w.partials, w.counters);
       launch(k_bi_xr, gr, kBlock, s, a, bv, par, x, n, rg, st, w.partials,
              w.counters);
     }
@@ -1338,6 +1735,9 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
     bv.dinv = w.vecs + 7 * len;
     const int gr = std::min(grid_for(pl.i1 - pl.i0), pl.red_blocks);
     const Rng rg = plan_range(pl);
+    TileGeo tg;
+    const bool tiled = tile_geo(pl, v, tg);
+    const int tgrid = tiled ? std::min(tg.ntiles, pl.red_blocks) : 0;
     PF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * len, s));
     // tol 0: the recurrence never converges inside the timed iterations
     launch(k_bi_reset, 1, 1, s, st, ncomp, iters + 1, 1, 0.0, 1, 0x7u);
@@ -1357,7 +1757,11 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
       const int par = k & 1;
       halo(pl, s, {{bv.r, ncomp}, {bv.p[par], ncomp}});
       PF_CUDA(cudaEventRecord(ev[0], s));
-      if (transpose)
+      if (tiled && transpose)
+        launch_tiled<true, 0>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
+      else if (tiled)
+        launch_tiled<false, 0>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
+      else if (transpose)
         launch(k_bi_pv<V, true>, gr, kBlock, s, v, a, bv, par, st, w.partials,
                w.counters);
       else
@@ -1365,7 +1769,11 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
                w.partials, w.counters);
       halo(pl, s, {{bv.v[par ^ 1], ncomp}});
       PF_CUDA(cudaEventRecord(ev[1], s));
-      if (transpose)
+      if (tiled && transpose)
+        launch_tiled<true, 1>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
+      else if (tiled)
+        launch_tiled<false, 1>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
+      else if (transpose)
         launch(k_bi_st<V, true>, gr, kBlock, s, v, a, bv, par, st, w.partials,
                w.counters);
       else
