@@ -806,21 +806,27 @@ constexpr size_t kTileSmem = sizeof(TileSmem);
 //                   undivided value), v' = A g, sums r^.v'
 // MODE 1 (pass st): g = (r - alpha v') / A, outputs t = A g, sums s.s, t.t,
 //                   t.s
+// MODE 2 (init):    g = x, outputs r = r^ = b - A x, p = v = 0, 1 / A; |r|
+// MODE 3 (verify):  g = x, sums |b - A x|^2 of every component (runs after
+//                   convergence too)
 template <bool kTrans, int MODE, int kMinB = 1>
 __global__ void __launch_bounds__(kTileThreads, kMinB)
     k_bi_tiled(TileGeo tg, const double *__restrict__ a, BiVecs w, int par,
                int64_t n, SolverState *st, double *partials,
-               unsigned *counter) {
-  if (st->all_done) return;
-  constexpr int K = MODE == 0 ? 3 : 9;
+               unsigned *counter, const double *__restrict__ xin = nullptr,
+               const double *__restrict__ bin = nullptr, int nverify = 0) {
+  if (MODE != 3 && st->all_done) return;
+  constexpr int K = MODE == 1 ? 9 : 3;
+  constexpr bool kX = MODE >= 2;  // the input is the iterate x itself
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem &sm = *reinterpret_cast<TileSmem *>(smem_raw);
-  const int nc = st->ncomp;
+  const int nc = MODE == 3 ? nverify : st->ncomp;
+  const int pc_on = st->precond;
   int act[3];
   double c0[3], c1[3];
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
-    act[q] = q < nc && !st->c[q].done;
+    act[q] = q < nc && (MODE == 3 || !st->c[q].done);
     if (MODE == 0) {
       c0[q] = q < nc ? st->c[q].beta : 0.0;
       c1[q] = q < nc ? st->c[q].omega : 0.0;
@@ -851,6 +857,13 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
     for (int q = 0; q < 3; ++q) {
       if (q >= nc || !act[q]) continue;
       const int64_t o = q * n + j;
+      if (kX) {
+        if (ok)
+          cp_async8(&sm.raw[b][q][sy][sz], xin + o);
+        else
+          sm.raw[b][q][sy][sz] = 0.0;
+        continue;
+      }
       if (ok) {
         cp_async8(&sm.raw[b][q][sy][sz], r + o);
         cp_async8(&sm.raw[b][3 + q][sy][sz], vin + o);
@@ -861,6 +874,7 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
         if (MODE == 0) sm.raw[b][6 + q][sy][sz] = 0.0;
       }
     }
+    if (kX) return;
     if (ok)
       cp_async8(&sm.raw[b][9][sy][sz], dinv + j);
     else
@@ -868,6 +882,13 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
   };
   // g (and the undivided value) of slot (sy, sz) of raw buffer b
   auto G = [&](int b, int sy, int sz, double (&g)[3], double (&pv)[3]) {
+    if (kX) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        g[q] = pv[q] = (q < nc && act[q]) ? sm.raw[b][q][sy][sz] : 0.0;
+      }
+      return;
+    }
     const double dj = sm.raw[b][9][sy][sz];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
@@ -972,7 +993,9 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
       double rh[3];
 #pragma unroll
       for (int q = 0; q < 3; ++q)
-        rh[q] = (MODE == 0 && q < nc && act[q]) ? w.rhat[q * n + i] : 0.0;
+        rh[q] = (MODE == 0 && q < nc && act[q]) ? w.rhat[q * n + i]
+                : (kX && q < nc && act[q]) ? bin[q * n + i]
+                                           : 0.0;
       cp_async_wait_all();  // my copies of plane x + 1 have landed
       __syncthreads();      // everyone's have; g of plane x is complete
       convert(x + 1, gn, pn);
@@ -987,16 +1010,27 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
                           cf[4] * sm.g[gb][q][ty + 1][tz] +
                           cf[5] * sm.g[gb][q][ty + 1][tz + 2];
         const int64_t o = q * n + i;
-        vout[o] = yv;
         if (MODE == 0) {
+          vout[o] = yv;
           pout[o] = pc[q];
           acc[q] += rh[q] * yv;
-        } else {
+        } else if (MODE == 1) {
+          vout[o] = yv;
           acc[3 * q] += pc[q] * pc[q];
           acc[3 * q + 1] += yv * yv;
           acc[3 * q + 2] += yv * pc[q];
+        } else {
+          const double rr = rh[q] - yv;  // b - A x
+          if (MODE == 2) {
+            w.r[o] = rr;
+            w.rhat[o] = rr;
+            w.p[0][o] = 0.0;
+            w.v[0][o] = 0.0;
+          }
+          acc[q] += rr * rr;
         }
       }
+      if (MODE == 2) w.dinv[i] = pc_on ? 1.0 / aii : 1.0;
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         gm[q] = gc[q];
@@ -1008,6 +1042,36 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
   }
   double tot[K];
   if (!grid_reduce<K>(acc, partials, counter, tot)) return;
+  if (MODE == 3) {
+    for (int q = 0; q < nc; ++q) st->c[q].true_res = sqrt(tot[q]);
+    return;
+  }
+  if (MODE == 2) {
+    int all = 1;
+    for (int q = 0; q < nc; ++q) {
+      CompState &c = st->c[q];
+      if (act[q]) {
+        c.res = sqrt(tot[q]);
+        if (c.res <= c.tol_abs) {
+          c.converged = 1;
+          c.done = 1;
+        } else {
+          c.rho = c.alpha = c.omega = 1.0;
+          c.iter = 1;
+          c.rho_new = tot[q];
+          if (fabs(c.rho_new) < DBL_MIN || fabs(c.omega) < DBL_MIN) {
+            c.fail = 1;
+            c.done = 1;
+          } else {
+            c.beta = (c.rho_new / c.rho) * (c.alpha / c.omega);
+          }
+        }
+      }
+      if (!c.done) all = 0;
+    }
+    st->all_done = all;
+    return;
+  }
   if (MODE == 0) {
     int all = 1;
     for (int q = 0; q < nc; ++q) {
@@ -1370,7 +1434,8 @@ namespace {
 template <bool kTrans, int MODE>
 void launch_tiled(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
                   const BiVecs &bv, int par, int64_t n, SolverState *st,
-                  Workspace &w) {
+                  Workspace &w, const double *xin = nullptr,
+                  const double *bin = nullptr, int nverify = 0) {
   // 2 CTAs per SM (<= 128 registers, 2 x 71 KB of shared memory) measured
   // best on C4: pass pv 5.3 TB/s, pass st 4.3 TB/s (1 CTA: 3.8 / 2.9; 3 CTAs
   // with the 80-register cap: 3.5 / 3.2).  PF_TILE_MINB overrides.
@@ -1387,7 +1452,8 @@ void launch_tiled(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
     }
     ++g_launches;
     kernel<<<grid, kTileThreads, kTileSmem, s>>>(tg, a, bv, par, n, st,
-                                                 w.partials, w.counters);
+                                                 w.partials, w.counters, xin,
+                                                 bin, nverify);
   };
   if (minb >= 3)
     go(k_bi_tiled<kTrans, MODE, 3>);
@@ -1445,8 +1511,11 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   launch(k_bi_reset, 1, 1, s, st, ncomp, maxiter, precond, tol, fresh, mask);
   if (fresh) launch(k_bi_bnorm, gr, kBlock, s, b, n, rg, st, w.partials, w.counters);
   halo(pl, s, {{x, ncomp}});
-  launch(k_bi_init<V, kTrans>, gr, kBlock, s, v, a, b, x, bv, st, w.partials,
-                                             w.counters);
+  if (tiled)
+    launch_tiled<kTrans, 2>(tg, tgrid, s, a, bv, 0, (int64_t)n, st, w, x, b, 0);
+  else
+    launch(k_bi_init<V, kTrans>, gr, kBlock, s, v, a, b, x, bv, st,
+           w.partials, w.counters);
   // slab plans: the stencil passes gather r, p, v and 1 / A_jj of the
   // neighbours (v[0] = 0 and dinv are exchanged once here)
   halo(pl, s, {{bv.v[0], ncomp}, {bv.dinv, 1}});
@@ -1481,6 +1550,10 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   }
   launch(k_bi_finish, ge, kBlock, s, x, n, rg, st);
   halo(pl, s, {{x, ncomp}});
+  if (tiled)
+    launch_tiled<kTrans, 3>(tg, tgrid, s, a, bv, 0, (int64_t)n, st, w, x, b,
+                            ncomp);
+  else
   launch(k_true_res<V>, gr, kBlock, s, v, a, kTrans ? 1 : 0, ncomp, b, x, st,
                                       w.partials, w.counters);
   PF_LAUNCH_CHECK("bicgstab finish");
