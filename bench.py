@@ -53,7 +53,8 @@ CONFIGS = {
               "C4 per-GPU slab proxy 128x96x128, fwd+adjoint"),
     "c5train": ((64, 48, 64), 1.095, 0.5,
                 "C5 LES training step: 64x48x64 sample per GPU, learned SGS "
-                "CNN corrector, 16-step unrolled fwd+adjoint, data parallel"),
+                "CNN corrector, 16-step unrolled fwd+adjoint, statistics "
+                "loss, data parallel"),
 }
 UNROLL = 16
 SAMPLE_SHAPE = (64, 48, 64)
@@ -429,10 +430,16 @@ def run_c5train(args, world, rank, local, dev):
     bc = torch.cat(list(state.bc), 0)
     cfg = piso.StepConfig(dt=dt, nu=nu, tol=args.tol)
     u0 = state.u.t().contiguous().t()
+    # the paper's statistics loss (S/stats.py:567-614) against the initial
+    # state's statistics, turbulent-channel weights
+    from paper_2505_16992_b200 import stats as S
+    sl = S.channel_slices(dom)
+    ref = tuple(t.detach() for t in S.frame_profile(sl, u0))
+    stats_target = (ref, S.tcf_default_weights(3), sl)
 
     def tstep():
         return les.train_step(dom, u0, bc, model, opt, forcing, nu, cfg,
-                              UNROLL, target)
+                              UNROLL, target, stats_target=stats_target)
 
     for _ in range(args.warmup):
         tstep()

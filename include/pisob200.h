@@ -368,6 +368,26 @@ PF_API int pf_reduce_dot(const pf_plan *plan, const double *x, const double *y,
 PF_API int pf_reduce_maxabs(const pf_plan *plan, const double *x, int64_t len,
                      void *workspace, double *out_host, void *stream);
 
+/* ---- channel statistics (SURVEY.md §8 f; S/stats.py) ----------------------- */
+
+/* frame_profile, S/stats.py:262-279 (slice_mean + slice_cov): for every
+ * wall-normal slice j (index along `wall_axis` of a box plan) the mean
+ * (Y, d) and the central covariance (Y, d, d) of the velocity (d, n) over
+ * the slice's cells, population convention; m3 / m4 (optional, (Y, d)) are
+ * the third and fourth central moments per component (ChannelAccumulator,
+ * S/stats.py:325-376).  Two-pass (means, then central products), fixed-order
+ * reductions; collective on slab plans (the slices span every rank). */
+PF_API int pf_slice_moments(const pf_plan *plan, const double *u,
+                            int32_t wall_axis, double *mean, double *cov,
+                            double *m3, double *m4, void *workspace,
+                            void *stream);
+/* frame_profile_backward, S/stats.py:281-290: du (d, n) on the owned cells
+ * from the cotangents of (mean, cov) of the same frame. */
+PF_API int pf_slice_moments_backward(const pf_plan *plan, const double *u,
+                                     int32_t wall_axis, const double *mean,
+                                     const double *d_mean, const double *d_cov,
+                                     double *du, void *stream);
+
 /* ---- slab decomposition across GPUs (SURVEY.md §8 e) ----------------------
  * The reference is single-process; these entry points have no reference
  * counterpart.  A slab plan (pf_plan_desc.slab_world > 0) computes its owned

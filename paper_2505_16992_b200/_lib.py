@@ -80,6 +80,10 @@ _SIGS = {
                           ctypes.POINTER(SolverReportC), c_ptr],
     "pf_cg_profile": [c_ptr, c_ptr, c_ptr, c_int, c_int, c_ptr, c_ptr,
                       ctypes.POINTER(c_dbl), c_ptr],
+    "pf_slice_moments": [c_ptr, c_ptr, c_int, c_ptr, c_ptr, c_ptr, c_ptr,
+                         c_ptr, c_ptr],
+    "pf_slice_moments_backward": [c_ptr, c_ptr, c_int, c_ptr, c_ptr, c_ptr,
+                                  c_ptr, c_ptr],
     "pf_comm_create": [c_ptr, ctypes.POINTER(c_ptr)],
     "pf_comm_ipc_handle": [c_ptr, c_ptr],
     "pf_comm_open_peer": [c_ptr, c_int, c_ptr],

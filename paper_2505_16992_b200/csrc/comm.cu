@@ -204,6 +204,16 @@ int comm_vec_allreduce(const Plan &p, double *buf, int k, int op,
   return PF_OK;
 }
 
+int comm_vec_allreduce_n(const Plan &p, double *buf, int64_t k, int op,
+                         cudaStream_t s) {
+  for (int64_t off = 0; off < k; off += kVecRedMax) {
+    const int len = (int)std::min<int64_t>(kVecRedMax, k - off);
+    int rc = comm_vec_allreduce(p, buf + off, len, op, s);
+    if (rc) return rc;
+  }
+  return PF_OK;
+}
+
 }  // namespace pf
 
 // ===========================================================================

@@ -154,6 +154,9 @@ int comm_barrier(const Plan &p, cudaStream_t s);
 int comm_check(const Plan &p, cudaStream_t s);
 int comm_vec_allreduce(const Plan &p, double *buf, int k, int op,
                        cudaStream_t s);
+// any length (chunks of the vector slot)
+int comm_vec_allreduce_n(const Plan &p, double *buf, int64_t k, int op,
+                         cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // face lookup

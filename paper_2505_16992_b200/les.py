@@ -9,8 +9,10 @@ training step here is:
    (:func:`~paper_2505_16992_b200.autograd.piso_step_fn`) on one
    64 x 48 x 64 channel sample per process, with source = wall forcing +
    S_theta(u);
-2. a loss on the rollout (mean streamwise profile against a target, summed
-   over the unrolled frames);
+2. a loss on the rollout: the paper's statistics loss (per-frame and
+   window-averaged wall-normal mean / covariance profiles against reference
+   statistics, S/stats.py:567-614, profiles from :mod:`.stats` on the
+   device), or a plain mean-streamwise-profile loss;
 3. ``loss.backward()`` -- the discrete adjoint through every step, then the
    CNN's own backward;
 4. data-parallel gradient averaging across processes (one sample per GPU;
@@ -76,6 +78,25 @@ def unrolled_loss(domain, u0, bc, model, forcing, nu, cfg, steps,
     return loss / steps, u
 
 
+def stats_unrolled_loss(domain, u0, bc, model, forcing, nu, cfg, steps,
+                        reference, weights, slices=None, step_fn=None):
+    """Differentiable k-step rollout scored by the statistics loss of the
+    training runs (S/stats.py:567-614): frame profiles from the device
+    kernels (stats.FrameProfile), window + weighted per-frame terms.
+    Returns (loss, final velocity)."""
+    from . import stats as _st
+    step_fn = step_fn or (lambda u, src: _ag.piso_step_fn(domain, u, src, nu,
+                                                          bc, cfg)[0])
+    sl = slices or _st.channel_slices(domain)
+    u = u0
+    profiles = []
+    for _ in range(steps):
+        src = forcing(u.detach(), nu) + model(u)
+        u = step_fn(u, src)
+        profiles.append(_st.frame_profile_fn(sl, u))
+    return _st.stats_loss_torch(profiles, reference, weights), u
+
+
 def average_gradients(model):
     """All-reduce-mean the parameter gradients over the default process
     group (the data-parallel collective of config 5)."""
@@ -95,16 +116,24 @@ def average_gradients(model):
 
 
 def train_step(domain, u0, bc, model, opt, forcing, nu, cfg, steps,
-               target_profile, step_fn=None):
-    """One data-parallel training step; returns the (local) loss value."""
+               target_profile, step_fn=None, stats_target=None):
+    """One data-parallel training step; returns the (local) loss value.
+    ``stats_target`` = (reference (mean, cov), LossWeights[, slices])
+    selects the statistics loss instead of the mean-profile loss."""
     opt.zero_grad(set_to_none=True)
-    loss, _ = unrolled_loss(domain, u0, bc, model, forcing, nu, cfg, steps,
-                            target_profile, step_fn)
+    if stats_target is not None:
+        ref, weights = stats_target[0], stats_target[1]
+        sl = stats_target[2] if len(stats_target) > 2 else None
+        loss, _ = stats_unrolled_loss(domain, u0, bc, model, forcing, nu,
+                                      cfg, steps, ref, weights, sl, step_fn)
+    else:
+        loss, _ = unrolled_loss(domain, u0, bc, model, forcing, nu, cfg,
+                                steps, target_profile, step_fn)
     loss.backward()
     average_gradients(model)
     opt.step()
     return float(loss.detach())
 
 
-__all__ = ["SGSCorrector", "unrolled_loss", "average_gradients",
-           "train_step"]
+__all__ = ["SGSCorrector", "unrolled_loss", "stats_unrolled_loss",
+           "average_gradients", "train_step"]
