@@ -30,14 +30,23 @@ __device__ __forceinline__ double2 twiddle(const double2 *tw, int k) {
   return w;
 }
 
+// Shared-memory layout of a line: element i sits at pad(i) = i + i / 16, so
+// the power-of-two strides of the butterflies spread over the banks (one
+// 16-byte pad slot per 16 elements; line stride padded_len(N)).
+__host__ __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
+__host__ __device__ __forceinline__ int padded_len(int n) {
+  return n + (n >> 4);
+}
+
 // Stockham autosort FFT (radix 4, a final radix-2 stage when log2 N is odd)
-// of `nl` lines of length N held in shared memory, line stride N; b is
-// scratch of the same size.  Returns the buffer holding the natural-order
+// of `nl` lines of length N held in shared memory (padded layout above);
+// b is scratch of the same size.  Returns the buffer holding the natural-order
 // result.  Forward: exp(-2 pi i jk / N); inverse: exp(+...), unnormalised.
 template <bool kInv>
 __device__ double2 *fft_lines(double2 *a, double2 *b, int N, int nl,
                               const double2 *tw) {
   const int q4 = N >> 2;
+  const int NP = padded_len(N);
   int n = N, ls = 0;  // current length, log2 of the stride
   while (n >= 4) {
     const int n1 = n >> 2, s = 1 << ls;
@@ -45,21 +54,23 @@ __device__ double2 *fft_lines(double2 *a, double2 *b, int N, int nl,
       const int line = t / q4;
       const int k = t - line * q4;
       const int q = k & (s - 1), p = k >> ls;
-      const double2 *x = a + line * N;
-      double2 *y = b + line * N;
-      const double2 x0 = x[q + s * p], x1 = x[q + s * (p + n1)];
-      const double2 x2 = x[q + s * (p + 2 * n1)];
-      const double2 x3 = x[q + s * (p + 3 * n1)];
+      const double2 *x = a + line * NP;
+      double2 *y = b + line * NP;
+      const double2 x0 = x[pad(q + s * p)], x1 = x[pad(q + s * (p + n1))];
+      const double2 x2 = x[pad(q + s * (p + 2 * n1))];
+      const double2 x3 = x[pad(q + s * (p + 3 * n1))];
       const double2 apc = cadd(x0, x2), amc = csub(x0, x2);
       const double2 bpd = cadd(x1, x3), bmd = csub(x1, x3);
       // forward: j (b - d) with j = i; the inverse flips its sign
       const double2 jb = kInv ? make_double2(bmd.y, -bmd.x)
                               : make_double2(-bmd.y, bmd.x);
       const int ps = p << ls;
-      y[q + s * (4 * p)] = cadd(apc, bpd);
-      y[q + s * (4 * p + 1)] = cmul(twiddle<kInv>(tw, ps), csub(amc, jb));
-      y[q + s * (4 * p + 2)] = cmul(twiddle<kInv>(tw, 2 * ps), csub(apc, bpd));
-      y[q + s * (4 * p + 3)] = cmul(twiddle<kInv>(tw, 3 * ps), cadd(amc, jb));
+      y[pad(q + s * (4 * p))] = cadd(apc, bpd);
+      y[pad(q + s * (4 * p + 1))] = cmul(twiddle<kInv>(tw, ps), csub(amc, jb));
+      y[pad(q + s * (4 * p + 2))] =
+          cmul(twiddle<kInv>(tw, 2 * ps), csub(apc, bpd));
+      y[pad(q + s * (4 * p + 3))] =
+          cmul(twiddle<kInv>(tw, 3 * ps), cadd(amc, jb));
     }
     __syncthreads();
     double2 *tmp = a;
@@ -73,11 +84,11 @@ __device__ double2 *fft_lines(double2 *a, double2 *b, int N, int nl,
     for (int t = threadIdx.x; t < nl * s; t += blockDim.x) {
       const int line = t / s;
       const int q = t - line * s;
-      const double2 *x = a + line * N;
-      double2 *y = b + line * N;
-      const double2 x0 = x[q], x1 = x[q + s];
-      y[q] = cadd(x0, x1);
-      y[q + s] = csub(x0, x1);
+      const double2 *x = a + line * NP;
+      double2 *y = b + line * NP;
+      const double2 x0 = x[pad(q)], x1 = x[pad(q + s)];
+      y[pad(q)] = cadd(x0, x1);
+      y[pad(q + s)] = csub(x0, x1);
     }
     __syncthreads();
     a = b;
@@ -114,7 +125,7 @@ __global__ void __launch_bounds__(kFftThreads)
     k_spec_fwd_z(SpecPlan sp, const double *__restrict__ r, const int *done) {
   SPEC_DONE_RETURN;
   extern __shared__ double2 sm[];
-  const int N = sp.sz, LP = sp.lpz, nk = sp.nkz;
+  const int N = sp.sz, LP = sp.lpz, nk = sp.nkz, NP = padded_len(N);
   const int64_t npairs = (int64_t)sp.nxl * sp.sy / 2;
   const int64_t ntiles = (npairs + LP - 1) / LP;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -127,17 +138,17 @@ __global__ void __launch_bounds__(kFftThreads)
         v.x = r[zline_base(sp, 2 * g) + z];
         v.y = r[zline_base(sp, 2 * g + 1) + z];
       }
-      sm[e] = v;
+      sm[j * NP + pad(z)] = v;
     }
     __syncthreads();
-    const double2 *f = fft_lines<false>(sm, sm + LP * N, N, LP, sp.twz);
+    const double2 *f = fft_lines<false>(sm, sm + LP * NP, N, LP, sp.twz);
     for (int e = threadIdx.x; e < 2 * LP * nk; e += blockDim.x) {
       const int kz = e / (2 * LP), jj = e - kz * 2 * LP;
       const int j = jj >> 1, side = jj & 1;
       const int64_t g = g0 + j;
       if (g >= npairs) continue;
-      const double2 zk = f[j * N + kz];
-      const double2 zm = f[j * N + ((N - kz) & (N - 1))];
+      const double2 zk = f[j * NP + pad(kz)];
+      const double2 zm = f[j * NP + pad((N - kz) & (N - 1))];
       // Z = A + iB with A, B the transforms of the two real lines
       const double2 o =
           side == 0 ? make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y))
@@ -156,7 +167,7 @@ __global__ void __launch_bounds__(kFftThreads)
     k_spec_x(SpecPlan sp, const int *done) {
   SPEC_DONE_RETURN;
   extern __shared__ double2 sm[];
-  const int N = sp.sx, LP = sp.lpx;
+  const int N = sp.sx, LP = sp.lpx, NP = padded_len(N);
   const int64_t nlines =
       (int64_t)sp.sy * (sp.kz0[sp.rank + 1] - sp.kz0[sp.rank]);
   const int64_t ntiles = (nlines + LP - 1) / LP;
@@ -164,11 +175,17 @@ __global__ void __launch_bounds__(kFftThreads)
     const int64_t l0 = tile * LP;
     const int64_t nl = nlines - l0 < LP ? nlines - l0 : LP;
     double2 *src = sp.s + l0 * N;
-    for (int e = threadIdx.x; e < LP * N; e += blockDim.x)
-      sm[e] = e < nl * N ? __ldcg(src + e) : make_double2(0.0, 0.0);
+    for (int e = threadIdx.x; e < LP * N; e += blockDim.x) {
+      const int ln = e / N, xx = e - ln * N;
+      sm[ln * NP + pad(xx)] =
+          e < nl * N ? __ldcg(src + e) : make_double2(0.0, 0.0);
+    }
     __syncthreads();
-    const double2 *f = fft_lines<kInv>(sm, sm + LP * N, N, LP, sp.twx);
-    for (int e = threadIdx.x; e < nl * N; e += blockDim.x) src[e] = f[e];
+    const double2 *f = fft_lines<kInv>(sm, sm + LP * NP, N, LP, sp.twx);
+    for (int e = threadIdx.x; e < nl * N; e += blockDim.x) {
+      const int ln = e / N, xx = e - ln * N;
+      src[e] = f[ln * NP + pad(xx)];
+    }
     __syncthreads();
   }
 }
@@ -263,7 +280,7 @@ __global__ void __launch_bounds__(kFftThreads)
                  double *__restrict__ z, CgFuse fz, const int *done) {
   SPEC_DONE_RETURN;
   extern __shared__ double2 sm[];
-  const int N = sp.sz, LP = sp.lpz, half = N >> 1;
+  const int N = sp.sz, LP = sp.lpz, half = N >> 1, NP = padded_len(N);
   const int64_t npairs = (int64_t)sp.nxl * sp.sy / 2;
   const int64_t ntiles = (npairs + LP - 1) / LP;
   double sums[3] = {0.0, 0.0, 0.0};
@@ -281,15 +298,15 @@ __global__ void __launch_bounds__(kFftThreads)
         v = k <= half ? make_double2(a.x - b.y, a.y + b.x)
                       : make_double2(a.x + b.y, b.x - a.y);
       }
-      sm[j * N + k] = v;
+      sm[j * NP + pad(k)] = v;
     }
     __syncthreads();
-    const double2 *f = fft_lines<true>(sm, sm + LP * N, N, LP, sp.twz);
+    const double2 *f = fft_lines<true>(sm, sm + LP * NP, N, LP, sp.twz);
     for (int e = threadIdx.x; e < LP * N; e += blockDim.x) {
       const int j = e / N, zz = e - j * N;
       const int64_t g = g0 + j;
       if (g >= npairs) continue;
-      const double2 v = f[e];
+      const double2 v = f[j * NP + pad(zz)];
       const int64_t i0 = zline_base(sp, 2 * g) + zz;
       const int64_t i1 = zline_base(sp, 2 * g + 1) + zz;
       z[i0] = v.x;
@@ -495,12 +512,12 @@ int spec_apply(const MgLevel &l0, const SpecPlan &sp, const double *r,
   const int64_t npairs = (int64_t)sp.nxl * sp.sy / 2;
   const int zt = (int)std::min<int64_t>((npairs + sp.lpz - 1) / sp.lpz,
                                         1 << 20);
-  const size_t zsm = 2 * sizeof(double2) * sp.lpz * sp.sz;
+  const size_t zsm = 2 * sizeof(double2) * sp.lpz * padded_len(sp.sz);
   const int nkl = sp.kz0[sp.rank + 1] - sp.kz0[sp.rank];
   const int64_t xlines = (int64_t)sp.sy * nkl;
   const int xt = (int)std::min<int64_t>((xlines + sp.lpx - 1) / sp.lpx,
                                         1 << 20);
-  const size_t xsm = 2 * sizeof(double2) * sp.lpx * sp.sx;
+  const size_t xsm = 2 * sizeof(double2) * sp.lpx * padded_len(sp.sx);
   const int64_t ncol2 = 2 * (int64_t)nkl * sp.sx;
   mark(0);
   launch_smem(k_spec_fwd_z, zt, kFftThreads, zsm, s, sp, r, done);
