@@ -120,6 +120,13 @@ typedef struct pf_plan_desc {
   int32_t slab_rank;
   int64_t slab_nx;
   int64_t slab_x0;
+  /* Separable (tensor-product, axis-aligned) box: the cell widths dx[a][k]
+   * and their inverses along each axis (NULL otherwise).  Kernels then form
+   * J = prod dx, T = diag(1/dx), alpha = J T^2 from these 1-D arrays (same
+   * operation order as the full (n) arrays) instead of streaming 13 metric
+   * values per cell from HBM. */
+  const double *sep_dx[3];
+  const double *sep_inv[3];
 } pf_plan_desc;
 
 typedef struct pf_plan pf_plan;

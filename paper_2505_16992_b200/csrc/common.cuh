@@ -176,6 +176,7 @@ __device__ __forceinline__ int back_face(const Face &fc, int s) {
 }
 
 struct GatherTopo {
+  static constexpr bool kBox = false;
   const int32_t *nbr;
   int64_t n;
   struct Cell {
@@ -202,6 +203,7 @@ struct GatherTopo {
 
 template <int D>
 struct BoxTopo {
+  static constexpr bool kBox = true;
   int32_t shape[3];
   int32_t stride[3];
   int32_t periodic[3];
@@ -283,6 +285,21 @@ struct View {
   const int32_t *__restrict__ bfid;       // (m) face id
   const int32_t *__restrict__ finfo;      // (nfaces, 8)
   int32_t has_cross;
+  // separable box metrics (sep != 0): 1-D widths and inverse widths; T
+  // (9 values per cell, diagonal) is formed from them
+  int32_t sep;
+  const double *__restrict__ sdx[3];
+  const double *__restrict__ sinv[3];
+
+  __device__ __forceinline__ int32_t coord(int a, int32_t i) const {
+    if constexpr (Topo::kBox) {
+      if (a == D - 1) return i % topo.shape[a];
+      if (a == 0) return i / topo.stride[0];
+      return (i / topo.stride[a]) % topo.shape[a];
+    } else {
+      return 0;
+    }
+  }
 
   __device__ __forceinline__ Rng rng() const { return Rng{i0, i1, ng}; }
   __host__ __device__ __forceinline__ int32_t owned() const { return i1 - i0; }
@@ -290,13 +307,17 @@ struct View {
     return __ldg(alpha_full + (int64_t)(a * D + k) * n + i);
   }
   __device__ __forceinline__ double T(int a, int j, int32_t i) const {
+    if (Topo::kBox && sep)
+      return a == j ? __ldg(sinv[a] + coord(a, i)) : 0.0;
     return __ldg(tmat + (int64_t)(a * D + j) * n + i);
+  }
+  // J and alpha stay full (n) arrays: their callers gather them at the
+  // neighbours, where decoding coordinates would cost more than the load
+  __device__ __forceinline__ double J(int32_t i) const {
+    return __ldg(jac + i);
   }
   __device__ __forceinline__ double A(int a, int32_t i) const {
     return __ldg(alpha + (int64_t)a * n + i);
-  }
-  __device__ __forceinline__ double J(int32_t i) const {
-    return __ldg(jac + i);
   }
   // contravariant flux component a of a (D, n) SoA velocity at cell i
   __device__ __forceinline__ double flux(const double *__restrict__ u, int a,
@@ -339,6 +360,11 @@ View<D, Topo> make_view(const Plan &p, const Topo &topo) {
   v.bfid = p.d.bfid;
   v.finfo = p.d.finfo;
   v.has_cross = p.d.has_cross;
+  v.sep = p.d.sep_dx[0] != nullptr && p.d.sep_inv[0] != nullptr;
+  for (int a = 0; a < 3; ++a) {
+    v.sdx[a] = p.d.sep_dx[a];
+    v.sinv[a] = p.d.sep_inv[a];
+  }
   return v;
 }
 

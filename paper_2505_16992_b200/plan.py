@@ -75,6 +75,10 @@ class DevicePlan:
                 tmat[a * d + a] = t
                 alpha[a] = jac * (t * t)
             self.jac, self.tmat, self.alpha_diag = jac, tmat, alpha
+            # the 1-D widths the kernels form the same values from
+            self.sep_dx = [torch.as_tensor(sep[a], **f64).contiguous()
+                           for a in range(d)]
+            self.sep_inv = [1.0 / w for w in self.sep_dx]
         else:
             self.jac = torch.as_tensor(domain.jac, **f64).contiguous()
             tm = np.ascontiguousarray(
@@ -83,6 +87,7 @@ class DevicePlan:
             al = np.ascontiguousarray(
                 domain.alpha[:, np.arange(d), np.arange(d)].T)
             self.alpha_diag = torch.as_tensor(al, **f64)
+            self.sep_dx = self.sep_inv = None
 
         # --- boundary entries ------------------------------------------------
         faces = domain.bfaces
@@ -184,6 +189,11 @@ class DevicePlan:
             desc.slab_world, desc.slab_rank = int(info[0]), int(info[1])
             desc.slab_nx, desc.slab_x0 = int(info[2]), int(info[3])
         self.slab = info is not None
+        if self.sep_dx is not None and box is not None and \
+                not self.nonortho:
+            for a in range(d):
+                desc.sep_dx[a] = self.sep_dx[a].data_ptr()
+                desc.sep_inv[a] = self.sep_inv[a].data_ptr()
         self.comm = None
         self._desc = desc
         handle = ctypes.c_void_p()
