@@ -14,6 +14,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def bench_names(kernel):
     k = re.sub(r"^void ", "", kernel)
     base = re.match(r"(?:pf::)?(\w+)", k).group(1)
+    if base == "k_bi_tiled":
+        m = re.search(r"k_bi_tiled<(\w+),\s*(\d)", k)
+        adj = m.group(1) in ("1", "true")
+        nm = {"0": "k_bi_pv", "1": "k_bi_st", "2": "k_bi_init",
+              "3": "k_bi_verify"}[m.group(2)]
+        return [nm + (" (adjoint)" if adj else "")]
     if base in ("k_bi_pv", "k_bi_st"):
         adj = re.search(r",\s*(?:true|1)>", k) is not None
         return [base + (" (adjoint)" if adj else "")]
