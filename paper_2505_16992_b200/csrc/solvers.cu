@@ -682,33 +682,51 @@ __global__ void __launch_bounds__(kBlock)
   const int32_t v1e = (n & 1) ? rg.i1 : (rg.i1 & ~1);
   const int32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int32_t nth = gridDim.x * blockDim.x;
+  const double *__restrict__ rr_ = w.r;
+  const double *__restrict__ tt_ = w.t;
+  const double *__restrict__ rh_ = w.rhat;
+  const double *__restrict__ di_ = w.dinv;
+  double *__restrict__ rw_ = w.r;
   for (int32_t k = v0 + 2 * tid; k + 1 < v1e; k += 2 * nth) {
-    const double2 di = *reinterpret_cast<const double2 *>(w.dinv + k);
-    _Pragma("unroll") for (int q = 0; q < 3; ++q) {
-      if (q >= nc) break;
+    // every load of the three components first (the stores below cannot
+    // then serialise them), then the updates
+    const double2 di = *reinterpret_cast<const double2 *>(di_ + k);
+    double2 pp[3], xx[3], rr[3], vv[3], tt[3], rh[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      if (q >= nc || !(act[q] || pend[q])) continue;
       const int64_t o = (int64_t)q * n + k;
-      const double2 pp = *reinterpret_cast<const double2 *>(p1 + o);
-      double2 xx = *reinterpret_cast<const double2 *>(x + o);
+      pp[q] = *reinterpret_cast<const double2 *>(p1 + o);
+      xx[q] = *reinterpret_cast<const double2 *>(x + o);
+      if (!act[q]) continue;
+      rr[q] = *reinterpret_cast<const double2 *>(rr_ + o);
+      vv[q] = *reinterpret_cast<const double2 *>(v1 + o);
+      tt[q] = *reinterpret_cast<const double2 *>(tt_ + o);
+      rh[q] = *reinterpret_cast<const double2 *>(rh_ + o);
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      if (q >= nc || !(act[q] || pend[q])) continue;
+      const int64_t o = (int64_t)q * n + k;
+      double2 xn = xx[q];
       if (pend[q]) {
-        xx.x += alpha[q] * (pp.x * di.x);
-        xx.y += alpha[q] * (pp.y * di.y);
+        xn.x += alpha[q] * (pp[q].x * di.x);
+        xn.y += alpha[q] * (pp[q].y * di.y);
       }
       if (act[q]) {
-        const double2 rr = *reinterpret_cast<const double2 *>(w.r + o);
-        const double2 vv = *reinterpret_cast<const double2 *>(v1 + o);
-        const double2 tt = *reinterpret_cast<const double2 *>(w.t + o);
-        const double2 rh = *reinterpret_cast<const double2 *>(w.rhat + o);
-        const double s0 = rr.x - alpha[q] * vv.x, s1 = rr.y - alpha[q] * vv.y;
-        xx.x = xx.x + alpha[q] * (pp.x * di.x) + omega[q] * (s0 * di.x);
-        xx.y = xx.y + alpha[q] * (pp.y * di.y) + omega[q] * (s1 * di.y);
-        const double r0 = s0 - omega[q] * tt.x, r1 = s1 - omega[q] * tt.y;
-        *reinterpret_cast<double2 *>(w.r + o) = make_double2(r0, r1);
+        const double s0 = rr[q].x - alpha[q] * vv[q].x;
+        const double s1 = rr[q].y - alpha[q] * vv[q].y;
+        xn.x = xn.x + alpha[q] * (pp[q].x * di.x) + omega[q] * (s0 * di.x);
+        xn.y = xn.y + alpha[q] * (pp[q].y * di.y) + omega[q] * (s1 * di.y);
+        const double r0 = s0 - omega[q] * tt[q].x;
+        const double r1 = s1 - omega[q] * tt[q].y;
+        *reinterpret_cast<double2 *>(rw_ + o) = make_double2(r0, r1);
         acc[2 * q] += r0 * r0;
         acc[2 * q] += r1 * r1;
-        acc[2 * q + 1] += rh.x * r0;
-        acc[2 * q + 1] += rh.y * r1;
+        acc[2 * q + 1] += rh[q].x * r0;
+        acc[2 * q + 1] += rh[q].y * r1;
       }
-      if (pend[q] || act[q]) *reinterpret_cast<double2 *>(x + o) = xx;
+      *reinterpret_cast<double2 *>(x + o) = xn;
     }
   }
   // scalar edges of the owned range
