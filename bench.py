@@ -461,7 +461,7 @@ def run_c5train(args, world, rank, local, dev):
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device="cpu" if share_dev() else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = world * dom.n * UNROLL * args.steps / (ms / 1e3) / 1e6
@@ -481,6 +481,10 @@ def run_c5train(args, world, rank, local, dev):
             "clocks": clk}))
     if world > 1:
         dist.destroy_process_group()
+
+
+def share_dev():
+    return os.environ.get("PF_BENCH_SHARE_DEVICE") == "1"
 
 
 def build_workload(args, dev, rank=0, world=1):
@@ -523,10 +527,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PF_BENCH_SHARE_DEVICE=1 (correctness runs of the multi-rank path on a
+    # one-GPU box): every rank on cuda:0, gloo for the host-side collectives
+    share = os.environ.get("PF_BENCH_SHARE_DEVICE") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     from paper_2505_16992_b200 import _lib, adjoint, piso
 
@@ -588,7 +600,7 @@ def main():
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device="cpu" if share_dev() else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
         ms = float(t.item())
@@ -652,7 +664,7 @@ def main():
     torch.cuda.synchronize()
     ms_e2e = e2.elapsed_time(e3)
     if world > 1:
-        t = torch.tensor([ms_e2e], device=dev)
+        t = torch.tensor([ms_e2e], device="cpu" if share_dev() else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
     e2e_value = cells_job * args.steps / (ms_e2e / 1e3) / 1e6
