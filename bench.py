@@ -20,7 +20,7 @@ The other configs run one replica per rank (weak scaling).
 
 --impl reference runs the reference's own CPU implementation (pisoflow,
 built unmodified into oracle/_ref by oracle/build_ref.py) on rank 0, one
-single-threaded process per host core up to 8, each advancing a bounded
+single-threaded process per host core, each advancing a bounded
 sample of the workload (the same channel recipe at 64x48x64 cells).
 """
 
@@ -143,7 +143,10 @@ def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    procs = max(1, min(os.cpu_count() or 1, 8))
+    # one single-threaded reference process per host core (the reference is
+    # serial; this is every host thread it can use)
+    procs = max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
+                else (os.cpu_count() or 1))
     steps = max(1, args.steps)
     try:
         from oracle import build_ref
