@@ -488,6 +488,9 @@ int spec_setup(const MgLevel &l0, const SpecPlan &sp, cudaStream_t s,
 template <typename... KArgs, typename... Args>
 static void launch_smem(void (*kernel)(KArgs...), int grid, int block,
                         size_t smem, cudaStream_t stream, Args... args) {
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
   ++g_launches;
   kernel<<<grid, block, smem, stream>>>(args...);
 }
