@@ -201,6 +201,18 @@ struct GatherTopo {
   }
 };
 
+// quotient of a non-negative int32 by a positive divisor through a double
+// reciprocal (exact after the +-1 correction; cheaper than the ~20
+// instruction integer division with a runtime divisor)
+__device__ __forceinline__ int32_t fast_div(int32_t i, int32_t d,
+                                            double inv) {
+  int32_t q = __double2int_rz((double)i * inv);
+  int32_t r = i - q * d;
+  if (r < 0) --q;
+  else if (r >= d) ++q;
+  return q;
+}
+
 template <int D>
 struct BoxTopo {
   static constexpr bool kBox = true;
@@ -208,6 +220,8 @@ struct BoxTopo {
   int32_t stride[3];
   int32_t periodic[3];
   int32_t face_off[6];
+  double inv_stride[3];  // 1 / stride (fast_div)
+  double inv_shape[3];   // 1 / shape
   struct Cell {
     int32_t i;
     int32_t x[3];
@@ -218,7 +232,7 @@ struct BoxTopo {
     int32_t rem = i;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      c.x[a] = rem / stride[a];
+      c.x[a] = a == D - 1 ? rem : fast_div(rem, stride[a], inv_stride[a]);
       rem -= c.x[a] * stride[a];
     }
     return c;
@@ -293,9 +307,10 @@ struct View {
 
   __device__ __forceinline__ int32_t coord(int a, int32_t i) const {
     if constexpr (Topo::kBox) {
-      if (a == D - 1) return i % topo.shape[a];
-      if (a == 0) return i / topo.stride[0];
-      return (i / topo.stride[a]) % topo.shape[a];
+      const int32_t q = a == 0 ? i : fast_div(i, topo.stride[a],
+                                              topo.inv_stride[a]);
+      if (a == 0) return fast_div(i, topo.stride[0], topo.inv_stride[0]);
+      return q - fast_div(q, topo.shape[a], topo.inv_shape[a]) * topo.shape[a];
     } else {
       return 0;
     }
@@ -453,6 +468,10 @@ BoxTopo<D> make_box(const Plan &p) {
     t.shape[a] = 1;
     t.stride[a] = 1;
     t.periodic[a] = 0;
+  }
+  for (int a = 0; a < 3; ++a) {
+    t.inv_stride[a] = 1.0 / t.stride[a];
+    t.inv_shape[a] = 1.0 / t.shape[a];
   }
   for (int f = 0; f < 6; ++f) t.face_off[f] = (int32_t)p.d.box_face_offset[f];
   return t;
