@@ -777,13 +777,14 @@ __global__ void __launch_bounds__(kBlock)
 // prologue planes of a chunk, from L2), instead of once per stencil point.
 
 constexpr int kTZ = 32, kTY = 8, kTileThreads = kTZ * kTY;
-constexpr int kXChunk = 32;
+constexpr int kXChunk = 32;  // X planes per tile (fewer on small boxes)
 
 struct TileGeo {
   int32_t X, Y, Z;          // local box
   int32_t px, py, pz;       // periodic flags
   int32_t x0, x1;           // owned planes [x0, x1)
   int32_t ty_tiles, tz_tiles, chunks, ntiles;
+  int32_t xc;               // X planes per chunk
 };
 
 __device__ __forceinline__ int32_t wrap(int32_t c, int32_t L, int32_t per,
@@ -932,8 +933,8 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
     const int tyt = rest % tg.ty_tiles;
     const int ch = rest / tg.ty_tiles;
     const int32_t y = tyt * kTY + ty, z = tzt * kTZ + tz;
-    const int32_t xs = tg.x0 + ch * kXChunk;
-    const int32_t xe = min(xs + kXChunk, tg.x1);
+    const int32_t xs = tg.x0 + ch * tg.xc;
+    const int32_t xe = min(xs + tg.xc, tg.x1);
     // the halo slot this thread fills (64 along Y, 16 along Z)
     bool halo_cell = true;
     int hy = 0, hz = 0, sy_ = 0, sz_ = 0;
@@ -1517,7 +1518,17 @@ bool tile_geo(const Plan &pl, const V &v, TileGeo &tg) {
   tg.x1 = (int32_t)(pl.i1 / plane);
   tg.ty_tiles = tg.Y / kTY;
   tg.tz_tiles = tg.Z / kTZ;
-  tg.chunks = (tg.x1 - tg.x0 + kXChunk - 1) / kXChunk;
+  // chunks of kXChunk planes, halved down to 4 until the tiles fill the GPU
+  // (two CTAs per SM, two waves): small boxes (the 64 x 48 x 64 LES
+  // sample) would otherwise run a few dozen CTAs
+  tg.xc = kXChunk;
+  const int64_t want = 4LL * pl.num_sms;
+  const int32_t nx = tg.x1 - tg.x0;
+  while (tg.xc > 4 &&
+         (int64_t)tg.ty_tiles * tg.tz_tiles * ((nx + tg.xc - 1) / tg.xc) <
+             want)
+    tg.xc /= 2;
+  tg.chunks = (nx + tg.xc - 1) / tg.xc;
   tg.ntiles = tg.ty_tiles * tg.tz_tiles * tg.chunks;
   return true;
 }
