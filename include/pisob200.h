@@ -127,6 +127,9 @@ typedef struct pf_plan_desc {
    * values per cell from HBM. */
   const double *sep_dx[3];
   const double *sep_inv[3];
+  /* optional (n) array 1 / jac (exactly 1.0 / jac[i]); kernels that divide
+   * by J at several cells per cell load it instead */
+  const double *ijac;
 } pf_plan_desc;
 
 typedef struct pf_plan pf_plan;

@@ -41,7 +41,7 @@ class PlanDesc(ctypes.Structure):
         ("geom_precond", c_int),
         ("slab_world", c_int), ("slab_rank", c_int), ("slab_nx", c_i64),
         ("slab_x0", c_i64),
-        ("sep_dx", c_ptr * 3), ("sep_inv", c_ptr * 3),
+        ("sep_dx", c_ptr * 3), ("sep_inv", c_ptr * 3), ("ijac", c_ptr),
     ]
 
 

@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kBlock)
     const int bf = __ldg(v.bface + e);
     const int f = bf & 15, kind = bf >> 4;
     const double nsgn = (f & 1) ? 1.0 : -1.0;
-    const double invj = 1.0 / v.J(i);
+    const double invj = v.IJ(i);
     const double fj = __ldg(v.bjac + e);
     double cr[D], ub[D], tr[D];
     double tu = 0.0, crub = 0.0;
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kBlock)
   RANGE_LOOP(j, v.rng()) {
     const auto cell = v.topo.cell(j);
     const double cdj = dc[j];
-    const double invj = 1.0 / v.J(j);
+    const double invj = v.IJ(j);
     double gf[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) gf[a] = 0.0;
@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(kBlock)
         const int fb = back_face(fc, f & 1);
         const double ci = dc[(int64_t)(1 + fb) * n + i] + dc[i];
         const double nsb = (fb & 1) ? 1.0 : -1.0;
-        const double cfm = 0.5 * (0.5 * nsb * (1.0 / v.J(i)) * ci);
+        const double cfm = 0.5 * (0.5 * nsb * (v.IJ(i)) * ci);
         gf[a] += fc.neg ? -cfm : cfm;
       } else {
         const int32_t e = fc.bidx;

@@ -286,6 +286,7 @@ struct View {
   int32_t i0, i1;  // owned cells (the whole range unless a slab plan)
   double ng;       // owned cells over all ranks (means, zero-mean projection)
   const double *__restrict__ jac;
+  const double *__restrict__ ijac;   // 1 / jac (or null)
   const double *__restrict__ tmat;   // (D*D, n)
   const double *__restrict__ alpha;  // (D, n)
   const int32_t *__restrict__ bcell;
@@ -331,6 +332,10 @@ struct View {
   __device__ __forceinline__ double J(int32_t i) const {
     return __ldg(jac + i);
   }
+  // 1.0 / J(i), bitwise (a load where the plan carries the array)
+  __device__ __forceinline__ double IJ(int32_t i) const {
+    return ijac ? __ldg(ijac + i) : 1.0 / __ldg(jac + i);
+  }
   __device__ __forceinline__ double A(int a, int32_t i) const {
     return __ldg(alpha + (int64_t)a * n + i);
   }
@@ -363,6 +368,7 @@ View<D, Topo> make_view(const Plan &p, const Topo &topo) {
   v.i1 = p.i1;
   v.ng = p.ng;
   v.jac = p.d.jac;
+  v.ijac = p.d.ijac;
   v.tmat = p.d.tmat;
   v.alpha = p.d.alpha_diag;
   v.bcell = p.d.bcell;

@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(kBlock)
   const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= v.i1) return;
   const auto cell = v.topo.cell(i);
-  const double invj = 1.0 / v.J(i);
+  const double invj = v.IJ(i);
   double diag = 1.0 / dt;
   const int64_t n = v.n;
 #pragma unroll
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(kBlock)
 #pragma unroll
   for (int c = 0; c < D; ++c)
     r[c] = u[c * n + i] / dt + (src_uniform ? src[c] : src[c * n + i]);
-  const double invj = 1.0 / v.J(i);
+  const double invj = v.IJ(i);
 #pragma unroll
   for (int f = 0; f < 2 * D; ++f) {
     const Face fc = v.topo.face(cell, f);

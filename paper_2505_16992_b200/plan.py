@@ -159,6 +159,8 @@ class DevicePlan:
             desc.nbr = self.nbr.data_ptr()
             self.topo = "gather"
         desc.jac = self.jac.data_ptr()
+        self.ijac = 1.0 / self.jac
+        desc.ijac = self.ijac.data_ptr()
         desc.tmat = self.tmat.data_ptr()
         desc.alpha_diag = self.alpha_diag.data_ptr()
         desc.m = m
