@@ -62,21 +62,28 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
-__global__ void __launch_bounds__(kBlock)
-    k_halo_get(CommDev *c, HaloSet hs, int64_t nxl) {
-  const int64_t plane = c->plane;
+// one thread waits for both neighbours' flags of the current exchange (a
+// single spinning CTA: several slabs sharing a device must never fill it
+// with waiting CTAs)
+__global__ void k_halo_wait(CommDev *c) {
+  if (threadIdx.x != 0) return;
   const unsigned long long e = vload(&c->halo_seq);
   const int par = (int)(e & 1);
   char *mine = c->peer[c->rank];
-  if (threadIdx.x == 0) {
-    wait_flag(c, flag_at(mine, kOffHaloFlag, par * 2 + 0), e);
-    wait_flag(c, flag_at(mine, kOffHaloFlag, par * 2 + 1), e);
-    __threadfence();
-  }
-  __syncthreads();
+  wait_flag(c, flag_at(mine, kOffHaloFlag, par * 2 + 0), e);
+  wait_flag(c, flag_at(mine, kOffHaloFlag, par * 2 + 1), e);
+  __threadfence();
+}
+
+// inbox -> ghost planes (after k_halo_wait)
+__global__ void __launch_bounds__(kBlock)
+    k_halo_unpack(CommDev *c, HaloSet hs, int64_t nxl) {
+  const int64_t plane = c->plane;
+  const int par = (int)(vload(&c->halo_seq) & 1);
+  const double *inbox =
+      reinterpret_cast<const double *>(c->peer[c->rank] + kOffHalo);
   const int64_t per_side = (int64_t)hs.planes * plane;
   const int64_t total = 2 * per_side;
-  const double *inbox = reinterpret_cast<const double *>(mine + kOffHalo);
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int side = t >= per_side;  // 0: lo ghost, 1: hi ghost
@@ -168,9 +175,9 @@ int halo_exchange(const Plan &p, const HaloItem *items, int count,
   const int64_t total = 2 * planes * plane;
   const int g = (int)std::min<int64_t>(grid_for(total), p.num_sms * 4);
   launch(k_halo_put, g, kBlock, s, p.comm->dev, hs, p.d.n, p.comm->nxl);
-  // one wave: every CTA of the get spins on the flags at its start
-  const int gg = (int)std::min<int64_t>(grid_for(total), p.num_sms);
-  launch(k_halo_get, gg, kBlock, s, p.comm->dev, hs, p.comm->nxl);
+  launch(k_halo_wait, 1, 32, s, p.comm->dev);
+  const int gg = (int)std::min<int64_t>(grid_for(total), p.num_sms * 4);
+  launch(k_halo_unpack, gg, kBlock, s, p.comm->dev, hs, p.comm->nxl);
   PF_LAUNCH_CHECK("halo exchange");
   return PF_OK;
 }

@@ -20,8 +20,8 @@
 //    ranks, no floating-point atomics;
 //  * halo exchange: a put kernel stores the first / last owned plane of a
 //    set of arrays straight into the left / right neighbour's inbox and
-//    releases a flag; the get kernel waits for both flags and copies the
-//    inbox into the local ghost planes;
+//    releases a flag; a one-thread kernel waits for both flags, then the
+//    inbox is copied into the local ghost planes;
 //  * barrier (the spectral preconditioner's all-to-all transposes store /
 //    load peer spectra directly, separated by barriers).
 //
