@@ -427,7 +427,11 @@ def run_c5train(args, world, rank, local, dev):
     dt = cfl * (2 * np.pi / shape[0]) / float(state.u.abs().max())
     forcing = channel.WallForcing(dom, dev)
     torch.manual_seed(0)
-    model = les.SGSCorrector(shape, dom.box_layout()[1]).to(dev)
+    # the CNN corrector computes in float32 (cuDNN, tensor cores); the PISO
+    # step and its adjoint stay float64
+    torch.backends.cudnn.benchmark = True
+    model = les.SGSCorrector(shape, dom.box_layout()[1],
+                             dtype=torch.float32).to(dev)
     opt = torch.optim.SGD(model.parameters(), lr=1e-3)
     target = state.u[:, 0].reshape(shape).mean(dim=(0, 2)).detach()
     bc = torch.cat(list(state.bc), 0)
@@ -477,6 +481,8 @@ def run_c5train(args, world, rank, local, dev):
             "data": "synthetic (reichardt_init seed = rank)",
             "config": {"workload": desc, "grid": list(shape),
                        "cells_per_sample": dom.n, "unroll": UNROLL,
+                       "sgs_cnn_dtype": "f32 (PISO step and adjoint f64)",
+                       "loss": "statistics loss (S/stats.py:567-614)",
                        "samples": world, "parallelism": f"dp{world}",
                        "tol": args.tol,
                        "l2": "working set > L2 per unrolled step chain"},

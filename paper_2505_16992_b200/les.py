@@ -33,13 +33,18 @@ class SGSCorrector(torch.nn.Module):
     (n, 3): periodic padding along the periodic axes, replicate along the
     walls."""
 
-    def __init__(self, shape, periodic, width=8, scale=1e-3):
+    def __init__(self, shape, periodic, width=8, scale=1e-3,
+                 dtype=torch.float64):
         super().__init__()
         self.shape = tuple(shape)
         self.periodic = tuple(periodic)
         self.scale = scale
-        self.c1 = torch.nn.Conv3d(3, width, 3, dtype=torch.float64)
-        self.c2 = torch.nn.Conv3d(width, 3, 1, dtype=torch.float64)
+        # the corrector's own arithmetic type (float32 runs the convolutions
+        # on the tensor cores); its input and output stay float64, the type
+        # of the PISO step
+        self.dtype = dtype
+        self.c1 = torch.nn.Conv3d(3, width, 3, dtype=dtype)
+        self.c2 = torch.nn.Conv3d(width, 3, 1, dtype=dtype)
 
     def _pad(self, x):
         out = x
@@ -55,9 +60,9 @@ class SGSCorrector(torch.nn.Module):
         return out
 
     def forward(self, u):
-        x = u.t().reshape(1, 3, *self.shape)
+        x = u.t().reshape(1, 3, *self.shape).to(self.dtype)
         y = self.c2(torch.nn.functional.gelu(self.c1(self._pad(x))))
-        return self.scale * y.reshape(3, -1).t()
+        return self.scale * y.reshape(3, -1).t().to(u.dtype)
 
 
 def unrolled_loss(domain, u0, bc, model, forcing, nu, cfg, steps,
