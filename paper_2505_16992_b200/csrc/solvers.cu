@@ -777,7 +777,7 @@ __global__ void __launch_bounds__(kBlock)
 // prologue planes of a chunk, from L2), instead of once per stencil point.
 
 constexpr int kTZ = 32, kTY = 8, kTileThreads = kTZ * kTY;
-constexpr int kXChunk = 32;  // X planes per tile (fewer on small boxes)
+constexpr int kXChunk = 64;  // X planes per tile (fewer on small boxes)
 
 struct TileGeo {
   int32_t X, Y, Z;          // local box
