@@ -198,7 +198,7 @@ def workload_config(args, sample=False):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 100 ms by a reader
+    """nvidia-smi clocks / throttle reasons sampled every 250 ms by a reader
     thread.  start() returns once the first sample has arrived, so the
     sampler's own start-up (which touches the GPU) is outside the timed
     region; stop() keeps only the samples taken while the region ran."""
@@ -226,7 +226,8 @@ class ClockSampler:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}",
                  f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE,
+                 "-lms", os.environ.get("PF_CLOCK_MS", "250")],
+                stdout=subprocess.PIPE,
                 stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
