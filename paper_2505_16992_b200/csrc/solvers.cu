@@ -1573,7 +1573,14 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     if (!rc) rc = comm_check(pl, s);
     if (rc) return rc;
     if (hs.all_done || launched >= maxiter) break;
-    const int bsz = std::min(launched < 4 ? 2 : next_batch(launched, 0),
+    // first batch: the previous solve's lock-step count on this plan and
+    // direction (time steps change slowly), so a typical solve polls once
+    static const bool use_hint = getenv("PF_NO_HINT") == nullptr;
+    const int hint = use_hint ? pl.bi_hint[kTrans ? 1 : 0] : 0;
+    const int first = hint > 0 ? std::min(std::max(2, hint), 64) : 2;
+    const int bsz = std::min(launched == 0 ? first
+                             : launched < 4 ? 2
+                                            : next_batch(launched, 0),
                              maxiter - launched);
     for (int k = 0; k < bsz; ++k) {
       const int par = (launched + k) & 1;
@@ -1594,6 +1601,11 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     }
     PF_LAUNCH_CHECK("bicgstab iterations");
     launched += bsz;
+  }
+  {
+    int lock = 0;  // lock-step iterations this solve needed
+    for (int q = 0; q < ncomp; ++q) lock = std::max(lock, (int)hs.c[q].iter);
+    pl.bi_hint[kTrans ? 1 : 0] = lock;
   }
   launch(k_bi_finish, ge, kBlock, s, x, n, rg, st);
   halo(pl, s, {{x, ncomp}});
