@@ -132,9 +132,12 @@ __global__ void __launch_bounds__(kBlock)
     const Face fc = v.topo.face(cell, f);
     double off = 0.0;
     if (fc.nb >= 0) {
-      const double nbp =
-          v.A(fc.ax, fc.nb) * (c_is_a_inv ? c[fc.nb] : 1.0 / c[fc.nb]);
-      const double pf = 0.5 * (v.A(a, i) * ainv + nbp);
+      // explicit roundings (no FMA contraction): the coupling is then the
+      // same bits seen from either cell, P exactly symmetric
+      // (T/test_piso.py:44-53)
+      const double nbp = __dmul_rn(
+          v.A(fc.ax, fc.nb), (c_is_a_inv ? c[fc.nb] : 1.0 / c[fc.nb]));
+      const double pf = 0.5 * __dadd_rn(__dmul_rn(v.A(a, i), ainv), nbp);
       diag -= pf;
       off = -pf;
     }
