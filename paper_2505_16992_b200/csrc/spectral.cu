@@ -1,5 +1,6 @@
 // spectral.cu -- FFT / tridiagonal preconditioner (see spectral.cuh).
 #include <algorithm>
+#include <cstdlib>
 
 #include "mg.cuh"
 #include "spectral.cuh"
@@ -9,6 +10,7 @@ namespace pf {
 constexpr int kFftThreads = 256;
 constexpr int kFftElems = 1024;  // complex elements per CTA buffer (16 KB)
 constexpr int kYThreads = 128;
+constexpr int kMaxLines = 2 * kFftElems / 4;  // real Z lines per tile (N >= 4)
 
 #define SPEC_DONE_RETURN \
   if (done && *done) return
@@ -33,8 +35,8 @@ __device__ __forceinline__ double2 twiddle(const double2 *tw, int k) {
 // Shared-memory layout of a line: element i sits at pad(i) = i + i / 16, so
 // the power-of-two strides of the butterflies spread over the banks (one
 // 16-byte pad slot per 16 elements; line stride padded_len(N)).
-__host__ __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
-__host__ __device__ __forceinline__ int padded_len(int n) {
+__host__ __device__ constexpr int pad(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int padded_len(int n) {
   return n + (n >> 4);
 }
 
@@ -45,14 +47,14 @@ __host__ __device__ __forceinline__ int padded_len(int n) {
 template <bool kInv>
 __device__ double2 *fft_lines(double2 *a, double2 *b, int N, int nl,
                               const double2 *tw) {
-  const int q4 = N >> 2;
+  const int q4 = N >> 2, lg = __ffs(N) - 1;
   const int NP = padded_len(N);
   int n = N, ls = 0;  // current length, log2 of the stride
   while (n >= 4) {
     const int n1 = n >> 2, s = 1 << ls;
     for (int t = threadIdx.x; t < nl * q4; t += blockDim.x) {
-      const int line = t / q4;
-      const int k = t - line * q4;
+      const int line = t >> (lg - 2);
+      const int k = t & (q4 - 1);
       const int q = k & (s - 1), p = k >> ls;
       const double2 *x = a + line * NP;
       double2 *y = b + line * NP;
@@ -82,8 +84,8 @@ __device__ double2 *fft_lines(double2 *a, double2 *b, int N, int nl,
   if (n == 2) {
     const int s = N >> 1;
     for (int t = threadIdx.x; t < nl * s; t += blockDim.x) {
-      const int line = t / s;
-      const int q = t - line * s;
+      const int line = t >> (lg - 1);
+      const int q = t & (s - 1);
       const double2 *x = a + line * NP;
       double2 *y = b + line * NP;
       const double2 x0 = x[pad(q)], x1 = x[pad(q + s)];
@@ -96,11 +98,25 @@ __device__ double2 *fft_lines(double2 *a, double2 *b, int N, int nl,
   return a;
 }
 
-// first element of the owned Z line number l (lines enumerated X fastest,
-// then Y; slab plans skip the ghost plane at local X = 0)
-__device__ __forceinline__ int64_t zline_base(const SpecPlan &sp, int64_t l) {
-  const int64_t x = l % sp.nxl, y = l / sp.nxl;
-  return ((x + sp.xoff) * sp.sy + y) * sp.sz;
+// The Z passes handle the real Z lines l0 .. l0 + 2 LP - 1 of a tile (lines
+// enumerated X fastest, then Y; slab plans skip the ghost plane at local
+// X = 0).  Their first elements and (x, y) are tabulated once per tile, so
+// the element loops carry no integer division.
+struct ZLines {
+  int32_t base[kMaxLines];
+  int32_t x[kMaxLines], y[kMaxLines];
+};
+
+__device__ __forceinline__ void zlines_fill(const SpecPlan &sp, int32_t l0,
+                                            int nl, ZLines &t) {
+  const int32_t last = sp.nxl * sp.sy - 1;
+  for (int j = threadIdx.x; j < nl; j += blockDim.x) {
+    const int32_t l = min(l0 + j, last);
+    const int32_t x = l % sp.nxl, y = l / sp.nxl;
+    t.base[j] = ((x + sp.xoff) * sp.sy + y) * sp.sz;
+    t.x[j] = x;
+    t.y[j] = y;
+  }
 }
 
 // rank holding wavenumber kz of the transposed spectrum
@@ -110,14 +126,15 @@ __device__ __forceinline__ int kz_owner(const SpecPlan &sp, int kz) {
   return q;
 }
 
-// address of (line l, wavenumber kz) in the owner's transposed spectrum
-// (Y, kz - kz0[q], global X): a peer address when another rank owns kz
-__device__ __forceinline__ double2 *spec_at(const SpecPlan &sp, int64_t l,
-                                            int kz) {
-  const int64_t x = l % sp.nxl, y = l / sp.nxl;
+// address of (line (x, y), wavenumber kz) in the owner's transposed
+// spectrum (Y, kz - kz0[q], global X): a peer address when another rank
+// owns kz
+__device__ __forceinline__ double2 *spec_at(const SpecPlan &sp, int32_t x,
+                                            int32_t y, int kz) {
   const int q = kz_owner(sp, kz);
   const int nkq = sp.kz0[q + 1] - sp.kz0[q];
-  return sp.peer_s[q] + (y * nkq + (kz - sp.kz0[q])) * sp.sx + sp.x0 + x;
+  return sp.peer_s[q] + ((int64_t)y * nkq + (kz - sp.kz0[q])) * sp.sx +
+         sp.x0 + x;
 }
 
 // pass 1: real FFT along Z, two real lines per complex transform
@@ -125,28 +142,30 @@ __global__ void __launch_bounds__(kFftThreads)
     k_spec_fwd_z(SpecPlan sp, const double *__restrict__ r, const int *done) {
   SPEC_DONE_RETURN;
   extern __shared__ double2 sm[];
+  __shared__ ZLines zl;
   const int N = sp.sz, LP = sp.lpz, nk = sp.nkz, NP = padded_len(N);
-  const int64_t npairs = (int64_t)sp.nxl * sp.sy / 2;
-  const int64_t ntiles = (npairs + LP - 1) / LP;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t g0 = tile * LP;
+  const int lg = __ffs(N) - 1, lg2p = __ffs(2 * LP) - 1;
+  const int32_t npairs = sp.nxl * sp.sy / 2;
+  const int32_t ntiles = (npairs + LP - 1) / LP;
+  for (int32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int32_t g0 = tile * LP;
+    zlines_fill(sp, 2 * g0, 2 * LP, zl);
+    __syncthreads();
     for (int e = threadIdx.x; e < LP * N; e += blockDim.x) {
-      const int j = e / N, z = e - j * N;
-      const int64_t g = g0 + j;
+      const int j = e >> lg, z = e & (N - 1);
       double2 v = make_double2(0.0, 0.0);
-      if (g < npairs) {
-        v.x = r[zline_base(sp, 2 * g) + z];
-        v.y = r[zline_base(sp, 2 * g + 1) + z];
+      if (g0 + j < npairs) {
+        v.x = r[zl.base[2 * j] + z];
+        v.y = r[zl.base[2 * j + 1] + z];
       }
       sm[j * NP + pad(z)] = v;
     }
     __syncthreads();
     const double2 *f = fft_lines<false>(sm, sm + LP * NP, N, LP, sp.twz);
     for (int e = threadIdx.x; e < 2 * LP * nk; e += blockDim.x) {
-      const int kz = e / (2 * LP), jj = e - kz * 2 * LP;
+      const int kz = e >> lg2p, jj = e & (2 * LP - 1);
       const int j = jj >> 1, side = jj & 1;
-      const int64_t g = g0 + j;
-      if (g >= npairs) continue;
+      if (g0 + j >= npairs) continue;
       const double2 zk = f[j * NP + pad(kz)];
       const double2 zm = f[j * NP + pad((N - kz) & (N - 1))];
       // Z = A + iB with A, B the transforms of the two real lines
@@ -155,7 +174,7 @@ __global__ void __launch_bounds__(kFftThreads)
                     : make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
       // slab plans: the transpose to the kz owner happens here, as a
       // store into the peer's spectrum over NVLink
-      *spec_at(sp, 2 * g + side, kz) = o;
+      *spec_at(sp, zl.x[jj], zl.y[jj], kz) = o;
     }
     __syncthreads();
   }
@@ -167,7 +186,7 @@ __global__ void __launch_bounds__(kFftThreads)
     k_spec_x(SpecPlan sp, const int *done) {
   SPEC_DONE_RETURN;
   extern __shared__ double2 sm[];
-  const int N = sp.sx, LP = sp.lpx, NP = padded_len(N);
+  const int N = sp.sx, LP = sp.lpx, NP = padded_len(N), lg = __ffs(N) - 1;
   const int64_t nlines =
       (int64_t)sp.sy * (sp.kz0[sp.rank + 1] - sp.kz0[sp.rank]);
   const int64_t ntiles = (nlines + LP - 1) / LP;
@@ -176,14 +195,14 @@ __global__ void __launch_bounds__(kFftThreads)
     const int64_t nl = nlines - l0 < LP ? nlines - l0 : LP;
     double2 *src = sp.s + l0 * N;
     for (int e = threadIdx.x; e < LP * N; e += blockDim.x) {
-      const int ln = e / N, xx = e - ln * N;
+      const int ln = e >> lg, xx = e & (N - 1);
       sm[ln * NP + pad(xx)] =
           e < nl * N ? __ldcg(src + e) : make_double2(0.0, 0.0);
     }
     __syncthreads();
     const double2 *f = fft_lines<kInv>(sm, sm + LP * NP, N, LP, sp.twx);
     for (int e = threadIdx.x; e < nl * N; e += blockDim.x) {
-      const int ln = e / N, xx = e - ln * N;
+      const int ln = e >> lg, xx = e & (N - 1);
       src[e] = f[ln * NP + pad(xx)];
     }
     __syncthreads();
@@ -220,7 +239,7 @@ __global__ void __launch_bounds__(kYThreads)
   const double scale = 1.0 / ((double)sp.sx * sp.sz);
   double *sv = reinterpret_cast<double *>(sp.s);
   const int64_t ystride = 2 * ncol;
-  constexpr int C = 8;
+  constexpr int C = 16;
   if (active) {
     double dp = 0.0, cprev = 0.0;
     for (int y0 = 0; y0 < sy; y0 += C) {
@@ -280,21 +299,26 @@ __global__ void __launch_bounds__(kFftThreads)
                  double *__restrict__ z, CgFuse fz, const int *done) {
   SPEC_DONE_RETURN;
   extern __shared__ double2 sm[];
+  __shared__ ZLines zl;
   const int N = sp.sz, LP = sp.lpz, half = N >> 1, NP = padded_len(N);
-  const int64_t npairs = (int64_t)sp.nxl * sp.sy / 2;
-  const int64_t ntiles = (npairs + LP - 1) / LP;
+  const int lg = __ffs(N) - 1, lgp = __ffs(LP) - 1;
+  const int32_t npairs = sp.nxl * sp.sy / 2;
+  const int32_t ntiles = (npairs + LP - 1) / LP;
   double sums[3] = {0.0, 0.0, 0.0};
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t g0 = tile * LP;
+  for (int32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int32_t g0 = tile * LP;
+    zlines_fill(sp, 2 * g0, 2 * LP, zl);
+    __syncthreads();
     for (int e = threadIdx.x; e < LP * N; e += blockDim.x) {
-      const int k = e / LP, j = e - k * LP;
-      const int64_t g = g0 + j;
+      const int k = e >> lgp, j = e & (LP - 1);
       double2 v = make_double2(0.0, 0.0);
-      if (g < npairs) {
+      if (g0 + j < npairs) {
         const int kk = k <= half ? k : N - k;
         // slab plans: the inverse transpose, loads from the kz owner
-        const double2 a = __ldcg(spec_at(sp, 2 * g, kk));
-        const double2 b = __ldcg(spec_at(sp, 2 * g + 1, kk));
+        const double2 a =
+            __ldcg(spec_at(sp, zl.x[2 * j], zl.y[2 * j], kk));
+        const double2 b =
+            __ldcg(spec_at(sp, zl.x[2 * j + 1], zl.y[2 * j + 1], kk));
         v = k <= half ? make_double2(a.x - b.y, a.y + b.x)
                       : make_double2(a.x + b.y, b.x - a.y);
       }
@@ -303,12 +327,11 @@ __global__ void __launch_bounds__(kFftThreads)
     __syncthreads();
     const double2 *f = fft_lines<true>(sm, sm + LP * NP, N, LP, sp.twz);
     for (int e = threadIdx.x; e < LP * N; e += blockDim.x) {
-      const int j = e / N, zz = e - j * N;
-      const int64_t g = g0 + j;
-      if (g >= npairs) continue;
+      const int j = e >> lg, zz = e & (N - 1);
+      if (g0 + j >= npairs) continue;
       const double2 v = f[j * NP + pad(zz)];
-      const int64_t i0 = zline_base(sp, 2 * g) + zz;
-      const int64_t i1 = zline_base(sp, 2 * g + 1) + zz;
+      const int32_t i0 = zl.base[2 * j] + zz;
+      const int32_t i1 = zl.base[2 * j + 1] + zz;
       z[i0] = v.x;
       z[i1] = v.y;
       if (kSums) {
@@ -316,6 +339,238 @@ __global__ void __launch_bounds__(kFftThreads)
         sums[0] += v.x + v.y;
         sums[1] += r0 * v.x + r1 * v.y;
         sums[2] += r0 + r1;
+      }
+    }
+    __syncthreads();
+  }
+  if (kSums) {
+    double tot[3];
+    if (grid_reduce<3>(sums, fz.partials, fz.counter, tot))
+      cg_fin_z(fz.st, tot[0], tot[1], tot[2], sp.sx * sp.sy * sp.sz,
+               fz.initial != 0);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Length-256 transforms (the channel's X and Z): four-step FFT 256 = 16 x 16
+// in registers.  A line is owned by 16 threads; thread c holds x[16 n1 + c],
+// transforms over n1 in registers (radix 4 x 4), applies W256^(c k1),
+// exchanges through one padded shared-memory transpose, and transforms over
+// n2.  Two shared-memory passes per transform instead of the Stockham
+// kernel's eight, no per-butterfly twiddle loads, and 16 independent loads
+// in flight per thread.
+
+constexpr int kR = 16, kN16 = kR * kR;
+constexpr int kL16 = 8;             // complex lines per CTA
+constexpr int kT16 = kL16 * kR;     // threads per CTA
+constexpr int kLP16 = padded_len(kN16);  // natural-order line stride (272)
+
+struct Spec16Smem {
+  double2 tw[kN16];
+  // transpose [line][n2][k1] (row stride 17: conflict-free both ways),
+  // reused as natural-order lines [line][pad(k)] (8 * 272 == 8 * 16 * 17)
+  double2 t[kL16][kR][kR + 1];
+  ZLines zl;
+};
+static_assert(kL16 * kLP16 == kL16 * kR * (kR + 1), "buffer reuse");
+
+__device__ __forceinline__ double2 *nat16(Spec16Smem &sm, int line) {
+  return &sm.t[0][0][0] + line * kLP16;
+}
+
+template <bool kInv>
+__device__ __forceinline__ void fft4(double2 &a0, double2 &a1, double2 &a2,
+                                     double2 &a3) {
+  const double2 s02 = cadd(a0, a2), d02 = csub(a0, a2);
+  const double2 s13 = cadd(a1, a3), d13 = csub(a1, a3);
+  // forward: -i d13; inverse: +i d13
+  const double2 jd = kInv ? make_double2(-d13.y, d13.x)
+                          : make_double2(d13.y, -d13.x);
+  a0 = cadd(s02, s13);
+  a2 = csub(s02, s13);
+  a1 = cadd(d02, jd);
+  a3 = csub(d02, jd);
+}
+
+// exp(-+ 2 pi i p / 16), p = j1 m2 in 0 .. 9
+template <bool kInv>
+__device__ __forceinline__ double2 w16(int p) {
+  constexpr double c1 = 0.92387953251128673848, s1 = 0.38268343236508978178;
+  constexpr double h = 0.70710678118654752440;
+  const double cs[10] = {1.0, c1, h, s1, 0.0, -s1, -h, -c1, -1.0, -c1};
+  const double sn[10] = {0.0, s1, h, c1, 1.0, c1, h, s1, 0.0, -s1};
+  return make_double2(cs[p], kInv ? sn[p] : -sn[p]);
+}
+
+// 16-point DFT in registers; X[k] ends in v[4 (k & 3) + (k >> 2)]
+template <bool kInv>
+__device__ __forceinline__ void fft16(double2 (&v)[kR]) {
+#pragma unroll
+  for (int m2 = 0; m2 < 4; ++m2) fft4<kInv>(v[m2], v[4 + m2], v[8 + m2], v[12 + m2]);
+#pragma unroll
+  for (int j1 = 1; j1 < 4; ++j1)
+#pragma unroll
+    for (int m2 = 1; m2 < 4; ++m2)
+      v[4 * j1 + m2] = cmul(v[4 * j1 + m2], w16<kInv>(j1 * m2));
+#pragma unroll
+  for (int j1 = 0; j1 < 4; ++j1)
+    fft4<kInv>(v[4 * j1], v[4 * j1 + 1], v[4 * j1 + 2], v[4 * j1 + 3]);
+}
+__device__ __forceinline__ int perm16(int k) { return 4 * (k & 3) + (k >> 2); }
+
+// v (thread c's x[16 n1 + c]) -> u (X[c + 16 k2] at u[perm16(k2)]); the
+// transpose buffer of `line` is free on entry and on exit
+template <bool kInv>
+__device__ __forceinline__ void fft256(Spec16Smem &sm, int line, int c,
+                                       double2 (&v)[kR]) {
+  fft16<kInv>(v);
+#pragma unroll
+  for (int k1 = 0; k1 < kR; ++k1) {
+    double2 y = v[perm16(k1)];
+    if (k1) {
+      double2 w = sm.tw[(c * k1) & (kN16 - 1)];  // shared: no __ldg
+      if (kInv) w.y = -w.y;
+      y = cmul(y, w);
+    }
+    sm.t[line][c][k1] = y;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int n2 = 0; n2 < kR; ++n2) v[n2] = sm.t[line][n2][c];
+  fft16<kInv>(v);
+}
+
+__device__ __forceinline__ void load_tw16(Spec16Smem &sm, const double2 *tw) {
+  for (int t = threadIdx.x; t < kN16; t += blockDim.x) sm.tw[t] = tw[t];
+}
+
+// pass 1 for sz == 256 (same output as k_spec_fwd_z)
+__global__ void __launch_bounds__(kT16)
+    k_spec_fwd_z16(SpecPlan sp, const double *__restrict__ r,
+                   const int *done) {
+  SPEC_DONE_RETURN;
+  __shared__ Spec16Smem sm;
+  load_tw16(sm, sp.twz);
+  const int line = threadIdx.x >> 4, c = threadIdx.x & (kR - 1);
+  const int nk = sp.nkz;
+  const int32_t npairs = sp.nxl * sp.sy / 2;
+  const int32_t ntiles = (npairs + kL16 - 1) / kL16;
+  for (int32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int32_t g0 = tile * kL16;
+    zlines_fill(sp, 2 * g0, 2 * kL16, sm.zl);
+    __syncthreads();
+    double2 v[kR];
+    const bool ok = g0 + line < npairs;
+    const int32_t b0 = sm.zl.base[2 * line], b1 = sm.zl.base[2 * line + 1];
+#pragma unroll
+    for (int n1 = 0; n1 < kR; ++n1)
+      v[n1] = ok ? make_double2(r[b0 + kR * n1 + c], r[b1 + kR * n1 + c])
+                 : make_double2(0.0, 0.0);
+    fft256<false>(sm, line, c, v);
+    __syncthreads();  // every transpose read is done: reuse as natural order
+    double2 *zb = nat16(sm, line);
+#pragma unroll
+    for (int k2 = 0; k2 < kR; ++k2) zb[pad(c + kR * k2)] = v[perm16(k2)];
+    __syncthreads();
+    for (int e = threadIdx.x; e < 2 * kL16 * nk; e += blockDim.x) {
+      const int kz = e >> 4, jj = e & (2 * kL16 - 1);
+      const int j = jj >> 1, side = jj & 1;
+      if (g0 + j >= npairs) continue;
+      const double2 *f = nat16(sm, j);
+      const double2 zk = f[pad(kz)];
+      const double2 zm = f[pad((kN16 - kz) & (kN16 - 1))];
+      const double2 o =
+          side == 0 ? make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y))
+                    : make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+      *spec_at(sp, sm.zl.x[jj], sm.zl.y[jj], kz) = o;
+    }
+    __syncthreads();
+  }
+}
+
+// passes 2 / 4 for sx == 256: complex FFT along X, in place
+template <bool kInv>
+__global__ void __launch_bounds__(kT16)
+    k_spec_x16(SpecPlan sp, const int *done) {
+  SPEC_DONE_RETURN;
+  __shared__ Spec16Smem sm;
+  load_tw16(sm, sp.twx);
+  const int line = threadIdx.x >> 4, c = threadIdx.x & (kR - 1);
+  const int64_t nlines =
+      (int64_t)sp.sy * (sp.kz0[sp.rank + 1] - sp.kz0[sp.rank]);
+  const int64_t ntiles = (nlines + kL16 - 1) / kL16;
+  __syncthreads();
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t l = tile * kL16 + line;
+    const bool ok = l < nlines;
+    double2 *src = sp.s + l * kN16;
+    double2 v[kR];
+#pragma unroll
+    for (int n1 = 0; n1 < kR; ++n1)
+      v[n1] = ok ? __ldcg(src + kR * n1 + c) : make_double2(0.0, 0.0);
+    fft256<kInv>(sm, line, c, v);
+    if (ok) {
+#pragma unroll
+      for (int k2 = 0; k2 < kR; ++k2) src[c + kR * k2] = v[perm16(k2)];
+    }
+    __syncthreads();  // the transpose buffer is free for the next tile
+  }
+}
+
+// pass 5 for sz == 256 (same output as k_spec_inv_z)
+template <bool kSums>
+__global__ void __launch_bounds__(kT16)
+    k_spec_inv_z16(SpecPlan sp, const double *__restrict__ r,
+                   double *__restrict__ z, CgFuse fz, const int *done) {
+  SPEC_DONE_RETURN;
+  __shared__ Spec16Smem sm;
+  load_tw16(sm, sp.twz);
+  const int line = threadIdx.x >> 4, c = threadIdx.x & (kR - 1);
+  constexpr int half = kN16 / 2;
+  const int32_t npairs = sp.nxl * sp.sy / 2;
+  const int32_t ntiles = (npairs + kL16 - 1) / kL16;
+  double sums[3] = {0.0, 0.0, 0.0};
+  for (int32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int32_t g0 = tile * kL16;
+    zlines_fill(sp, 2 * g0, 2 * kL16, sm.zl);
+    __syncthreads();
+    // Hermitian extension of the two real lines' spectra, loaded with the
+    // lines of the tile adjacent (coalesced), into natural order
+    for (int e = threadIdx.x; e < kL16 * kN16; e += blockDim.x) {
+      const int k = e >> 3, j = e & (kL16 - 1);
+      double2 v = make_double2(0.0, 0.0);
+      if (g0 + j < npairs) {
+        const int kk = k <= half ? k : kN16 - k;
+        const double2 a =
+            __ldcg(spec_at(sp, sm.zl.x[2 * j], sm.zl.y[2 * j], kk));
+        const double2 b =
+            __ldcg(spec_at(sp, sm.zl.x[2 * j + 1], sm.zl.y[2 * j + 1], kk));
+        v = k <= half ? make_double2(a.x - b.y, a.y + b.x)
+                      : make_double2(a.x + b.y, b.x - a.y);
+      }
+      nat16(sm, j)[pad(k)] = v;
+    }
+    __syncthreads();
+    double2 v[kR];
+    const double2 *zb = nat16(sm, line);
+#pragma unroll
+    for (int n1 = 0; n1 < kR; ++n1) v[n1] = zb[pad(kR * n1 + c)];
+    __syncthreads();  // natural-order reads done: the buffer is the transpose
+    fft256<true>(sm, line, c, v);
+    if (g0 + line < npairs) {
+      const int32_t b0 = sm.zl.base[2 * line], b1 = sm.zl.base[2 * line + 1];
+#pragma unroll
+      for (int k2 = 0; k2 < kR; ++k2) {
+        const double2 o = v[perm16(k2)];
+        const int32_t i0 = b0 + c + kR * k2, i1 = b1 + c + kR * k2;
+        z[i0] = o.x;
+        z[i1] = o.y;
+        if (kSums) {
+          const double r0 = r[i0], r1 = r[i1];
+          sums[0] += o.x + o.y;
+          sums[1] += r0 * o.x + r1 * o.y;
+          sums[2] += r0 + r1;
+        }
       }
     }
     __syncthreads();
@@ -380,6 +635,12 @@ __global__ void __launch_bounds__(kBlock) k_spec_plane_mean(SpecPlan sp) {
 static bool pow2_in(int n, int lo, int hi) {
   return n >= lo && n <= hi && (n & (n - 1)) == 0;
 }
+
+// PF_SPEC_GENERIC=1: the Stockham kernels for every length (comparison)
+static const bool g_spec_generic = [] {
+  const char *e = getenv("PF_SPEC_GENERIC");
+  return e && e[0] == '1';
+}();
 
 bool spec_ok(int dim, int sx, int sy, int sz, int px, int pz) {
   if (!pz || !pow2_in(sz, 4, kFftElems) || sy < 2) return false;
@@ -523,25 +784,46 @@ int spec_apply(const MgLevel &l0, const SpecPlan &sp, const double *r,
   const size_t xsm = 2 * sizeof(double2) * sp.lpx * padded_len(sp.sx);
   const int64_t ncol2 = 2 * (int64_t)nkl * sp.sx;
   mark(0);
-  launch_smem(k_spec_fwd_z, zt, kFftThreads, zsm, s, sp, r, done);
+  const bool z16 = sp.sz == kN16 && !g_spec_generic;
+  const bool x16 = sp.sx == kN16 && !g_spec_generic;
+  const int zt16 = (int)std::min<int64_t>((npairs + kL16 - 1) / kL16, 1 << 20);
+  const int xt16 = (int)std::min<int64_t>((xlines + kL16 - 1) / kL16, 1 << 20);
+  if (z16)
+    launch(k_spec_fwd_z16, zt16, kT16, s, sp, r, done);
+  else
+    launch_smem(k_spec_fwd_z, zt, kFftThreads, zsm, s, sp, r, done);
   barrier();
   mark(1);
-  if (sp.sx > 1) launch_smem(k_spec_x<false>, xt, kFftThreads, xsm, s, sp, done);
+  if (x16)
+    launch(k_spec_x16<false>, xt16, kT16, s, sp, done);
+  else if (sp.sx > 1)
+    launch_smem(k_spec_x<false>, xt, kFftThreads, xsm, s, sp, done);
   mark(2);
   launch_smem(k_spec_ysolve, grid_for(ncol2, kYThreads), kYThreads,
               3 * sizeof(double) * sp.sy, s, sp, done);
   mark(3);
-  if (sp.sx > 1) launch_smem(k_spec_x<true>, xt, kFftThreads, xsm, s, sp, done);
+  if (x16)
+    launch(k_spec_x16<true>, xt16, kT16, s, sp, done);
+  else if (sp.sx > 1)
+    launch_smem(k_spec_x<true>, xt, kFftThreads, xsm, s, sp, done);
   barrier();
   mark(4);
   if (fuse && fuse->st) {
     // the fused z-sums end in a cross-rank allreduce, which no rank leaves
     // before every rank's loads are done: it doubles as the closing barrier
-    launch_smem(k_spec_inv_z<true>, std::min(zt, red_blocks), kFftThreads,
-                zsm, s, sp, r, z, *fuse, done);
+    if (z16)
+      launch(k_spec_inv_z16<true>, std::min(zt16, red_blocks), kT16, s, sp, r,
+             z, *fuse, done);
+    else
+      launch_smem(k_spec_inv_z<true>, std::min(zt, red_blocks), kFftThreads,
+                  zsm, s, sp, r, z, *fuse, done);
   } else {
-    launch_smem(k_spec_inv_z<false>, zt, kFftThreads, zsm, s, sp, r, z,
-                CgFuse{nullptr, nullptr, nullptr, 0}, done);
+    if (z16)
+      launch(k_spec_inv_z16<false>, zt16, kT16, s, sp, r, z,
+             CgFuse{nullptr, nullptr, nullptr, 0}, done);
+    else
+      launch_smem(k_spec_inv_z<false>, zt, kFftThreads, zsm, s, sp, r, z,
+                  CgFuse{nullptr, nullptr, nullptr, 0}, done);
     barrier();
   }
   mark(5);

@@ -229,6 +229,13 @@ SPECTRAL_DOMAINS = {
     "channel_wide": lambda: __import__("paper_2505_16992_b200.mesh",
                                        fromlist=["m"])
     .make_channel((4, 16, 64), ratio=1.05),
+    # length-256 X / Z: the register four-step FFT kernels
+    "channel_z256": lambda: __import__("paper_2505_16992_b200.mesh",
+                                       fromlist=["m"])
+    .make_channel((4, 8, 256), ratio=1.1),
+    "channel_x256": lambda: __import__("paper_2505_16992_b200.mesh",
+                                       fromlist=["m"])
+    .make_channel((256, 6, 8), ratio=1.1),
 }
 
 
