@@ -136,6 +136,14 @@ __device__ __forceinline__ double2 *spec_at(const SpecPlan &sp, int32_t x,
   return sp.peer_s[q] + ((int64_t)y * nkq + (kz - sp.kz0[q])) * sp.sx +
          sp.x0 + x;
 }
+// one GPU: every wavenumber is local (no owner search, so the loads of an
+// unrolled loop issue back to back)
+template <bool kSlab>
+__device__ __forceinline__ double2 *spec_at_t(const SpecPlan &sp, int32_t x,
+                                              int32_t y, int kz) {
+  if (kSlab) return spec_at(sp, x, y, kz);
+  return sp.s + ((int64_t)y * sp.nkz + kz) * sp.sx + x;
+}
 
 // pass 1: real FFT along Z, two real lines per complex transform
 __global__ void __launch_bounds__(kFftThreads)
@@ -363,19 +371,23 @@ __global__ void __launch_bounds__(kFftThreads)
 constexpr int kR = 16, kN16 = kR * kR;
 constexpr int kL16 = 8;             // complex lines per CTA
 constexpr int kT16 = kL16 * kR;     // threads per CTA
-constexpr int kLP16 = padded_len(kN16);  // natural-order line stride (272)
+// natural-order line stride: padded_len(256) + 1, odd in 16-byte units so
+// the 8 lines of a tile read at one wavenumber fall in distinct banks
+constexpr int kLP16 = padded_len(kN16) + 1;
 
 struct Spec16Smem {
   double2 tw[kN16];
   // transpose [line][n2][k1] (row stride 17: conflict-free both ways),
-  // reused as natural-order lines [line][pad(k)] (8 * 272 == 8 * 16 * 17)
-  double2 t[kL16][kR][kR + 1];
+  // reused as natural-order lines [line][pad(k)]
+  union {
+    double2 t[kL16][kR][kR + 1];
+    double2 nat[kL16 * kLP16];
+  };
   ZLines zl;
 };
-static_assert(kL16 * kLP16 == kL16 * kR * (kR + 1), "buffer reuse");
 
 __device__ __forceinline__ double2 *nat16(Spec16Smem &sm, int line) {
-  return &sm.t[0][0][0] + line * kLP16;
+  return sm.nat + line * kLP16;
 }
 
 template <bool kInv>
@@ -445,6 +457,7 @@ __device__ __forceinline__ void load_tw16(Spec16Smem &sm, const double2 *tw) {
 }
 
 // pass 1 for sz == 256 (same output as k_spec_fwd_z)
+template <bool kSlab>
 __global__ void __launch_bounds__(kT16)
     k_spec_fwd_z16(SpecPlan sp, const double *__restrict__ r,
                    const int *done) {
@@ -472,17 +485,28 @@ __global__ void __launch_bounds__(kT16)
 #pragma unroll
     for (int k2 = 0; k2 < kR; ++k2) zb[pad(c + kR * k2)] = v[perm16(k2)];
     __syncthreads();
-    for (int e = threadIdx.x; e < 2 * kL16 * nk; e += blockDim.x) {
-      const int kz = e >> 4, jj = e & (2 * kL16 - 1);
+    {
+      // thread: real line jj of the tile, wavenumbers kz0, kz0 + 8, ...
+      const int jj = threadIdx.x & (2 * kL16 - 1), kz0 = threadIdx.x >> 4;
       const int j = jj >> 1, side = jj & 1;
-      if (g0 + j >= npairs) continue;
+      const int32_t lx = sm.zl.x[jj], ly = sm.zl.y[jj];
+      double2 *dst = sp.s + (int64_t)ly * nk * sp.sx + lx;
       const double2 *f = nat16(sm, j);
-      const double2 zk = f[pad(kz)];
-      const double2 zm = f[pad((kN16 - kz) & (kN16 - 1))];
-      const double2 o =
-          side == 0 ? make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y))
-                    : make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
-      *spec_at(sp, sm.zl.x[jj], sm.zl.y[jj], kz) = o;
+      if (g0 + j < npairs) {
+#pragma unroll 4
+        for (int kz = kz0; kz < nk; kz += kT16 / (2 * kL16)) {
+          const double2 zk = f[pad(kz)];
+          const double2 zm = f[pad((kN16 - kz) & (kN16 - 1))];
+          const double2 o =
+              side == 0
+                  ? make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y))
+                  : make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+          if (kSlab)
+            *spec_at(sp, lx, ly, kz) = o;
+          else
+            dst[(int64_t)kz * sp.sx] = o;
+        }
+      }
     }
     __syncthreads();
   }
@@ -518,8 +542,8 @@ __global__ void __launch_bounds__(kT16)
 }
 
 // pass 5 for sz == 256 (same output as k_spec_inv_z)
-template <bool kSums>
-__global__ void __launch_bounds__(kT16)
+template <bool kSums, bool kSlab>
+__global__ void __launch_bounds__(kT16, 4)
     k_spec_inv_z16(SpecPlan sp, const double *__restrict__ r,
                    double *__restrict__ z, CgFuse fz, const int *done) {
   SPEC_DONE_RETURN;
@@ -536,19 +560,41 @@ __global__ void __launch_bounds__(kT16)
     __syncthreads();
     // Hermitian extension of the two real lines' spectra, loaded with the
     // lines of the tile adjacent (coalesced), into natural order
-    for (int e = threadIdx.x; e < kL16 * kN16; e += blockDim.x) {
-      const int k = e >> 3, j = e & (kL16 - 1);
-      double2 v = make_double2(0.0, 0.0);
-      if (g0 + j < npairs) {
-        const int kk = k <= half ? k : kN16 - k;
-        const double2 a =
-            __ldcg(spec_at(sp, sm.zl.x[2 * j], sm.zl.y[2 * j], kk));
-        const double2 b =
-            __ldcg(spec_at(sp, sm.zl.x[2 * j + 1], sm.zl.y[2 * j + 1], kk));
-        v = k <= half ? make_double2(a.x - b.y, a.y + b.x)
-                      : make_double2(a.x + b.y, b.x - a.y);
+    {
+      // thread: line pair j of the tile, wavenumbers k0, k0 + 16, ...; the
+      // loads of a half are issued back to back (lines are clamped, so
+      // every address is valid).  Slab plans: the inverse transpose, loads
+      // from the kz owner.
+      const int j = threadIdx.x & (kL16 - 1), k0 = threadIdx.x >> 3;
+      constexpr int kStep = kT16 / kL16, kH = kN16 / kStep / 2;
+      const bool okj = g0 + j < npairs;
+      const int32_t xa = sm.zl.x[2 * j], ya = sm.zl.y[2 * j];
+      const int32_t xb = sm.zl.x[2 * j + 1], yb = sm.zl.y[2 * j + 1];
+      const double2 *pa = sp.s + (int64_t)ya * sp.nkz * sp.sx + xa;
+      const double2 *pb = sp.s + (int64_t)yb * sp.nkz * sp.sx + xb;
+      double2 *dst = nat16(sm, j);
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        double2 av[kH], bv[kH];
+#pragma unroll
+        for (int i = 0; i < kH; ++i) {
+          const int k = k0 + kStep * (hh * kH + i);
+          const int kk = k <= half ? k : kN16 - k;
+          av[i] = __ldcg(kSlab ? spec_at(sp, xa, ya, kk)
+                               : pa + (int64_t)kk * sp.sx);
+          bv[i] = __ldcg(kSlab ? spec_at(sp, xb, yb, kk)
+                               : pb + (int64_t)kk * sp.sx);
+        }
+#pragma unroll
+        for (int i = 0; i < kH; ++i) {
+          const int k = k0 + kStep * (hh * kH + i);
+          const double2 a = av[i], b = bv[i];
+          double2 v = k <= half ? make_double2(a.x - b.y, a.y + b.x)
+                                : make_double2(a.x + b.y, b.x - a.y);
+          if (!okj) v = make_double2(0.0, 0.0);
+          dst[pad(k)] = v;
+        }
       }
-      nat16(sm, j)[pad(k)] = v;
     }
     __syncthreads();
     double2 v[kR];
@@ -788,8 +834,11 @@ int spec_apply(const MgLevel &l0, const SpecPlan &sp, const double *r,
   const bool x16 = sp.sx == kN16 && !g_spec_generic;
   const int zt16 = (int)std::min<int64_t>((npairs + kL16 - 1) / kL16, 1 << 20);
   const int xt16 = (int)std::min<int64_t>((xlines + kL16 - 1) / kL16, 1 << 20);
-  if (z16)
-    launch(k_spec_fwd_z16, zt16, kT16, s, sp, r, done);
+  const bool slab = sp.world > 1;
+  if (z16 && slab)
+    launch(k_spec_fwd_z16<true>, zt16, kT16, s, sp, r, done);
+  else if (z16)
+    launch(k_spec_fwd_z16<false>, zt16, kT16, s, sp, r, done);
   else
     launch_smem(k_spec_fwd_z, zt, kFftThreads, zsm, s, sp, r, done);
   barrier();
@@ -812,15 +861,16 @@ int spec_apply(const MgLevel &l0, const SpecPlan &sp, const double *r,
     // the fused z-sums end in a cross-rank allreduce, which no rank leaves
     // before every rank's loads are done: it doubles as the closing barrier
     if (z16)
-      launch(k_spec_inv_z16<true>, std::min(zt16, red_blocks), kT16, s, sp, r,
-             z, *fuse, done);
+      launch(slab ? k_spec_inv_z16<true, true> : k_spec_inv_z16<true, false>,
+             std::min(zt16, red_blocks), kT16, s, sp, r, z, *fuse, done);
     else
       launch_smem(k_spec_inv_z<true>, std::min(zt, red_blocks), kFftThreads,
                   zsm, s, sp, r, z, *fuse, done);
   } else {
     if (z16)
-      launch(k_spec_inv_z16<false>, zt16, kT16, s, sp, r, z,
-             CgFuse{nullptr, nullptr, nullptr, 0}, done);
+      launch(slab ? k_spec_inv_z16<false, true> : k_spec_inv_z16<false, false>,
+             zt16, kT16, s, sp, r, z, CgFuse{nullptr, nullptr, nullptr, 0},
+             done);
     else
       launch_smem(k_spec_inv_z<false>, zt, kFftThreads, zsm, s, sp, r, z,
                   CgFuse{nullptr, nullptr, nullptr, 0}, done);
