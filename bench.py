@@ -567,12 +567,17 @@ def main():
     stats = {"mom": 0, "p": 0, "adj": 0, "steps": 0, "bi_fwd": 0,
              "bi_adj": 0, "cg": 0}
 
-    def step(state):
+    def fwd(state):
         cfg = piso.StepConfig(dt=dt, nu=nu, source=forcing(state.u, nu),
                               tol=args.tol)
         tape = piso.StepTape()
         new, dg = piso.piso_step(dom, state, cfg, ws, tape)
-        g = adjoint.backward_step(dom, tape, cot, tol=args.tol)
+        return new, dg, tape
+
+    def adj(tape):
+        return adjoint.backward_step(dom, tape, cot, tol=args.tol)
+
+    def count(dg, g):
         stats["mom"] += dg.momentum_iterations
         stats["p"] += dg.pressure_iterations
         stats["adj"] += g.solve_iterations
@@ -583,6 +588,11 @@ def main():
                         + sum(r.iterations for r in (g.reports or [])
                               if r.stage.startswith("adjoint_pressure")))
         stats["steps"] += 1
+
+    def step(state):
+        new, dg, tape = fwd(state)
+        g = adj(tape)
+        count(dg, g)
         return new, g
 
     state = state0
@@ -620,56 +630,106 @@ def main():
     it_per_step = {k: stats[k] / max(stats["steps"], 1)
                    for k in ("mom", "p", "adj", "bi_fwd", "bi_adj", "cg")}
 
-    # end to end through the public API with host buffers: every step
-    # copies its input velocity and boundary values in from pinned host
-    # memory and its velocity and gradient out to pinned host memory.  The
-    # copies run on a side stream, overlapped with the neighbouring steps'
-    # compute (the next input is prefetched, the last output drained while
-    # the next step runs), as a production loop would.
-    u_host = state.u.detach().cpu().contiguous().pin_memory()
-    outs = [(torch.empty_like(u_host).pin_memory(),
-             torch.empty_like(u_host).pin_memory()) for _ in range(2)]
-    bc_host = [b.detach().cpu().contiguous().pin_memory() for b in state.bc]
-    h2d = u_host.numel() * 8 + sum(b.numel() * 8 for b in bc_host)
-    d2h = 2 * u_host.numel() * 8
-    main = torch.cuda.current_stream(dev)
-    side = torch.cuda.Stream(dev)
+    # end to end through the public API with host buffers: every step's
+    # input state (velocity, pressure, boundary values) is copied in from
+    # pinned host memory, and its output velocity / pressure and the
+    # velocity gradient are copied out to pinned host memory.  The state
+    # makes a real host round trip: step k's output goes to the host and
+    # comes back as step k + 1's input.  Those copies run while step k's
+    # adjoint computes, in chunks on two side streams so the device-to-host
+    # and host-to-device engines overlap (the gradient drains during the
+    # next forward step), as a production loop would.
+    n_loc, d_loc = state.u.shape
+    nU, nP = state.u.numel(), state.p.numel()
 
-    def fetch():
-        with torch.cuda.stream(side):
-            u = u_host.to(dev, non_blocking=True)
+    def flat(t):
+        # storage-order flat view of a field ((n, d) fields are transposed
+        # views of (d, n) storage)
+        st_ = t.t() if t.dim() == 2 else t
+        return (st_ if st_.is_contiguous() else st_.contiguous()).reshape(-1)
+
+    def pinned(m):
+        return torch.empty(m, dtype=torch.float64, pin_memory=True)
+
+    u_host = [pinned(nU) for _ in range(2)]
+    p_host = [pinned(nP) for _ in range(2)]
+    g_host = [pinned(nU) for _ in range(2)]
+    bc_host = [b.detach().cpu().contiguous().pin_memory() for b in state.bc]
+    u_host[0].copy_(flat(state.u))
+    p_host[0].copy_(flat(state.p))
+    h2d = (nU + nP) * 8 + sum(b.numel() * 8 for b in bc_host)
+    d2h = (2 * nU + nP) * 8
+    main = torch.cuda.current_stream(dev)
+    s_out = torch.cuda.Stream(dev)
+    s_in = torch.cuda.Stream(dev)
+    n_chunks = 8
+
+    def bcs_in():
+        with torch.cuda.stream(s_in):
             bcs = [b.to(dev, non_blocking=True) for b in bc_host]
             ev = torch.cuda.Event()
-            ev.record(side)
-        return u, bcs, ev
+            ev.record(s_in)
+        return bcs, ev
 
+    e2e_stats0 = dict(stats)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e2 = torch.cuda.Event(enable_timing=True)
     e3 = torch.cuda.Event(enable_timing=True)
     e2.record(main)
-    nxt = fetch()
+    with torch.cuda.stream(s_in):
+        u_in = u_host[0].to(dev, non_blocking=True)
+        p_in = p_host[0].to(dev, non_blocking=True)
+    bc_in, ev = bcs_in()
+    t_state, n_state = state.t, state.step
     for k in range(args.steps):
-        u_in, bc_in, ev = nxt
         main.wait_event(ev)
-        for t in [u_in] + bc_in:
+        for t in [u_in, p_in] + bc_in:
             t.record_stream(main)
-        if k + 1 < args.steps:
-            nxt = fetch()
-        st = piso.FlowState(u=u_in, p=state.p, bc=bc_in, t=state.t,
-                            step=state.step)
-        new, g = step(st)
-        done = torch.cuda.Event()
-        done.record(main)
-        ou, og = outs[k % 2]
-        with torch.cuda.stream(side):
-            side.wait_event(done)
-            ou.copy_(new.u, non_blocking=True)
-            og.copy_(g.u, non_blocking=True)
-        new.u.record_stream(side)
-        g.u.record_stream(side)
-    main.wait_stream(side)
+        st = piso.FlowState(u=u_in.view(d_loc, n_loc).t(), p=p_in, bc=bc_in,
+                            t=t_state, step=n_state)
+        new, dg, tape = fwd(st)
+        t_state, n_state = new.t, new.step
+        done_f = torch.cuda.Event()
+        done_f.record(main)
+        slot = (k + 1) % 2
+        last = k + 1 == args.steps
+        u_nx = None if last else torch.empty(nU, dtype=torch.float64,
+                                             device=dev)
+        p_nx = None if last else torch.empty(nP, dtype=torch.float64,
+                                             device=dev)
+        s_out.wait_event(done_f)
+        for src, hst, dst in ((flat(new.u), u_host[slot], u_nx),
+                              (flat(new.p), p_host[slot], p_nx)):
+            src.record_stream(s_out)
+            m = src.numel()
+            for c in range(n_chunks):
+                a, b = m * c // n_chunks, m * (c + 1) // n_chunks
+                with torch.cuda.stream(s_out):
+                    hst[a:b].copy_(src[a:b], non_blocking=True)
+                    e_c = torch.cuda.Event()
+                    e_c.record(s_out)
+                if dst is not None:
+                    s_in.wait_event(e_c)
+                    with torch.cuda.stream(s_in):
+                        dst[a:b].copy_(hst[a:b], non_blocking=True)
+        if not last:
+            u_nx.record_stream(s_in)
+            p_nx.record_stream(s_in)
+            u_in, p_in = u_nx, p_nx
+            bc_in, ev = bcs_in()
+        g = adj(tape)
+        count(dg, g)
+        done_a = torch.cuda.Event()
+        done_a.record(main)
+        s_out.wait_event(done_a)
+        with torch.cuda.stream(s_out):
+            gf = flat(g.u)
+            g_host[k % 2].copy_(gf, non_blocking=True)
+        gf.record_stream(s_out)
+    main.wait_stream(s_out)
+    main.wait_stream(s_in)
     e3.record(main)
     torch.cuda.synchronize()
     ms_e2e = e2.elapsed_time(e3)
@@ -677,6 +737,25 @@ def main():
         t = torch.tensor([ms_e2e], device="cpu" if share_dev() else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
+    # the box's pinned-copy bandwidth (context for e2e: the round trip is
+    # hidden under the adjoint only while the copies outrun it)
+    def copy_gbs(dst, src, reps=3):
+        ea = torch.cuda.Event(enable_timing=True)
+        eb = torch.cuda.Event(enable_timing=True)
+        ea.record(main)
+        for _ in range(reps):
+            dst.copy_(src, non_blocking=True)
+        eb.record(main)
+        torch.cuda.synchronize()
+        return reps * src.numel() * 8 / (ea.elapsed_time(eb) / 1e3) / 1e9
+
+    dbuf = torch.empty(nU, dtype=torch.float64, device=dev)
+    pcie = {"h2d_gbs": copy_gbs(dbuf, u_host[0]),
+            "d2h_gbs": copy_gbs(u_host[1], dbuf)}
+    del dbuf
+    e2e_it = {k: (stats[k] - e2e_stats0[k]) / max(
+        stats["steps"] - e2e_stats0["steps"], 1)
+        for k in ("bi_fwd", "bi_adj", "cg")}
     e2e_value = cells_job * args.steps / (ms_e2e / 1e3) / 1e6
 
     per_step = {k: stats[k] / max(stats["steps"], 1)
@@ -714,7 +793,9 @@ def main():
             "clocks": clk,
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h)},
+                    "d2h_bytes_per_step": int(d2h),
+                    "iterations_per_step": e2e_it,
+                    "pinned_copy": pcie},
             "gpu_launches": int(launches),
             "iterations_per_step": it_per_step,
         }

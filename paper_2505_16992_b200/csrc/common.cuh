@@ -123,6 +123,7 @@ struct Plan {
   // driver shares between streams, which would serialise slabs that share
   // a device
   void *pinned = nullptr;
+  void *pinned_dev = nullptr;  // its device alias (mapped)
   // lock-step iterations of the last BiCGStab solve (plain, transposed):
   // the first batch the next solve launches before polling
   mutable int bi_hint[2] = {0, 0};

@@ -21,13 +21,30 @@ int cuda_check(cudaError_t e, const char *what) {
   return PF_ERR_CUDA;
 }
 
+// the small status reads are stored into the mapped staging buffer by a
+// one-CTA kernel, not by a copy engine: a solver's poll then never queues
+// behind a caller's bulk device-to-host copy on another stream
+__global__ void k_d2h_small(unsigned char *dst, const unsigned char *src,
+                            int bytes) {
+  for (int i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+}
+
 int d2h(const Plan &p, void *host, const void *dev, size_t bytes,
         cudaStream_t s) {
   if (bytes > kPinnedBytes || !p.pinned) {
     set_error("d2h: read too large for the plan's staging buffer");
     return PF_ERR_ARG;
   }
-  PF_CUDA(cudaMemcpyAsync(p.pinned, dev, bytes, cudaMemcpyDeviceToHost, s));
+  if (p.pinned_dev && !p.comm) {
+    ++g_launches;
+    k_d2h_small<<<1, 128, 0, s>>>(static_cast<unsigned char *>(p.pinned_dev),
+                                  static_cast<const unsigned char *>(dev),
+                                  (int)bytes);
+  } else {
+    // slab ranks sharing one device in tests: a copy engine needs no SM
+    // while peers' kernels may occupy them all
+    PF_CUDA(cudaMemcpyAsync(p.pinned, dev, bytes, cudaMemcpyDeviceToHost, s));
+  }
   PF_CUDA(cudaStreamSynchronize(s));
   std::memcpy(host, p.pinned, bytes);
   return PF_OK;
@@ -124,10 +141,15 @@ extern "C" int pf_plan_create(const pf_plan_desc *desc, pf_plan **out) {
   }
   p->has_mg = mg_plan(*p, p->mg, &p->mg_bytes);
   {
-    const cudaError_t e = cudaMallocHost(&p->pinned, kPinnedBytes);
+    const cudaError_t e =
+        cudaHostAlloc(&p->pinned, kPinnedBytes, cudaHostAllocMapped);
     if (e != cudaSuccess) {
       delete p;
-      return cuda_check(e, "cudaMallocHost(plan staging)");
+      return cuda_check(e, "cudaHostAlloc(plan staging)");
+    }
+    if (cudaHostGetDevicePointer(&p->pinned_dev, p->pinned, 0) != cudaSuccess) {
+      cudaGetLastError();
+      p->pinned_dev = nullptr;  // copy-engine reads only
     }
   }
   *out = reinterpret_cast<pf_plan *>(p);

@@ -1295,12 +1295,15 @@ int cg_core_mg(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     rc = mg_graph(pl, w, st, mg, x, &exec, &nk);
     if (rc) return rc;
   }
+  // the first batch goes out without a poll (its kernels return at once
+  // when the setup already converged): one host round trip per batch
   int launched = 0;
   for (;;) {
-    rc = read_state(pl, st, &hs, s);
-    if (!rc) rc = comm_check(pl, s);
-    if (rc) return rc;
-    if (hs.all_done || launched >= maxiter) break;
+    if (launched >= maxiter) {  // maxiter <= 0: no iteration at all
+      rc = read_state(pl, st, &hs, s);
+      if (rc) return rc;
+      break;
+    }
     int b = std::min(next_batch(launched, 0), maxiter - launched);
     b = std::max(1, (b + kGraphIters - 1) / kGraphIters);
     for (int k = 0; k < b; ++k) {
@@ -1313,6 +1316,10 @@ int cg_core_mg(const Plan &pl, const V &v, Workspace &w, SolverState *st,
       }
     }
     launched += b * kGraphIters;
+    rc = read_state(pl, st, &hs, s);
+    if (!rc) rc = comm_check(pl, s);
+    if (rc) return rc;
+    if (hs.all_done || launched >= maxiter) break;
   }
   launch(k_cg_finish, ge, kBlock, s, x, rg, st);
   PF_LAUNCH_CHECK("mg-cg finish");
@@ -1338,7 +1345,6 @@ int cg_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
                             cudaMemcpyDeviceToDevice, s));
     int rc = cg_core_mg(pl, v, w, st, hs, a, bp, xw, tol, maxiter, zero_mean,
                         mg, s);
-    if (!rc) rc = read_state(pl, st, &hs, s);
     if (rc) return rc;
     PF_CUDA(cudaMemcpyAsync(x, xw, sizeof(double) * n,
                             cudaMemcpyDeviceToDevice, s));
@@ -1360,10 +1366,11 @@ int cg_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   PF_LAUNCH_CHECK("cg setup");
   int launched = 0;
   for (;;) {
-    int rc = read_state(pl, st, &hs, s);
-    if (!rc) rc = comm_check(pl, s);
-    if (rc) return rc;
-    if (hs.all_done || launched >= maxiter) break;
+    if (launched >= maxiter) {  // maxiter <= 0: no iteration at all
+      const int rc = read_state(pl, st, &hs, s);
+      if (rc) return rc;
+      break;
+    }
     const int b = std::min(next_batch(launched, 0), maxiter - launched);
     for (int k = 0; k < b; ++k) {
       halo(pl, s, {{p, 1}});
@@ -1375,6 +1382,10 @@ int cg_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     }
     PF_LAUNCH_CHECK("cg iterations");
     launched += b;
+    int rc = read_state(pl, st, &hs, s);
+    if (!rc) rc = comm_check(pl, s);
+    if (rc) return rc;
+    if (hs.all_done || launched >= maxiter) break;
   }
   launch(k_cg_finish, ge, kBlock, s, x, rg, st);
   if (hs.c[0].converged && !hs.c[0].zero_rhs) {
@@ -1567,12 +1578,15 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   // neighbours (v[0] = 0 and dinv are exchanged once here)
   halo(pl, s, {{bv.v[0], ncomp}, {bv.dinv, 1}});
   PF_LAUNCH_CHECK("bicgstab setup");
+  // the first batch goes out without a poll (its kernels return at once
+  // when the setup already converged)
   int launched = 0;
   for (;;) {
-    int rc = read_state(pl, st, &hs, s);
-    if (!rc) rc = comm_check(pl, s);
-    if (rc) return rc;
-    if (hs.all_done || launched >= maxiter) break;
+    if (launched >= maxiter) {  // maxiter <= 0: no iteration at all
+      const int rc = read_state(pl, st, &hs, s);
+      if (rc) return rc;
+      break;
+    }
     // first batch: the previous solve's lock-step count on this plan and
     // direction (time steps change slowly), so a typical solve polls once
     static const bool use_hint = getenv("PF_NO_HINT") == nullptr;
@@ -1601,6 +1615,10 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     }
     PF_LAUNCH_CHECK("bicgstab iterations");
     launched += bsz;
+    int rc = read_state(pl, st, &hs, s);
+    if (!rc) rc = comm_check(pl, s);
+    if (rc) return rc;
+    if (hs.all_done || launched >= maxiter) break;
   }
   {
     int lock = 0;  // lock-step iterations this solve needed
