@@ -822,10 +822,12 @@ struct TileSmem {
 constexpr size_t kTileSmem = sizeof(TileSmem);
 
 // MODE 0 (pass pv): g = (r + beta (p0 - omega v0)) / A, outputs p' (the
-//                   undivided value), v' = A g, sums r^.v'
+//                   undivided value), v' = A g, sums r^.v'.  `first` (the
+//                   first iteration, p0 = v0 = 0): g = r / A, p0 and v0 are
+//                   neither read nor (by MODE 2) written
+// MODE 2 (init):    g = x, outputs r = r^ = b - A x, 1 / A; |r|
 // MODE 1 (pass st): g = (r - alpha v') / A, outputs t = A g, sums s.s, t.t,
 //                   t.s
-// MODE 2 (init):    g = x, outputs r = r^ = b - A x, p = v = 0, 1 / A; |r|
 // MODE 3 (verify):  g = x, sums |b - A x|^2 of every component (runs after
 //                   convergence too)
 template <bool kTrans, int MODE, int kMinB = 1>
@@ -833,8 +835,10 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
     k_bi_tiled(TileGeo tg, const double *__restrict__ a, BiVecs w, int par,
                int64_t n, SolverState *st, double *partials,
                unsigned *counter, const double *__restrict__ xin = nullptr,
-               const double *__restrict__ bin = nullptr, int nverify = 0) {
+               const double *__restrict__ bin = nullptr, int nverify = 0,
+               int first = 0) {
   if (MODE != 3 && st->all_done) return;
+  const bool fresh = MODE == 0 && first;
   constexpr int K = MODE == 1 ? 9 : 3;
   constexpr bool kX = MODE >= 2;  // the input is the iterate x itself
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -885,8 +889,10 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
       }
       if (ok) {
         cp_async8(&sm.raw[b][q][sy][sz], r + o);
-        cp_async8(&sm.raw[b][3 + q][sy][sz], vin + o);
-        if (MODE == 0) cp_async8(&sm.raw[b][6 + q][sy][sz], pin + o);
+        if (!fresh) {
+          cp_async8(&sm.raw[b][3 + q][sy][sz], vin + o);
+          if (MODE == 0) cp_async8(&sm.raw[b][6 + q][sy][sz], pin + o);
+        }
       } else {
         sm.raw[b][q][sy][sz] = 0.0;
         sm.raw[b][3 + q][sy][sz] = 0.0;
@@ -913,11 +919,16 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
     for (int q = 0; q < 3; ++q) {
       g[q] = pv[q] = 0.0;
       if (q >= nc || !act[q]) continue;
-      const double rr = sm.raw[b][q][sy][sz], vv = sm.raw[b][3 + q][sy][sz];
-      const double val = MODE == 0
-                             ? rr + c0[q] * (sm.raw[b][6 + q][sy][sz] -
-                                             c1[q] * vv)
-                             : rr - c0[q] * vv;
+      const double rr = sm.raw[b][q][sy][sz];
+      double val;
+      if (fresh) {
+        val = rr;  // r + beta (0 - omega 0)
+      } else {
+        const double vv = sm.raw[b][3 + q][sy][sz];
+        val = MODE == 0
+                  ? rr + c0[q] * (sm.raw[b][6 + q][sy][sz] - c1[q] * vv)
+                  : rr - c0[q] * vv;
+      }
       pv[q] = val;
       g[q] = val * dj;
     }
@@ -1043,8 +1054,6 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
           if (MODE == 2) {
             w.r[o] = rr;
             w.rhat[o] = rr;
-            w.p[0][o] = 0.0;
-            w.v[0][o] = 0.0;
           }
           acc[q] += rr * rr;
         }
@@ -1483,7 +1492,8 @@ template <bool kTrans, int MODE>
 void launch_tiled(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
                   const BiVecs &bv, int par, int64_t n, SolverState *st,
                   Workspace &w, const double *xin = nullptr,
-                  const double *bin = nullptr, int nverify = 0) {
+                  const double *bin = nullptr, int nverify = 0,
+                  int first = 0) {
   // 2 CTAs per SM (<= 128 registers, 2 x 71 KB of shared memory) measured
   // best on C4: pass pv 5.3 TB/s, pass st 4.3 TB/s (1 CTA: 3.8 / 2.9; 3 CTAs
   // with the 80-register cap: 3.5 / 3.2).  PF_TILE_MINB overrides.
@@ -1501,7 +1511,7 @@ void launch_tiled(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
     ++g_launches;
     kernel<<<grid, kTileThreads, kTileSmem, s>>>(tg, a, bv, par, n, st,
                                                  w.partials, w.counters, xin,
-                                                 bin, nverify);
+                                                 bin, nverify, first);
   };
   if (minb >= 3)
     go(k_bi_tiled<kTrans, MODE, 3>);
@@ -1600,7 +1610,8 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
       const int par = (launched + k) & 1;
       halo(pl, s, {{bv.r, ncomp}, {bv.p[par], ncomp}});
       if (tiled)
-        launch_tiled<kTrans, 0>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
+        launch_tiled<kTrans, 0>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w,
+                                nullptr, nullptr, 0, launched + k == 0);
       else
         launch(k_bi_pv<V, kTrans>, gr, kBlock, s, v, a, bv, par, st,
                w.partials, w.counters);
