@@ -825,7 +825,9 @@ constexpr size_t kTileSmem = sizeof(TileSmem);
 //                   undivided value), v' = A g, sums r^.v'.  `first` (the
 //                   first iteration, p0 = v0 = 0): g = r / A, p0 and v0 are
 //                   neither read nor (by MODE 2) written
-// MODE 2 (init):    g = x, outputs r = r^ = b - A x, 1 / A; |r|
+// MODE 2 (init):    g = x, outputs r = r^ = b - A x, 1 / A; |r|, and |b|
+//                   when the state has no |b| yet (a fresh solve: the
+//                   separate k_bi_bnorm pass is folded in here)
 // MODE 1 (pass st): g = (r - alpha v') / A, outputs t = A g, sums s.s, t.t,
 //                   t.s
 // MODE 3 (verify):  g = x, sums |b - A x|^2 of every component (runs after
@@ -839,7 +841,7 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
                int first = 0) {
   if (MODE != 3 && st->all_done) return;
   const bool fresh = MODE == 0 && first;
-  constexpr int K = MODE == 1 ? 9 : 3;
+  constexpr int K = MODE == 1 ? 9 : MODE == 2 ? 6 : 3;
   constexpr bool kX = MODE >= 2;  // the input is the iterate x itself
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem &sm = *reinterpret_cast<TileSmem *>(smem_raw);
@@ -1054,6 +1056,7 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
           if (MODE == 2) {
             w.r[o] = rr;
             w.rhat[o] = rr;
+            acc[3 + q] += rh[q] * rh[q];
           }
           acc[q] += rr * rr;
         }
@@ -1078,7 +1081,17 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
     int all = 1;
     for (int q = 0; q < nc; ++q) {
       CompState &c = st->c[q];
-      if (act[q]) {
+      if (act[q] && c.bnorm == 0.0) {
+        // fresh solve: |b| and the absolute tolerance (k_bi_bnorm)
+        c.bnorm = sqrt(tot[3 + q]);
+        c.tol_abs = c.tol * c.bnorm;
+        if (c.bnorm == 0.0) {
+          c.zero_rhs = 1;
+          c.done = 1;
+          c.converged = 1;
+        }
+      }
+      if (act[q] && !c.done) {
         c.res = sqrt(tot[q]);
         if (c.res <= c.tol_abs) {
           c.converged = 1;
@@ -1577,7 +1590,9 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   const bool tiled = tile_geo(pl, v, tg);
   const int tgrid = tiled ? std::min(tg.ntiles, pl.red_blocks) : 0;
   launch(k_bi_reset, 1, 1, s, st, ncomp, maxiter, precond, tol, fresh, mask);
-  if (fresh) launch(k_bi_bnorm, gr, kBlock, s, b, n, rg, st, w.partials, w.counters);
+  // the tiled init pass forms |b| itself
+  if (fresh && !tiled)
+    launch(k_bi_bnorm, gr, kBlock, s, b, n, rg, st, w.partials, w.counters);
   halo(pl, s, {{x, ncomp}});
   if (tiled)
     launch_tiled<kTrans, 2>(tg, tgrid, s, a, bv, 0, (int64_t)n, st, w, x, b, 0);
