@@ -15,6 +15,8 @@
 // GPU never waits on a host round trip per iteration.
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
+#include <set>
 
 #include "cgstate.cuh"
 #include "common.cuh"
@@ -832,15 +834,15 @@ constexpr size_t kTileSmem = sizeof(TileSmem);
 //                   t.s
 // MODE 3 (verify):  g = x, sums |b - A x|^2 of every component (runs after
 //                   convergence too)
-template <bool kTrans, int MODE, int kMinB = 1>
+template <bool kTrans, int MODE, int kMinB = 1, bool kFirst = false>
 __global__ void __launch_bounds__(kTileThreads, kMinB)
     k_bi_tiled(TileGeo tg, const double *__restrict__ a, BiVecs w, int par,
                int64_t n, SolverState *st, double *partials,
                unsigned *counter, const double *__restrict__ xin = nullptr,
-               const double *__restrict__ bin = nullptr, int nverify = 0,
-               int first = 0) {
+               const double *__restrict__ bin = nullptr, int nverify = 0) {
   if (MODE != 3 && st->all_done) return;
-  const bool fresh = MODE == 0 && first;
+  // compile-time: a runtime branch here slows the transposed pass ~15 %
+  constexpr bool fresh = MODE == 0 && kFirst;
   constexpr int K = MODE == 1 ? 9 : MODE == 2 ? 6 : 3;
   constexpr bool kX = MODE >= 2;  // the input is the iterate x itself
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1515,23 +1517,36 @@ void launch_tiled(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
     return e ? atoi(e) : 2;
   }();
   auto go = [&](auto kernel) {
-    static bool attr = false;  // per instantiation
-    if (!attr) {
-      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kTileSmem);
-      attr = true;
+    // the shared-memory opt-in, once per kernel (instantiations share the
+    // lambda's type, so the flag is keyed by the kernel's address)
+    static std::mutex mu;
+    static std::set<const void *> done;
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      if (done.insert(reinterpret_cast<const void *>(kernel)).second)
+        cudaFuncSetAttribute(kernel,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kTileSmem);
     }
     ++g_launches;
     kernel<<<grid, kTileThreads, kTileSmem, s>>>(tg, a, bv, par, n, st,
                                                  w.partials, w.counters, xin,
-                                                 bin, nverify, first);
+                                                 bin, nverify);
   };
-  if (minb >= 3)
+  if (MODE == 0 && first) {
+    if (minb >= 3)
+      go(k_bi_tiled<kTrans, MODE, 3, true>);
+    else if (minb == 2)
+      go(k_bi_tiled<kTrans, MODE, 2, true>);
+    else
+      go(k_bi_tiled<kTrans, MODE, 1, true>);
+  } else if (minb >= 3) {
     go(k_bi_tiled<kTrans, MODE, 3>);
-  else if (minb == 2)
+  } else if (minb == 2) {
     go(k_bi_tiled<kTrans, MODE, 2>);
-  else
+  } else {
     go(k_bi_tiled<kTrans, MODE, 1>);
+  }
 }
 
 // tiled stencil passes apply to 3D boxes whose Y / Z extents are whole tiles
@@ -1552,16 +1567,36 @@ bool tile_geo(const Plan &pl, const V &v, TileGeo &tg) {
   tg.x1 = (int32_t)(pl.i1 / plane);
   tg.ty_tiles = tg.Y / kTY;
   tg.tz_tiles = tg.Z / kTZ;
-  // chunks of kXChunk planes, halved down to 4 until the tiles fill the GPU
-  // (two CTAs per SM, two waves): small boxes (the 64 x 48 x 64 LES
-  // sample) would otherwise run a few dozen CTAs
-  tg.xc = kXChunk;
-  const int64_t want = 4LL * pl.num_sms;
+  // X chunk length: tiles run in rounds of R resident CTAs (two per SM), a
+  // tile of xc planes costs ~ xc + 2 plane steps (its two prologue planes),
+  // so pick xc minimising rounds * (xc + 2).  C4 (192 columns x 256
+  // planes, R = 296): xc = 86, 576 tiles in 2 full rounds, instead of the
+  // 768 tiles of xc = 64 whose third round is 59 % full.  Small boxes get
+  // short chunks and enough tiles to fill the GPU.
   const int32_t nx = tg.x1 - tg.x0;
-  while (tg.xc > 4 &&
-         (int64_t)tg.ty_tiles * tg.tz_tiles * ((nx + tg.xc - 1) / tg.xc) <
-             want)
-    tg.xc /= 2;
+  {
+    static const int minb = [] {
+      const char *e = getenv("PF_TILE_MINB");
+      return e ? std::max(1, atoi(e)) : 2;
+    }();
+    const int64_t R = (int64_t)std::min(minb, 3) * pl.num_sms;
+    const int64_t ncols = (int64_t)tg.ty_tiles * tg.tz_tiles;
+    int64_t best = -1;
+    tg.xc = 1;
+    for (int32_t xc = 1; xc <= std::max(1, nx); ++xc) {
+      const int64_t tiles = ncols * ((nx + xc - 1) / xc);
+      const int64_t cost = (tiles + R - 1) / R * (xc + 2);
+      if (best < 0 || cost <= best) {
+        best = cost;
+        tg.xc = xc;
+      }
+    }
+    static const int force = [] {  // PF_TILE_XC: fixed chunk (experiments)
+      const char *e = getenv("PF_TILE_XC");
+      return e ? atoi(e) : 0;
+    }();
+    if (force > 0) tg.xc = std::min(force, std::max(1, nx));
+  }
   tg.chunks = (nx + tg.xc - 1) / tg.xc;
   tg.ntiles = tg.ty_tiles * tg.tz_tiles * tg.chunks;
   return true;
