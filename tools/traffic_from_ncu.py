@@ -1,6 +1,8 @@
-"""profiles/traffic.json from an `ncu --set full` raw CSV: mean DRAM bytes
+"""profiles/traffic.json from an `ncu --set full` raw CSV: median DRAM bytes
 (read + write) per launch of each kernel, under the names bench.py's
-roofline uses.  Usage: python tools/traffic_from_ncu.py raw.csv config"""
+roofline uses.  The median is the steady iteration: a solve's first pv pass
+(no p / v to read) and its tail (converged components skipped) move less.
+Usage: python tools/traffic_from_ncu.py raw.csv config"""
 import csv
 import json
 import os
@@ -43,9 +45,10 @@ def main(path, config):
     out_path = os.path.join(ROOT, "profiles", "traffic.json")
     data = json.load(open(out_path)) if os.path.exists(out_path) else {}
     data.setdefault(config, {}).update(
-        {k: sum(v) / len(v) for k, v in acc.items()})
+        {k: sorted(v)[len(v) // 2] for k, v in acc.items()})
     data["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch "
-                     "from ncu --set full (tools/traffic_from_ncu.py)")
+                     "(median over the step's launches) from ncu --set full "
+                     "(tools/traffic_from_ncu.py)")
     json.dump(data, open(out_path, "w"), indent=1, sort_keys=True)
     print(json.dumps(data[config], indent=1))
 
