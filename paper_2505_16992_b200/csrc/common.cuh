@@ -74,7 +74,8 @@ struct SpecPlan {
   int32_t kz0[kMaxRanks + 1];
   double2 *peer_s[kMaxRanks];
   double2 *s;          // (sy, kz of this rank, sx) spectral work array
-  double *cw;          // (sy, nkz * sx) Thomas c' scratch
+  double *cw;          // (sy, nkz * sx) Thomas c'
+  double *iw;          // (sy, nkz * sx) Thomas 1 / den
   double *ax, *ay, *az;  // (sy) plane-mean face weights
   double2 *twx, *twz;    // exp(-2 pi i k / N), N = sx, sz
   double *lx, *lz;       // 2 - 2 cos(2 pi k / N)

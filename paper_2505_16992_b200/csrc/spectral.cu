@@ -217,11 +217,49 @@ __global__ void __launch_bounds__(kFftThreads)
   }
 }
 
+// setup: the Thomas factors of every wavenumber pair's Y system (they
+// depend on the plane-mean weights only, so once per operator, not per
+// application): c'_y and 1 / den_y, one thread per column
+__global__ void __launch_bounds__(kYThreads)
+    k_spec_factors(SpecPlan sp, const int *done) {
+  SPEC_DONE_RETURN;
+  extern __shared__ double sh[];
+  const int sy = sp.sy;
+  double *ax = sh, *ay = sh + sy, *az = sh + 2 * sy;
+  for (int y = threadIdx.x; y < sy; y += blockDim.x) {
+    ax[y] = sp.ax[y];
+    ay[y] = y + 1 < sy ? sp.ay[y] : 0.0;
+    az[y] = sp.az[y];
+  }
+  __syncthreads();
+  const int kzb = sp.kz0[sp.rank];
+  const int64_t ncol = (int64_t)(sp.kz0[sp.rank + 1] - kzb) * sp.sx;
+  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= ncol) return;
+  const int kx = (int)(col % sp.sx), kz = kzb + (int)(col / sp.sx);
+  const double lxv = sp.lx[kx], lzv = sp.lz[kz];
+  const bool pinned = kz == 0 && kx == 0;
+  double cprev = 0.0;
+  for (int y = 0; y < sy; ++y) {
+    const double lo = y > 0 ? ay[y - 1] : 0.0, up = ay[y];
+    double c = 0.0, iv = 0.0;
+    if (!(pinned && y == sy - 1)) {
+      const double den = ax[y] * lxv + az[y] * lzv + lo + up + lo * cprev;
+      iv = 1.0 / den;
+      c = -up * iv;
+    }
+    cprev = c;
+    sp.cw[(int64_t)y * ncol + col] = c;
+    sp.iw[(int64_t)y * ncol + col] = iv;
+  }
+}
+
 // pass 3: per wavenumber pair (kx, kz) the tridiagonal Y system
 //   (ax lx + az lz + ay- + ay+) z_y - ay- z_{y-1} - ay+ z_{y+1} = rhs_y,
-// one thread per real / imaginary part (the coefficients are real); the
-// forward sweep overwrites the work array in place, the real lane keeps c'.
-// The 1 / (sx sz) normalisation of the transforms is folded in here.
+// one thread per real / imaginary part (the coefficients are real), with
+// the factors of k_spec_factors: no division on the sweeps' dependency
+// chain.  The forward sweep overwrites the work array in place.  The
+// 1 / (sx sz) normalisation of the transforms is folded in here.
 __global__ void __launch_bounds__(kYThreads)
     k_spec_ysolve(SpecPlan sp, const int *done) {
   SPEC_DONE_RETURN;
@@ -241,41 +279,33 @@ __global__ void __launch_bounds__(kYThreads)
   const int64_t col = t >> 1;
   const int comp = (int)(t & 1);
   const int kx = (int)(col % sp.sx), kz = kzb + (int)(col / sp.sx);
-  const double lxv = active ? sp.lx[kx] : 0.0;
-  const double lzv = active ? sp.lz[kz] : 0.0;
   const bool pinned = kz == 0 && kx == 0;
   const double scale = 1.0 / ((double)sp.sx * sp.sz);
   double *sv = reinterpret_cast<double *>(sp.s);
   const int64_t ystride = 2 * ncol;
   constexpr int C = 16;
+  (void)comp;
   if (active) {
-    double dp = 0.0, cprev = 0.0;
+    double dp = 0.0;
     for (int y0 = 0; y0 < sy; y0 += C) {
-      double rr[C];
+      double rr[C], ivs[C];
 #pragma unroll
       for (int k = 0; k < C; ++k)
-        if (y0 + k < sy) rr[k] = __ldcg(sv + (int64_t)(y0 + k) * ystride + t);
+        if (y0 + k < sy) {
+          rr[k] = __ldcg(sv + (int64_t)(y0 + k) * ystride + t);
+          ivs[k] = __ldcg(sp.iw + (int64_t)(y0 + k) * ncol + col);
+        }
 #pragma unroll
       for (int k = 0; k < C; ++k) {
         const int y = y0 + k;
         if (y >= sy) break;
-        const double lo = y > 0 ? ay[y - 1] : 0.0, up = ay[y];
-        double c = 0.0;
-        if (pinned && y == sy - 1) {
-          dp = 0.0;
-        } else {
-          const double den = ax[y] * lxv + az[y] * lzv + lo + up + lo * cprev;
-          const double iv = 1.0 / den;
-          c = -up * iv;
-          dp = (rr[k] * scale + lo * dp) * iv;
-        }
-        cprev = c;
+        const double lo = y > 0 ? ay[y - 1] : 0.0;
+        dp = (pinned && y == sy - 1) ? 0.0
+                                     : (rr[k] * scale + lo * dp) * ivs[k];
         sv[(int64_t)y * ystride + t] = dp;
-        if (comp == 0) sp.cw[(int64_t)y * ncol + col] = c;
       }
     }
   }
-  __syncwarp();
   if (active) {
     double zn = 0.0;
     for (int y0 = sy - 1; y0 >= 0; y0 -= C) {
@@ -285,7 +315,7 @@ __global__ void __launch_bounds__(kYThreads)
         const int y = y0 - k;
         if (y >= 0) {
           dd[k] = sv[(int64_t)y * ystride + t];
-          cc[k] = sp.cw[(int64_t)y * ncol + col];
+          cc[k] = __ldcg(sp.cw + (int64_t)y * ncol + col);
         }
       }
 #pragma unroll
@@ -745,7 +775,7 @@ void spec_slab_bind(SpecPlan &sp, const CommHost &c) {
 int64_t spec_bytes(const SpecPlan &sp) {
   // the work array of a slab plan lives in the comm's symmetric buffer
   const int64_t ns = (int64_t)sp.sy * nkz_max(sp) * sp.sx;
-  return (spec_is_slab(sp) ? 0 : al(ns * 16)) + al(ns * 8) +
+  return (spec_is_slab(sp) ? 0 : al(ns * 16)) + 2 * al(ns * 8) +
          al(3 * sp.sy * 8) + al(sp.sx * 16) + al(sp.sz * 16) +
          al(sp.sx * 8) + al(sp.nkz * 8);
 }
@@ -758,6 +788,8 @@ char *spec_bind(SpecPlan &sp, char *q) {
     q += al(ns * 16);
   }
   sp.cw = reinterpret_cast<double *>(q);
+  q += al(ns * 8);
+  sp.iw = reinterpret_cast<double *>(q);
   q += al(ns * 8);
   sp.ax = reinterpret_cast<double *>(q);
   sp.ay = sp.ax + sp.sy;
@@ -774,6 +806,16 @@ char *spec_bind(SpecPlan &sp, char *q) {
   return q;
 }
 
+template <typename... KArgs, typename... Args>
+static void launch_smem(void (*kernel)(KArgs...), int grid, int block,
+                        size_t smem, cudaStream_t stream, Args... args) {
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  ++g_launches;
+  kernel<<<grid, block, smem, stream>>>(args...);
+}
+
 int spec_setup(const MgLevel &l0, const SpecPlan &sp, cudaStream_t s,
                const int *done, const Plan *pl) {
   if (spec_is_slab(sp) && (!pl || !pl->comm)) {
@@ -788,19 +830,16 @@ int spec_setup(const MgLevel &l0, const SpecPlan &sp, cudaStream_t s,
     if (rc) return rc;
   }
   launch(k_spec_plane_mean, grid_for(3 * sp.sy), kBlock, s, sp);
+  {
+    const int64_t ncol =
+        (int64_t)(sp.kz0[sp.rank + 1] - sp.kz0[sp.rank]) * sp.sx;
+    launch_smem(k_spec_factors, grid_for(ncol, kYThreads), kYThreads,
+                3 * sizeof(double) * sp.sy, s, sp, done);
+  }
   PF_LAUNCH_CHECK("spec_setup");
   return PF_OK;
 }
 
-template <typename... KArgs, typename... Args>
-static void launch_smem(void (*kernel)(KArgs...), int grid, int block,
-                        size_t smem, cudaStream_t stream, Args... args) {
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-  ++g_launches;
-  kernel<<<grid, block, smem, stream>>>(args...);
-}
 
 int spec_apply(const MgLevel &l0, const SpecPlan &sp, const double *r,
                double *z, cudaStream_t s, const int *done, cudaEvent_t *ev,
