@@ -102,13 +102,16 @@ __device__ double2 *fft_lines(double2 *a, double2 *b, int N, int nl,
 // enumerated X fastest, then Y; slab plans skip the ghost plane at local
 // X = 0).  Their first elements and (x, y) are tabulated once per tile, so
 // the element loops carry no integer division.
-struct ZLines {
-  int32_t base[kMaxLines];
-  int32_t x[kMaxLines], y[kMaxLines];
+template <int N>
+struct ZLinesT {
+  int32_t base[N];
+  int32_t x[N], y[N];
 };
+using ZLines = ZLinesT<kMaxLines>;
 
+template <class T>
 __device__ __forceinline__ void zlines_fill(const SpecPlan &sp, int32_t l0,
-                                            int nl, ZLines &t) {
+                                            int nl, T &t) {
   const int32_t last = sp.nxl * sp.sy - 1;
   for (int j = threadIdx.x; j < nl; j += blockDim.x) {
     const int32_t l = min(l0 + j, last);
@@ -413,7 +416,7 @@ struct Spec16Smem {
     double2 t[kL16][kR][kR + 1];
     double2 nat[kL16 * kLP16];
   };
-  ZLines zl;
+  ZLinesT<2 * kL16> zl;
 };
 
 __device__ __forceinline__ double2 *nat16(Spec16Smem &sm, int line) {
