@@ -159,6 +159,22 @@ def test_slab_step_matches_single_domain(world):
                    - diag.momentum_iterations) <= 3
 
 
+@pytest.mark.parametrize("shape", [(8, 8, 256), (256, 8, 8)])
+def test_slab_step_256_point_transforms(shape):
+    """Length-256 Z / X: the register four-step FFT kernels of the spectral
+    preconditioner in their slab form (transposes over peer memory)."""
+    dom, dev, u0, nu, dt, w = _setup(shape)
+    ref = _single(dom, dev, u0, nu, dt, w, steps=1)
+    slabs, res = _slabs(dom, dev, u0, nu, dt, w, 2, steps=1)
+    st, diag, g = ref[0]
+    u = _gather(slabs, res, 0, lambda r: r[0].u, dom.n, 3)
+    p = _gather(slabs, res, 0, lambda r: r[0].p, dom.n, 0)
+    gu = _gather(slabs, res, 0, lambda r: r[2].u, dom.n, 3)
+    assert _rel(u, st.u) < FIELD_TOL
+    assert _rel(p, st.p) < FIELD_TOL
+    assert _rel(gu, g.u) < FIELD_TOL
+
+
 def test_slab_wall_forcing_matches_global():
     from paper_2505_16992_b200 import channel, slab
     dom, dev, u0, nu, dt, w = _setup()
