@@ -654,19 +654,22 @@ def main():
     u_host = [pinned(nU) for _ in range(2)]
     p_host = [pinned(nP) for _ in range(2)]
     g_host = [pinned(nU) for _ in range(2)]
-    bc_host = [b.detach().cpu().contiguous().pin_memory() for b in state.bc]
+    # boundary values round-trip too (outflow faces change every step)
+    bc_host = [[b.detach().cpu().contiguous().pin_memory() for b in state.bc]
+               for _ in range(2)]
     u_host[0].copy_(flat(state.u))
     p_host[0].copy_(flat(state.p))
-    h2d = (nU + nP) * 8 + sum(b.numel() * 8 for b in bc_host)
-    d2h = (2 * nU + nP) * 8
+    nbc = sum(b.numel() for b in bc_host[0])
+    h2d = (nU + nP + nbc) * 8
+    d2h = (2 * nU + nP + nbc) * 8
     main = torch.cuda.current_stream(dev)
     s_out = torch.cuda.Stream(dev)
     s_in = torch.cuda.Stream(dev)
     n_chunks = 8
 
-    def bcs_in():
+    def bcs_in(slot):
         with torch.cuda.stream(s_in):
-            bcs = [b.to(dev, non_blocking=True) for b in bc_host]
+            bcs = [b.to(dev, non_blocking=True) for b in bc_host[slot]]
             ev = torch.cuda.Event()
             ev.record(s_in)
         return bcs, ev
@@ -681,7 +684,7 @@ def main():
     with torch.cuda.stream(s_in):
         u_in = u_host[0].to(dev, non_blocking=True)
         p_in = p_host[0].to(dev, non_blocking=True)
-    bc_in, ev = bcs_in()
+    bc_in, ev = bcs_in(0)
     t_state, n_state = state.t, state.step
     for k in range(args.steps):
         main.wait_event(ev)
@@ -714,11 +717,18 @@ def main():
                     s_in.wait_event(e_c)
                     with torch.cuda.stream(s_in):
                         dst[a:b].copy_(hst[a:b], non_blocking=True)
+        with torch.cuda.stream(s_out):
+            for hb, nb in zip(bc_host[slot], new.bc):
+                hb.copy_(nb, non_blocking=True)
+                nb.record_stream(s_out)
+            e_bc = torch.cuda.Event()
+            e_bc.record(s_out)
         if not last:
             u_nx.record_stream(s_in)
             p_nx.record_stream(s_in)
             u_in, p_in = u_nx, p_nx
-            bc_in, ev = bcs_in()
+            s_in.wait_event(e_bc)
+            bc_in, ev = bcs_in(slot)
         g = adj(tape)
         count(dg, g)
         done_a = torch.cuda.Event()
