@@ -58,6 +58,7 @@ CONFIGS = {
 }
 UNROLL = 16
 SAMPLE_SHAPE = (64, 48, 64)
+CPU_SAMPLE_STEPS = 4
 
 
 def parse():
@@ -74,6 +75,8 @@ def parse():
                     help=argparse.SUPPRESS)
     ap.add_argument("--worker-steps", type=int, default=1,
                     help=argparse.SUPPRESS)
+    ap.add_argument("--worker-shape", default="64,48,64",
+                    help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -82,9 +85,11 @@ def parse():
 
 
 def reference_worker(args):
-    """One single-threaded reference process: build the sample channel with
-    the reference's own API, take `worker-steps` fwd+adjoint steps, print
-    cell-steps and seconds (domain build excluded)."""
+    """One single-threaded reference process: build the channel with the
+    reference's own API (make_channel + reichardt_init + wall forcing, the
+    C4 recipe at `--worker-shape`), take `worker-steps` taped fwd+adjoint
+    steps, print one JSON progress line per phase (domain build and initial
+    condition excluded from the timing)."""
     for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS",
               "PISOFLOW_THREADS"):
         os.environ[k] = "1"
@@ -92,36 +97,57 @@ def reference_worker(args):
     sys.path.insert(0, build_ref.ref_path())
     import numpy as np
     from pisoflow import adjoint, kernels, mesh, piso
-    shape = SAMPLE_SHAPE
-    dom = mesh.make_channel(shape, ratio=CONFIGS["c4"][1])
+    shape = tuple(int(v) for v in args.worker_shape.split(","))
+    _, ratio, cfl, _ = CONFIGS[args.config]
+    tb = time.perf_counter()
+    dom = mesh.make_channel(shape, ratio=ratio)
     state, nu, u_tau = piso.reichardt_init(dom, 180.0, perturbation=0.1,
                                            seed=0)
-    dt = CONFIGS["c4"][2] * (2 * np.pi / shape[0]) / np.abs(state.u).max()
+    dt = cfl * (2 * np.pi / shape[0]) / np.abs(state.u).max()
     rng = np.random.default_rng(0)
     w = rng.standard_normal((dom.n, 3))
     ws = piso.PisoWorkspace(dom)
+
+    def emit(**kw):
+        print(json.dumps(kw), flush=True)
+
+    emit(phase="setup", seconds=time.perf_counter() - tb, n=dom.n)
     t0 = time.perf_counter()
-    iters = []
-    for _ in range(args.worker_steps):
+    iters, fwd_s, bwd_s = [], 0.0, 0.0
+    for k in range(args.worker_steps):
+        ta = time.perf_counter()
         src = piso.wall_forcing_source(dom, state.u, nu)
         cfg = piso.StepConfig(dt=dt, nu=nu, source=src, tol=args.tol)
         tape = piso.StepTape()
         state, dg = piso.piso_step(dom, state, cfg, ws, tape)
+        tf = time.perf_counter()
+        emit(phase="forward", step=k, seconds=tf - ta,
+             iterations=[dg.momentum_iterations, dg.pressure_iterations])
         g = adjoint.backward_step(dom, tape,
                                   adjoint.GradState(u=w, p=np.zeros(dom.n)),
                                   tol=args.tol)
+        tg = time.perf_counter()
+        emit(phase="backward", step=k, seconds=tg - tf,
+             iterations=g.solve_iterations)
+        fwd_s += tf - ta
+        bwd_s += tg - tf
         iters.append((dg.momentum_iterations, dg.pressure_iterations,
                       g.solve_iterations))
     sec = time.perf_counter() - t0
-    print(json.dumps({"cell_steps": dom.n * args.worker_steps,
-                      "seconds": sec, "lane": kernels.LANE,
-                      "iterations": iters}))
+    emit(phase="done", cell_steps=dom.n * args.worker_steps, seconds=sec,
+         forward_seconds=fwd_s, backward_seconds=bwd_s, lane=kernels.LANE,
+         iterations=iters, shape=list(shape))
 
 
-def run_reference_sample(procs, steps, tol):
+def _worker_cmd(shape, steps, tol, config="c4"):
+    return [sys.executable, os.path.abspath(__file__), "--reference-worker",
+            "--config", config, "--worker-shape", ",".join(map(str, shape)),
+            "--worker-steps", str(steps), "--tol", str(tol)]
+
+
+def run_reference_sample(procs, steps, tol, shape=None):
     """Run `procs` concurrent reference workers; aggregate Mcell-steps/s."""
-    cmd = [sys.executable, os.path.abspath(__file__), "--reference-worker",
-           "--worker-steps", str(steps), "--tol", str(tol)]
+    cmd = _worker_cmd(shape or SAMPLE_SHAPE, steps, tol)
     t0 = time.perf_counter()
     ps = [subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
                            text=True, cwd=ROOT) for _ in range(procs)]
@@ -139,47 +165,99 @@ def run_reference_sample(procs, steps, tol):
             "iterations": outs[0]["iterations"], "wall": wall}
 
 
+def run_reference_full(shape, steps, tol, budget_s, config="c4"):
+    """The reference on the full workload in ONE single-threaded process
+    (the reference is serial: S/_kernels_c.pyx loops, NumPy elementwise).
+    Returns the worker's phase records; a run that would overrun `budget_s`
+    is stopped and reported as such (never extrapolated)."""
+    p = subprocess.Popen(_worker_cmd(shape, steps, tol, config),
+                         stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                         text=True, cwd=ROOT)
+    recs = []
+    timer = threading.Timer(budget_s, p.kill)
+    timer.start()
+    try:
+        for line in p.stdout:
+            line = line.strip()
+            if line.startswith("{"):
+                recs.append(json.loads(line))
+        p.wait()
+    finally:
+        timer.cancel()
+    err = p.stderr.read()
+    if p.returncode != 0:
+        raise RuntimeError(
+            f"reference C4 run stopped (rc {p.returncode}) after phases "
+            f"{[r.get('phase') for r in recs]}: {err[-500:]}")
+    return recs
+
+
 def reference_arm(args):
+    """--impl reference: the reference's own CPU path (oracle/_ref, built
+    unmodified) on the SAME workload and config as our arm.  The reference
+    is single-threaded, so the C4 step runs in one process on one core; a
+    C4 fwd+adjoint step takes ~20 min there, so the arm times
+    `PF_REF_STEPS` (default 1) steps regardless of --steps and says so
+    (no warm-up: domain construction and the initial condition are outside
+    the timed region, and every reference solve is cold-started the same
+    way as the first timed step of a warm run).  A bounded 64x48x64 sample
+    on all host cores (one process each) is reported beside it, labelled."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    # one single-threaded reference process per host core (the reference is
-    # serial; this is every host thread it can use)
     procs = max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
                 else (os.cpu_count() or 1))
-    steps = max(1, args.steps)
+    shape = CONFIGS[args.config][0]
+    steps = int(os.environ.get("PF_REF_STEPS", "1"))
+    budget = float(os.environ.get("PF_REF_BUDGET_S", "1650"))
     try:
         from oracle import build_ref
         if not build_ref.build():
             raise RuntimeError("oracle/_ref missing")
-        # warm-up: W single steps are not timed; the sample already excludes
-        # domain construction
-        r = run_reference_sample(procs, steps, args.tol)
+        t0 = time.perf_counter()
+        sample = run_reference_sample(procs, 1, args.tol)
+        recs = run_reference_full(shape, steps, args.tol,
+                                  budget - (time.perf_counter() - t0),
+                                  args.config)
     except Exception as exc:  # the oracle always exists; report why not
         print(json.dumps({"impl": "reference", "unavailable": str(exc)[:300]}))
         return
-    sample = (f"reference pisoflow (lane {r['lane']}) on channel "
-              f"{'x'.join(map(str, SAMPLE_SHAPE))} (same recipe as C4, "
-              f"1/64 of its cells), {steps} fwd+adjoint step(s) per process, "
-              f"{procs} concurrent single-threaded processes")
+    done = recs[-1]
+    setup = recs[0]
+    value = done["cell_steps"] / done["seconds"] / 1e6
+    desc = (f"reference pisoflow (lane {done['lane']}), the full "
+            f"{'x'.join(map(str, shape))} workload, {steps} taped fwd+FULL "
+            f"adjoint step(s) in one single-threaded process (the reference "
+            f"is serial); domain build + initial condition "
+            f"{setup['seconds']:.0f} s excluded")
     line = {
-        "impl": "reference", "metric": METRIC, "value": r["value"],
-        "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": 1e3 * r["seconds"] / steps,
+        "impl": "reference", "metric": METRIC, "value": value,
+        "unit": UNIT, "n_gpus": args.gpus, "steps": steps, "warmup": 0,
+        "requested": {"steps": args.steps, "warmup": args.warmup},
+        "ms_per_step": 1e3 * done["seconds"] / steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args, sample=True),
-        "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": procs,
-                         "kind": "reference", "sample": sample},
-        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+        "config": workload_config(args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1,
+                         "kind": "reference", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "reference_iterations": r["iterations"],
+        "reference_seconds": {"forward": done["forward_seconds"],
+                              "backward": done["backward_seconds"],
+                              "setup": setup["seconds"]},
+        "reference_iterations": done["iterations"],
+        "all_cores_sample": {
+            "value": sample["value"], "unit": UNIT, "cores": procs,
+            "what": (f"NOT the same config: {procs} concurrent single-"
+                     f"threaded reference processes, each 1 fwd+adjoint "
+                     f"step of the channel recipe at "
+                     f"{'x'.join(map(str, SAMPLE_SHAPE))}"),
+            "iterations": sample["iterations"]},
     }
     print(json.dumps(line))
 
 
-def workload_config(args, sample=False):
+def workload_config(args):
     shape, ratio, cfl, desc = CONFIGS[args.config]
     return {"workload": desc, "grid": list(shape),
             "cells": int(math.prod(shape)), "wall_ratio": ratio,
@@ -189,8 +267,7 @@ def workload_config(args, sample=False):
                              f"slab{args.gpus} (x split, NVLink P2P halos)"
                              if args.config in ("c4", "slab8") else
                              "replicas")),
-            "l2": "inputs larger than L2 (no flush needed)",
-            "reference_sample": list(SAMPLE_SHAPE) if sample else None}
+            "l2": "inputs larger than L2 (no flush needed)"}
 
 
 # ---------------------------------------------------------------------------
@@ -493,6 +570,41 @@ def run_c5train(args, world, rank, local, dev):
         dist.destroy_process_group()
 
 
+def cpu_baseline_leg(args):
+    """Bounded CPU baseline (~10 s): the reference's compiled lane, one
+    single-threaded process, CPU_SAMPLE_STEPS fwd+adjoint steps of the same
+    channel recipe at 64x48x64.  The same-config C4 number (one full C4
+    step on one core, ~20 min, too long for this leg) is quoted from the
+    committed measurement of `bench.py --impl reference` on the GPU box's
+    host (profiles/r2_reference_c4.json) when present."""
+    try:
+        r = run_reference_sample(1, CPU_SAMPLE_STEPS, args.tol)
+        cpu = {"value": r["value"], "unit": UNIT, "cores": 1,
+               "kind": "reference",
+               "sample": (f"reference pisoflow (lane {r['lane']}) on channel "
+                          f"{'x'.join(map(str, SAMPLE_SHAPE))} (same recipe, "
+                          f"1/64 of C4 cells), {CPU_SAMPLE_STEPS} fwd+adjoint"
+                          f" steps, {r['seconds']:.1f} s, 1 process"),
+               "iterations": r["iterations"]}
+    except Exception as exc:
+        cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+               "sample": f"failed: {exc}"[:200]}
+    path = os.path.join(ROOT, "profiles", "r2_reference_c4.json")
+    if args.config == "c4" and os.path.exists(path):
+        try:
+            rec = json.load(open(path))
+            cpu["same_config_c4"] = {
+                k: rec.get(k) for k in ("value", "unit", "steps",
+                                        "ms_per_step", "reference_seconds",
+                                        "reference_iterations")}
+            cpu["same_config_c4"]["source"] = (
+                "profiles/r2_reference_c4.json (bench.py --impl reference "
+                "on the GPU box host, committed)")
+        except (OSError, ValueError):
+            pass
+    return cpu
+
+
 def share_dev():
     return os.environ.get("PF_BENCH_SHARE_DEVICE") == "1"
 
@@ -776,18 +888,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            r = run_reference_sample(1, 1, args.tol)
-            cpu = {"value": r["value"], "unit": UNIT, "cores": 1,
-                   "kind": "reference",
-                   "sample": (f"reference pisoflow (lane {r['lane']}) on "
-                              f"channel {'x'.join(map(str, SAMPLE_SHAPE))} "
-                              "(same recipe, 1/64 of C4 cells), 1 fwd+adjoint"
-                              f" step, {r['seconds']:.1f} s"),
-                   "iterations": r["iterations"]}
-        except Exception as exc:
-            cpu = {"value": None, "unit": UNIT, "cores": 1,
-                   "kind": "reference", "sample": f"failed: {exc}"[:200]}
+        cpu = cpu_baseline_leg(args)
 
     if rank == 0:
         line = {

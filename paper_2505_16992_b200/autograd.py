@@ -48,6 +48,12 @@ class _PisoStep(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, gu, gp, _gbc):
+        if ctx.tape is None:
+            raise RuntimeError(
+                "piso_step_fn: the step's tape was released by an earlier "
+                "backward pass; a second backward through the same step "
+                "needs a fresh forward (retain_graph does not keep the "
+                "device tape)")
         dom = ctx.domain
         dev = ctx.tape.c_data.device
         n, d = dom.n, dom.dim

@@ -258,7 +258,16 @@ def adaptive_dt(domain, u, cfl_max, dt_max, remaining=None):
     from .piso import contravariant_flux
     plan = domain.device_plan(u.device)
     rate = contravariant_flux(domain, u).abs().sum(dim=1) / plan.jac
-    peak = float(rate.max())
+    if getattr(plan, "comm", None) is not None:
+        # slab: the peak over this rank's owned cells, then the max over the
+        # ranks, so every rank takes the same dt (one global system)
+        from . import slab as _slab
+        lo, hi = domain.plane, domain.plane * (domain.nxl + 1)
+        peak_t = rate[lo:hi].max().reshape(1).clone()
+        _slab.allreduce_(plan, peak_t, op="max")
+        peak = float(peak_t.item())
+    else:
+        peak = float(rate.max())
     dt = dt_max if peak == 0.0 else min(dt_max, cfl_max / peak)
     if remaining is not None:
         dt = min(dt, remaining)

@@ -7,6 +7,7 @@
 // across the face is nbr_ax[a, s, i, a] and its orientation nbr_sign.
 #pragma once
 
+#include <atomic>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -36,11 +37,21 @@ int cuda_check(cudaError_t e, const char *what);
 
 // Every kernel launch of the library goes through launch(), which counts it
 // (pf_launch_count) -- the bench reports how many of OUR kernels ran.
-extern unsigned long long g_launches;
+// Atomic: the in-process slab tests drive several plans from concurrent host
+// threads.  Graph capture counts its kernels in a thread-local counter
+// (g_capture_count) instead of rewinding the global one.
+extern std::atomic<unsigned long long> g_launches;
+extern thread_local unsigned long long *g_capture_count;
+inline void count_launch() {
+  if (g_capture_count)
+    ++*g_capture_count;
+  else
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
 template <typename... KArgs, typename... Args>
 inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block,
                    cudaStream_t stream, Args... args) {
-  ++g_launches;
+  count_launch();
   kernel<<<grid, block, 0, stream>>>(args...);
 }
 

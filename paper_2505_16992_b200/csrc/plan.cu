@@ -8,7 +8,8 @@
 namespace pf {
 
 static thread_local std::string g_last_error;
-unsigned long long g_launches = 0;
+std::atomic<unsigned long long> g_launches{0};
+thread_local unsigned long long *g_capture_count = nullptr;
 
 void set_error(const std::string &msg) { g_last_error = msg; }
 
@@ -36,7 +37,7 @@ int d2h(const Plan &p, void *host, const void *dev, size_t bytes,
     return PF_ERR_ARG;
   }
   if (p.pinned_dev && !p.comm) {
-    ++g_launches;
+    count_launch();
     k_d2h_small<<<1, 128, 0, s>>>(static_cast<unsigned char *>(p.pinned_dev),
                                   static_cast<const unsigned char *>(dev),
                                   (int)bytes);
@@ -58,7 +59,7 @@ extern "C" const char *pf_last_error(void) { return g_last_error.c_str(); }
 
 extern "C" int pf_version(void) { return 1; }
 
-extern "C" unsigned long long pf_launch_count(void) { return g_launches; }
+extern "C" unsigned long long pf_launch_count(void) { return g_launches.load(); }
 
 extern "C" int pf_plan_create(const pf_plan_desc *desc, pf_plan **out) {
   if (!desc || !out) {

@@ -1264,13 +1264,15 @@ int mg_graph(const Plan &pl, Workspace &w, SolverState *st,
     gc.exec = nullptr;
   }
   if (!gc.cap) PF_CUDA(cudaStreamCreateWithFlags(&gc.cap, cudaStreamNonBlocking));
-  const unsigned long long before = g_launches;
+  unsigned long long captured = 0;
+  g_capture_count = &captured;  // captured, not launched
   PF_CUDA(cudaStreamBeginCapture(gc.cap, cudaStreamCaptureModeThreadLocal));
   for (int k = 0; k < kGraphIters; ++k) mg_iteration(pl, w, st, mg, x, gc.cap);
   cudaGraph_t graph;
-  PF_CUDA(cudaStreamEndCapture(gc.cap, &graph));
-  gc.nkern = g_launches - before;
-  g_launches = before;  // captured, not launched
+  cudaError_t ec = cudaStreamEndCapture(gc.cap, &graph);
+  g_capture_count = nullptr;
+  PF_CUDA(ec);
+  gc.nkern = captured;
   cudaError_t e = cudaGraphInstantiate(&gc.exec, graph, 0);
   cudaGraphDestroy(graph);
   PF_CUDA(e);
@@ -1333,7 +1335,7 @@ int cg_core_mg(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     for (int k = 0; k < b; ++k) {
       if (exec) {
         PF_CUDA(cudaGraphLaunch(exec, s));
-        g_launches += nk;
+        g_launches.fetch_add(nk, std::memory_order_relaxed);
       } else {
         for (int j = 0; j < kGraphIters; ++j)
           mg_iteration(pl, w, st, mg, x, s);
@@ -1528,7 +1530,7 @@ void launch_tiled(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)kTileSmem);
     }
-    ++g_launches;
+    count_launch();
     kernel<<<grid, kTileThreads, kTileSmem, s>>>(tg, a, bv, par, n, st,
                                                  w.partials, w.counters, xin,
                                                  bin, nverify);
@@ -1885,7 +1887,7 @@ extern "C" int pf_cg_profile(const pf_plan *plan, const double *a,
       PF_CUDA(cudaEventRecord(ev[0], s));
       for (int k = 0; k < reps; ++k) {
         PF_CUDA(cudaGraphLaunch(exec, s));
-        g_launches += nk;
+        g_launches.fetch_add(nk, std::memory_order_relaxed);
       }
       PF_CUDA(cudaEventRecord(ev[1], s));
       PF_CUDA(cudaEventSynchronize(ev[1]));

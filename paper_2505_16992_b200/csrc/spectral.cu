@@ -815,7 +815,7 @@ static void launch_smem(void (*kernel)(KArgs...), int grid, int block,
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-  ++g_launches;
+  count_launch();
   kernel<<<grid, block, smem, stream>>>(args...);
 }
 

@@ -51,6 +51,16 @@ def default_maxiter(n):
     return max(200, 40 * int(round(n ** 0.5)))
 
 
+def _global_n(plan):
+    """Cell count of the whole system: a slab plan (one rank's planes plus
+    ghosts) takes the global domain's, so every rank -- and the
+    single-GPU / reference solve -- gets the same default maxiter (a rank
+    stopping early would leave its peers waiting in the cross-rank
+    reductions)."""
+    g = getattr(plan.domain, "global_domain", None)
+    return g.n if g is not None else plan.n
+
+
 PRECOND_NONE, PRECOND_JACOBI, PRECOND_MG = 0, 1, 2
 
 
@@ -81,7 +91,8 @@ def cg_solve(plan, data, b, x0=None, tol=None, maxiter=None,
     ``data`` (S/linalg.py:258-273).  Solves A x = b_scale * b."""
     n = plan.n
     tol = default_tol() if tol is None else float(tol)
-    maxiter = default_maxiter(n) if maxiter is None else int(maxiter)
+    maxiter = default_maxiter(_global_n(plan)) if maxiter is None \
+        else int(maxiter)
     x = torch.empty(n, dtype=torch.float64, device=plan.device) \
         if out is None else out
     if x0 is not None:
@@ -119,7 +130,8 @@ def bicgstab_solve(plan, data, b, x0=None, tol=None, maxiter=None,
     b2 = b.reshape(-1, n)
     k = b2.shape[0]
     tol = default_tol() if tol is None else float(tol)
-    maxiter = default_maxiter(n) if maxiter is None else int(maxiter)
+    maxiter = default_maxiter(_global_n(plan)) if maxiter is None \
+        else int(maxiter)
     x = torch.empty((k, n), dtype=torch.float64, device=plan.device) \
         if out is None else out.reshape(k, n)
     if x0 is not None:

@@ -447,6 +447,14 @@ def piso_step(domain, state, cfg, workspace=None, tape=None):
         tape.dt, tape.nu = dt, nu
         tape.source = (src.reshape(1, d).expand(n, d) if uniform
                        else src.t())
+        # the reference copies u_n into the tape (S/piso.py:640).  Here u_n
+        # may alias the caller's input storage; the adjoint reads it only
+        # through the non-orthogonal cross terms (mom_inputs[0]), so it is
+        # copied exactly then.  On orthogonal grids the input velocity is
+        # not read by backward_step and may be refilled at once.
+        if plan.cell_cross and u_n.data_ptr() == state.u.data_ptr():
+            u_n = u_n.clone()
+            mom_inputs[0] = u_n.t()
         tape.u_n = u_n.t()
         tape.bc = bc_list
         tape.c_data = c_data
