@@ -121,14 +121,22 @@ def _compare(name, ref, ours, atol_rel=FIELD_TOL):
     if rg.bc:
         errs["grad_bc"] = RL.rel(np.concatenate([_np(b) for b in og.bc]),
                                  np.concatenate(rg.bc))
-    its = {"ours": [(d.momentum_iterations, d.pressure_iterations)
-                    for d in od] + [og.solve_iterations],
-           "reference": [(d.momentum_iterations, d.pressure_iterations)
-                         for d in rd] + [rg.solve_iterations]}
-    print(f"\n[{name}] iterations (momentum, pressure) per step + adjoint "
-          f"total: ours {its['ours']} reference {its['reference']}")
-    print(f"[{name}] relative errors: "
-          + ", ".join(f"{k}={v:.2e}" for k, v in errs.items()))
+    def its(diags, g):
+        mom = [d.momentum_iterations for d in diags]
+        prs = [d.pressure_iterations for d in diags]
+        if len(diags) > 4:   # long rollouts: totals
+            return (f"momentum {sum(mom)}, pressure {sum(prs)} over "
+                    f"{len(diags)} steps, adjoint {g.solve_iterations}")
+        return (f"momentum {mom}, pressure {prs}, adjoint "
+                f"{g.solve_iterations}")
+    print(f"\n[{name}] solver iterations: ours {its(od, og)}; reference "
+          f"{its(rd, rg)}")
+    worst = {}
+    for k, v in errs.items():
+        key = k.split("[")[0]
+        worst[key] = max(worst.get(key, 0.0), v)
+    print(f"[{name}] worst relative error (L-inf / max|ref|) per field: "
+          + ", ".join(f"{k}={v:.2e}" for k, v in worst.items()))
     bad = {k: v for k, v in errs.items() if not v <= atol_rel}
     assert not bad, f"{name}: parity beyond {atol_rel}: {bad}"
     return errs
