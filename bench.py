@@ -1,7 +1,9 @@
 """Benchmark: forward + adjoint PISO steps on the 3D turbulent channel.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c4|c5|c2|c1] [--no-cpu-baseline]
+                    [--config c4|c5|c5train|slab8] [--no-cpu-baseline]
+
+--gpus N > 1 without torchrun starts the N ranks itself.
 
 Metric (BASELINE.json): Mcell-steps/s of forward+adjoint PISO on the 3D
 channel; one "step" = one taped ``piso_step`` plus its ``backward_step``
@@ -58,6 +60,51 @@ CONFIGS = {
 }
 UNROLL = 16
 SAMPLE_SHAPE = (64, 48, 64)
+
+# 2D BASELINE configs (BASELINE.md §3a recipes): name -> description, tol.
+# One step = one taped piso_step + its FULL backward_step, as for C4.
+CASES2D = {
+    "c1": ("C1 lid-driven cavity 32x32 Re=100 (nu 0.01, dt 0.02), "
+           "fwd+adjoint", 1e-10),
+    "c2": ("C2 lid-driven cavity 1024x1024 wall-refined (ratio 1.0045) "
+           "Re=1000 (nu 1e-3, dt 25 dx_min), fwd+adjoint", 1e-8),
+    "c3": ("C3 obstacle (Karman) grid 2048x512 in 8 blocks, Re=100 "
+           "(inflow 1, nu 0.01, dt 0.0125), fwd+adjoint", 1e-8),
+}
+
+
+def case_2d(mesh, name, sample=False):
+    """Domain, nu, dt and initial velocity (n, 2) of a 2D config, built
+    with `mesh` -- ours or the reference's (same API: S/mesh.py:476-700).
+    `sample`: the same recipe at 1/16 of the cells (the bounded CPU
+    baseline of C2 / C3)."""
+    import numpy as np
+    if name == "c1":
+        dom = mesh.make_cavity((32, 32))
+        return dom, 0.01, 0.02, np.zeros((dom.n, 2))
+    if name == "c2":
+        m = 256 if sample else 1024
+        x = mesh.wall_refined_coords(m, 0.5, 1.0045)
+        blk = mesh.BlockSpec(mesh._grid_vertices(x, x))
+        bnd = {(0, a, s_): mesh.Dirichlet(0.0) for a in range(2)
+               for s_ in (0, 1)}
+        bnd[(0, 1, 1)] = mesh.Dirichlet((1.0, 0.0))
+        dom = mesh.Domain([blk], bnd)
+        return dom, 1e-3, 25.0 * float(np.diff(x).min()), np.zeros((dom.n, 2))
+    if name == "c3":
+        f = 4 if sample else 1
+
+        def inlet(fc):
+            return np.stack([np.ones(len(fc)), np.zeros(len(fc))], axis=-1)
+        dom = mesh.make_obstacle_grid(
+            domain_size=(32.0, 8.0), obstacle_center=(6.5, 4.0),
+            obstacle_size=(1.0, 1.0),
+            nx=(384 // f, 64 // f, 1600 // f), ny=(224 // f, 64 // f, 224 // f),
+            inlet=inlet)
+        u0 = np.zeros((dom.n, 2))
+        u0[:, 0] = 1.0
+        return dom, 0.01, 0.0125 * f, u0
+    raise KeyError(name)
 CPU_SAMPLE_STEPS = 4
 
 
@@ -67,7 +114,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c4",
+                    choices=sorted(CONFIGS) + sorted(CASES2D))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-iters", type=int, default=20)
     ap.add_argument("--tol", type=float, default=1e-8)
@@ -97,15 +145,27 @@ def reference_worker(args):
     sys.path.insert(0, build_ref.ref_path())
     import numpy as np
     from pisoflow import adjoint, kernels, mesh, piso
-    shape = tuple(int(v) for v in args.worker_shape.split(","))
-    _, ratio, cfl, _ = CONFIGS[args.config]
     tb = time.perf_counter()
-    dom = mesh.make_channel(shape, ratio=ratio)
-    state, nu, u_tau = piso.reichardt_init(dom, 180.0, perturbation=0.1,
-                                           seed=0)
-    dt = cfl * (2 * np.pi / shape[0]) / np.abs(state.u).max()
+    if args.config in CASES2D:
+        dom, nu, dt, u0 = case_2d(mesh, args.config,
+                                  sample=args.worker_shape == "sample")
+        state = piso.make_state(dom, u0=u0)
+        shape = (args.worker_shape,)
+
+        def source(u):
+            return None
+    else:
+        shape = tuple(int(v) for v in args.worker_shape.split(","))
+        _, ratio, cfl, _ = CONFIGS[args.config]
+        dom = mesh.make_channel(shape, ratio=ratio)
+        state, nu, u_tau = piso.reichardt_init(dom, 180.0, perturbation=0.1,
+                                               seed=0)
+        dt = cfl * (2 * np.pi / shape[0]) / np.abs(state.u).max()
+
+        def source(u):
+            return piso.wall_forcing_source(dom, u, nu)
     rng = np.random.default_rng(0)
-    w = rng.standard_normal((dom.n, 3))
+    w = rng.standard_normal((dom.n, dom.dim))
     ws = piso.PisoWorkspace(dom)
 
     def emit(**kw):
@@ -116,8 +176,8 @@ def reference_worker(args):
     iters, fwd_s, bwd_s = [], 0.0, 0.0
     for k in range(args.worker_steps):
         ta = time.perf_counter()
-        src = piso.wall_forcing_source(dom, state.u, nu)
-        cfg = piso.StepConfig(dt=dt, nu=nu, source=src, tol=args.tol)
+        cfg = piso.StepConfig(dt=dt, nu=nu, source=source(state.u),
+                              tol=args.tol)
         tape = piso.StepTape()
         state, dg = piso.piso_step(dom, state, cfg, ws, tape)
         tf = time.perf_counter()
@@ -145,9 +205,9 @@ def _worker_cmd(shape, steps, tol, config="c4"):
             "--worker-steps", str(steps), "--tol", str(tol)]
 
 
-def run_reference_sample(procs, steps, tol, shape=None):
+def run_reference_sample(procs, steps, tol, shape=None, config="c4"):
     """Run `procs` concurrent reference workers; aggregate Mcell-steps/s."""
-    cmd = _worker_cmd(shape or SAMPLE_SHAPE, steps, tol)
+    cmd = _worker_cmd(shape or SAMPLE_SHAPE, steps, tol, config)
     t0 = time.perf_counter()
     ps = [subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
                            text=True, cwd=ROOT) for _ in range(procs)]
@@ -207,15 +267,21 @@ def reference_arm(args):
         return
     procs = max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
                 else (os.cpu_count() or 1))
-    shape = CONFIGS[args.config][0]
-    steps = int(os.environ.get("PF_REF_STEPS", "1"))
+    is2d = args.config in CASES2D
+    if is2d:
+        args.tol = CASES2D[args.config][1]
+    shape = ("full",) if is2d else CONFIGS[args.config][0]
+    # C1 is small: all requested steps; the others one step (BASELINE.md
+    # §2: C2-C4 one taped step fwd + backward on one core)
+    steps = args.steps if args.config == "c1" else \
+        int(os.environ.get("PF_REF_STEPS", "1"))
     budget = float(os.environ.get("PF_REF_BUDGET_S", "1650"))
     try:
         from oracle import build_ref
         if not build_ref.build():
             raise RuntimeError("oracle/_ref missing")
         t0 = time.perf_counter()
-        sample = run_reference_sample(procs, 1, args.tol)
+        sample = None if is2d else run_reference_sample(procs, 1, args.tol)
         recs = run_reference_full(shape, steps, args.tol,
                                   budget - (time.perf_counter() - t0),
                                   args.config)
@@ -246,18 +312,26 @@ def reference_arm(args):
                               "backward": done["backward_seconds"],
                               "setup": setup["seconds"]},
         "reference_iterations": done["iterations"],
-        "all_cores_sample": {
+    }
+    if sample is not None:
+        line["all_cores_sample"] = {
             "value": sample["value"], "unit": UNIT, "cores": procs,
             "what": (f"NOT the same config: {procs} concurrent single-"
                      f"threaded reference processes, each 1 fwd+adjoint "
                      f"step of the channel recipe at "
                      f"{'x'.join(map(str, SAMPLE_SHAPE))}"),
-            "iterations": sample["iterations"]},
-    }
+            "iterations": sample["iterations"]}
     print(json.dumps(line))
 
 
 def workload_config(args):
+    if args.config in CASES2D:
+        desc, tol = CASES2D[args.config]
+        return {"workload": desc, "tol": tol, "gradient_path": "full",
+                "parallelism": "single" if args.gpus <= 1 else "replicas",
+                "l2": ("C1 fits in L2 (latency-bound, no flush)"
+                       if args.config == "c1" else
+                       "inputs larger than L2 (no flush needed)")}
     shape, ratio, cfl, desc = CONFIGS[args.config]
     return {"workload": desc, "grid": list(shape),
             "cells": int(math.prod(shape)), "wall_ratio": ratio,
@@ -383,7 +457,33 @@ KERNEL_BYTES = {
 # st: C rows 56 + per comp r, v read, t written (24)
 # xr: diag 8 + per comp x r/w, p, r, v, t, rhat read, r written (64)
 BI_BYTES = {"k_bi_pv": 56 + 3 * 48, "k_bi_st": 56 + 3 * 24,
-            "k_bi_xr": 8 + 3 * 64}
+            "k_bi_xr": 8 + 3 * 64,
+            # Neumann-2 passes: 6 off-diagonal rows + 1/A (no diagonal row);
+            # per component pv reads r, p, v, r^ and writes p', v'; st reads
+            # r, v' and writes t; xr on z reads z, p', r, v', t, r^ and
+            # writes z, r (no 1/A)
+            "k_bi_nm_pv": 48 + 8 + 3 * 48, "k_bi_nm_st": 48 + 8 + 3 * 24,
+            "k_bi_xr_z": 3 * 64}
+
+def kernel_bytes(nm, d):
+    """Algorithmic bytes per cell of kernel `nm` in d dimensions (the
+    tables above are the 3D figures; stencils carry 2d+1 rows, the face
+    form d faces, the multigrid transfers 1/2^d coarse values)."""
+    rows = 2 * d + 1
+    bi = {"k_bi_pv": 8 * rows + d * 48, "k_bi_st": 8 * rows + d * 24,
+          "k_bi_xr": 8 + d * 64, "k_bi_nm_pv": 16 * d + 8 + d * 48,
+          "k_bi_nm_st": 16 * d + 8 + d * 24, "k_bi_xr_z": d * 64}
+    if nm in bi:
+        return bi[nm]
+    co = 8.0 / 2 ** d
+    dep = {"k_cg_spmv_faces": 8 * (d + 2),
+           # stencil form (Jacobi plans: multi-block grids): rows + p + q
+           "k_cg_spmv": 8 * rows + 16,
+           "k_mg_resid_restrict (level 0)": 8 * (2 + d) + co,
+           "k_mg_prolong_resid (level 0)": 8 * (3 + d) + co,
+           "k_mg_smooth2_cg (level 0)": 56 + co}
+    return dep.get(nm, KERNEL_BYTES.get(nm))
+
 
 MG_NAMES = ["k_mg_smooth0 (level 0)", "k_mg_resid_restrict (level 0)",
             "mg coarse levels", "k_mg_prolong_resid (level 0)",
@@ -436,10 +536,12 @@ def measure_roofline(args, dom, plan, state, nu, dt, dev, per_step):
     bb = torch.randn((d, dom.n), dtype=torch.float64, device=dev)
     bi = {}
     for trans, tag in ((0, ""), (1, " (adjoint)")):
-        bm = (ctypes.c_double * 4)()
+        bm = (ctypes.c_double * 5)()
         _lib.call("pf_bicgstab_profile", plan.handle, _lib.ptr(c), trans, d,
                   _lib.ptr(bb), 8, _lib.ptr(plan.workspace), bm, plan.stream)
-        for j, nm in enumerate(("k_bi_pv", "k_bi_st", "k_bi_xr")):
+        names = (("k_bi_nm_pv", "k_bi_nm_st", "k_bi_xr_z") if bm[4] == 3
+                 else ("k_bi_pv", "k_bi_st", "k_bi_xr"))
+        for j, nm in enumerate(names):
             bi[nm + tag] = float(bm[j])
     peaks = {}
     try:
@@ -460,7 +562,7 @@ def measure_roofline(args, dom, plan, state, nu, dt, dev, per_step):
     allk.update(bi)
 
     def nbytes(nm):
-        return BI_BYTES.get(nm.replace(" (adjoint)", ""), KERNEL_BYTES.get(nm))
+        return kernel_bytes(nm.replace(" (adjoint)", ""), d)
 
     share = {nm: allk[nm] * launches[nm] / per_step["ms"] for nm in allk}
     top = max(share, key=share.get)
@@ -577,6 +679,25 @@ def cpu_baseline_leg(args):
     step on one core, ~20 min, too long for this leg) is quoted from the
     committed measurement of `bench.py --impl reference` on the GPU box's
     host (profiles/r2_reference_c4.json) when present."""
+    if args.config in CASES2D:
+        # C1: the full config (100 steps take ~2 s on one core); C2 / C3:
+        # one step of the same recipe at 1/16 of the cells
+        c1 = args.config == "c1"
+        try:
+            r = run_reference_sample(1, 100 if c1 else 4, args.tol,
+                                     ("full",) if c1 else ("sample",),
+                                     args.config)
+            what = ("the full C1 config, 100 fwd+adjoint steps" if c1 else
+                    f"the {args.config} recipe at 1/16 of the cells, 4 "
+                    f"fwd+adjoint steps")
+            return {"value": r["value"], "unit": UNIT, "cores": 1,
+                    "kind": "reference",
+                    "sample": (f"reference pisoflow (lane {r['lane']}): "
+                               f"{what}, {r['seconds']:.1f} s, 1 process"),
+                    "iterations": r["iterations"]}
+        except Exception as exc:
+            return {"value": None, "unit": UNIT, "cores": 1,
+                    "kind": "reference", "sample": f"failed: {exc}"[:200]}
     try:
         r = run_reference_sample(1, CPU_SAMPLE_STEPS, args.tol)
         cpu = {"value": r["value"], "unit": UNIT, "cores": 1,
@@ -617,6 +738,12 @@ def build_workload(args, dev, rank=0, world=1):
     import numpy as np
     import torch
     from paper_2505_16992_b200 import channel, mesh, piso, slab
+    if args.config in CASES2D:
+        dom, nu, dt, u0 = case_2d(mesh, args.config)
+        g = torch.Generator(device="cpu").manual_seed(0)
+        w = torch.randn((dom.n, 2), generator=g, dtype=torch.float64).to(dev)
+        state = piso.make_state(dom, u0=u0, device=dev)
+        return dom, state, nu, dt, (lambda u, nu_: None), w, None
     shape, ratio, cfl, _ = CONFIGS[args.config]
     dom = mesh.make_channel(shape, ratio=ratio)
     u0, nu, u_tau = channel.reichardt_velocity(dom, 180.0, perturbation=0.1,
@@ -635,12 +762,38 @@ def build_workload(args, dev, rank=0, world=1):
     return sd, state, nu, dt, slab.SlabWallForcing(sd, dev), wl, comm
 
 
+def self_launch(args):
+    """`bench.py --gpus N` (N > 1) outside torchrun: start the N ranks
+    ourselves (torch.distributed.run on 127.0.0.1), one per visible GPU, and
+    fail loudly when fewer than N GPUs are visible (PF_BENCH_SHARE_DEVICE=1:
+    every rank on cuda:0, a correctness run of the multi-rank path)."""
+    import socket
+    import torch
+    n = args.gpus
+    vis = torch.cuda.device_count()
+    if not share_dev() and vis < n:
+        raise SystemExit(f"bench.py --gpus {n}: only {vis} GPU(s) visible; "
+                         f"refusing to report a {n}-GPU number")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    return subprocess.call(cmd, cwd=ROOT)
+
+
 def main():
     args = parse()
     if args.reference_worker:
         return reference_worker(args)
     if args.impl == "reference":
         return reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
+    if args.config in CASES2D:
+        args.tol = CASES2D[args.config][1]
 
     import numpy as np
     import torch
@@ -897,7 +1050,10 @@ def main():
             "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if slabbed else "weak",
             "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reichardt_init seed 0, random cotangent)",
+            "data": ("synthetic (reichardt_init seed 0, random cotangent)"
+                     if args.config not in CASES2D else
+                     "synthetic (rest / uniform-inflow start, random "
+                     "cotangent)"),
             "config": workload_config(args),
             "roofline": roofline,
             "cpu_baseline": cpu,
@@ -916,4 +1072,5 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    rc = main()
+    sys.exit(rc if isinstance(rc, int) else 0)

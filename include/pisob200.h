@@ -59,6 +59,10 @@ extern "C" {
 #define PF_PRECOND_NONE 0
 #define PF_PRECOND_JACOBI 1
 #define PF_PRECOND_MG 2
+/* BiCGStab only: two Jacobi sweeps, M^-1 = D^-1 (2I - A D^-1), fused into
+ * the tiled passes (single-device 3D boxes with whole 8 x 32 Y/Z tiles);
+ * elsewhere it runs as PF_PRECOND_JACOBI */
+#define PF_PRECOND_NEUMANN2 3
 
 #define PF_GEOM_NONE (-1)
 #define PF_GEOM_MULTIGRID 0
@@ -241,8 +245,9 @@ PF_API int pf_mg_kind(const pf_plan *plan);
 PF_API int pf_mg_setup(const pf_plan *plan, const double *k,
                        void *mg_workspace, void *stream);
 
-/* ncomp independent Jacobi-preconditioned BiCGStab solves sharing matrix `a`
- * (transpose != 0 solves with A^t) -- bicgstab_solve / _bicgstab_core,
+/* ncomp independent preconditioned BiCGStab solves sharing matrix `a`
+ * (transpose != 0 solves with A^t); precond PF_PRECOND_NONE, _JACOBI or
+ * _NEUMANN2 (see above) -- bicgstab_solve / _bicgstab_core,
  * S/linalg.py:173-212, 276-281; the predictor loop S/piso.py:583-590 and the
  * adjoint momentum solve S/adjoint.py:369-380.  One report per component. */
 PF_API int pf_bicgstab_solve(const pf_plan *plan, const double *a, int32_t transpose,
@@ -268,10 +273,12 @@ PF_API int pf_cg_profile(const pf_plan *plan, const double *a,
                          double *ms_host, void *stream);
 
 /* Live per-pass timing of the batched BiCGStab iteration (bench.py roofline):
- * `iters` Jacobi-preconditioned iterations on `ncomp` right-hand sides of the
- * operator a (transposed if `transpose`), each pass bracketed by CUDA events
- * on `stream`.  ms_host[0..3] = mean ms of pass pv, pass st, pass xr and the
- * whole iteration.  Not part of the reference interface. */
+ * `iters` iterations with the production preconditioner (Neumann-2 where it
+ * runs, else Jacobi) on `ncomp` right-hand sides of the operator a
+ * (transposed if `transpose`), each pass bracketed by CUDA events on
+ * `stream`.  ms_host[0..3] = mean ms of pass pv, pass st, pass xr and the
+ * whole iteration; ms_host[4] = the preconditioner timed (1 Jacobi, 3
+ * Neumann-2).  Not part of the reference interface. */
 PF_API int pf_bicgstab_profile(const pf_plan *plan, const double *a,
                                int32_t transpose, int32_t ncomp,
                                const double *b, int32_t iters,

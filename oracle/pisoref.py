@@ -310,7 +310,11 @@ def cg(dom, st, b, x0=None, tol=1e-8, maxiter=None, precond="jacobi",
 def bicgstab(dom, st, b, x0=None, tol=1e-8, maxiter=None, precond="jacobi",
              transpose=False):
     """Restatement of _bicgstab_core (S/linalg.py:173-212) with the same
-    wrapper semantics.  Returns (x, converged, iterations)."""
+    wrapper semantics.  Returns (x, converged, iterations).  precond:
+    "jacobi", or "neumann2" -- the product's two-sweep Jacobi polynomial
+    M^-1 = D^-1 - D^-1 N D^-1 (N = A - D), checked here as a plain
+    right preconditioner (the product keeps the iterate as x0 + M^-1 z,
+    which is the same sequence of iterates)."""
     n = dom.n
     if maxiter is None:
         maxiter = max(200, 40 * int(round(n ** 0.5)))
@@ -325,7 +329,12 @@ def bicgstab(dom, st, b, x0=None, tol=1e-8, maxiter=None, precond="jacobi",
 
     def core(x, pc, mi):
         def M(v):
-            return v / st[0] if pc else v
+            if not pc:
+                return v
+            g = v / st[0]
+            if precond != "neumann2":
+                return g
+            return g - (A(g) - st[0] * g) / st[0]
         r = b - A(x)
         if np.linalg.norm(r) <= tol_abs:
             return x, True, 0

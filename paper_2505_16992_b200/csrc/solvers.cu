@@ -645,10 +645,16 @@ __global__ void __launch_bounds__(kBlock)
 // x += alpha phat + omega shat; r = s - omega t; |r|, r^.r -> next beta.
 // Two cells per thread with 128-bit loads and stores (the owned range is
 // split into an even-aligned vector part and scalar edges).
+//
+// kZ (Neumann-2 passes): x is the preconditioned iterate z (x = x0 + M^-1 z
+// is formed once at the end), so z += alpha p' + omega s with no division;
+// zfirst: the first iteration's z starts from 0 (it is neither read nor
+// memset).
+template <bool kZ = false>
 __global__ void __launch_bounds__(kBlock)
     k_bi_xr(const double *__restrict__ a, BiVecs w, int par,
             double *__restrict__ x, int32_t n, Rng rg, SolverState *st,
-            double *partials, unsigned *counter) {
+            double *partials, unsigned *counter, int zfirst = 0) {
   if (st->all_done) return;
   const int nc = st->ncomp;
   int act[3], pend[3];
@@ -662,11 +668,13 @@ __global__ void __launch_bounds__(kBlock)
   const double *__restrict__ p1 = w.p[par ^ 1];
   const double *__restrict__ v1 = w.v[par ^ 1];
   double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const bool z0 = kZ && zfirst;
   auto cell = [&](int32_t i) {
-    const double di = w.dinv[i];
+    const double di = kZ ? 1.0 : w.dinv[i];
     _Pragma("unroll") for (int q = 0; q < 3; ++q) {
       if (q >= nc) break;
       const int64_t o = (int64_t)q * n + i;
+      if (z0 && (act[q] || pend[q])) x[o] = 0.0;
       if (pend[q]) x[o] += alpha[q] * (p1[o] * di);
       if (!act[q]) continue;
       const double phat = p1[o] * di;
@@ -692,14 +700,16 @@ __global__ void __launch_bounds__(kBlock)
   for (int32_t k = v0 + 2 * tid; k + 1 < v1e; k += 2 * nth) {
     // every load of the three components first (the stores below cannot
     // then serialise them), then the updates
-    const double2 di = *reinterpret_cast<const double2 *>(di_ + k);
+    const double2 di = kZ ? make_double2(1.0, 1.0)
+                          : *reinterpret_cast<const double2 *>(di_ + k);
     double2 pp[3], xx[3], rr[3], vv[3], tt[3], rh[3];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
       if (q >= nc || !(act[q] || pend[q])) continue;
       const int64_t o = (int64_t)q * n + k;
       pp[q] = *reinterpret_cast<const double2 *>(p1 + o);
-      xx[q] = *reinterpret_cast<const double2 *>(x + o);
+      xx[q] = z0 ? make_double2(0.0, 0.0)
+                 : *reinterpret_cast<const double2 *>(x + o);
       if (!act[q]) continue;
       rr[q] = *reinterpret_cast<const double2 *>(rr_ + o);
       vv[q] = *reinterpret_cast<const double2 *>(v1 + o);
@@ -1157,6 +1167,8 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+#include "bicg_nm.cuh"
+
 }  // namespace pf
 
 // ===========================================================================
@@ -1604,6 +1616,62 @@ bool tile_geo(const Plan &pl, const V &v, TileGeo &tg) {
   return true;
 }
 
+constexpr int kPrecondNeumann2 = 3;
+
+// tile geometry of the Neumann-2 passes: the tiled geometry with chunks
+// costed at xc + 4 planes (two prologue planes per stencil stage), two
+// CTAs per SM; single-device plans only
+template <class V>
+bool nm_geo(const Plan &pl, const V &v, TileGeo &tg) {
+  if (pl.slab || getenv("PF_NO_NEUMANN")) return false;
+  if (!tile_geo(pl, v, tg)) return false;
+  if (tg.X < 4) return false;
+  const int32_t nx = tg.x1 - tg.x0;
+  const int64_t R = 2 * (int64_t)pl.num_sms;
+  const int64_t ncols = (int64_t)tg.ty_tiles * tg.tz_tiles;
+  int64_t best = -1;
+  for (int32_t xc = 1; xc <= std::max(1, nx); ++xc) {
+    const int64_t tiles = ncols * ((nx + xc - 1) / xc);
+    const int64_t cost = (tiles + R - 1) / R * (xc + 4);
+    if (best < 0 || cost <= best) {
+      best = cost;
+      tg.xc = xc;
+    }
+  }
+  tg.chunks = (nx + tg.xc - 1) / tg.xc;
+  tg.ntiles = tg.ty_tiles * tg.tz_tiles * tg.chunks;
+  return true;
+}
+
+template <bool kTrans, int MODE>
+void launch_nm(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
+               const BiVecs &bv, int par, int64_t n, SolverState *st,
+               Workspace &w, int first = 0, const double *zin = nullptr,
+               double *xout = nullptr) {
+  auto go = [&](auto kernel) {
+    static std::mutex mu;
+    static std::set<const void *> done;
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      if (done.insert(reinterpret_cast<const void *>(kernel)).second)
+        cudaFuncSetAttribute(kernel,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kNmSmem);
+    }
+    count_launch();
+    kernel<<<grid, kTileThreads, kNmSmem, s>>>(tg, a, bv, par, n, st,
+                                               w.partials, w.counters, zin,
+                                               xout);
+  };
+  if constexpr (MODE == 0) {
+    if (first) {
+      go(k_bi_nm<kTrans, MODE, true>);
+      return;
+    }
+  }
+  go(k_bi_nm<kTrans, MODE, false>);
+}
+
 template <class V, bool kTrans>
 int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
             SolverState &hs, const double *a, const double *b, double *x,
@@ -1623,9 +1691,16 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   bv.dinv = base + 7 * len;
   const int ge = grid_for(pl.i1 - pl.i0), gr = std::min(ge, pl.red_blocks);
   const Rng rg = plan_range(pl);
-  TileGeo tg;
+  TileGeo tg, tgn;
   const bool tiled = tile_geo(pl, v, tg);
   const int tgrid = tiled ? std::min(tg.ntiles, pl.red_blocks) : 0;
+  // Neumann-2 (PRECOND_NEUMANN2) runs fused on single-device tiled boxes;
+  // elsewhere (generic grids, slab plans: their ghost region is one plane
+  // deep) the request degrades to Jacobi
+  const bool nm = precond == kPrecondNeumann2 && nm_geo(pl, v, tgn);
+  if (precond == kPrecondNeumann2 && !nm) precond = 1;
+  const int ngrid = nm ? std::min(tgn.ntiles, 2 * pl.num_sms) : 0;
+  double *z = base + 8 * len;  // the preconditioned iterate (nm)
   launch(k_bi_reset, 1, 1, s, st, ncomp, maxiter, precond, tol, fresh, mask);
   // the tiled init pass forms |b| itself
   if (fresh && !tiled)
@@ -1661,20 +1736,29 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     for (int k = 0; k < bsz; ++k) {
       const int par = (launched + k) & 1;
       halo(pl, s, {{bv.r, ncomp}, {bv.p[par], ncomp}});
-      if (tiled)
+      if (nm)
+        launch_nm<kTrans, 0>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w,
+                             launched + k == 0);
+      else if (tiled)
         launch_tiled<kTrans, 0>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w,
                                 nullptr, nullptr, 0, launched + k == 0);
       else
         launch(k_bi_pv<V, kTrans>, gr, kBlock, s, v, a, bv, par, st,
                w.partials, w.counters);
       halo(pl, s, {{bv.v[par ^ 1], ncomp}});
-      if (tiled)
+      if (nm)
+        launch_nm<kTrans, 1>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w);
+      else if (tiled)
         launch_tiled<kTrans, 1>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
       else
         launch(k_bi_st<V, kTrans>, gr, kBlock, s, v, a, bv, par, st,
                w.partials, w.counters);
-      launch(k_bi_xr, gr, kBlock, s, a, bv, par, x, n, rg, st, w.partials,
-             w.counters);
+      if (nm)
+        launch(k_bi_xr<true>, gr, kBlock, s, a, bv, par, z, n, rg, st,
+               w.partials, w.counters, (int)(launched + k == 0));
+      else
+        launch(k_bi_xr<false>, gr, kBlock, s, a, bv, par, x, n, rg, st,
+               w.partials, w.counters, 0);
     }
     PF_LAUNCH_CHECK("bicgstab iterations");
     launched += bsz;
@@ -1688,6 +1772,7 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     for (int q = 0; q < ncomp; ++q) lock = std::max(lock, (int)hs.c[q].iter);
     pl.bi_hint[kTrans ? 1 : 0] = lock;
   }
+  if (nm) launch_nm<kTrans, 2>(tgn, ngrid, s, a, bv, 0, (int64_t)n, st, w, 0, z, x);
   launch(k_bi_finish, ge, kBlock, s, x, n, rg, st);
   halo(pl, s, {{x, ncomp}});
   if (tiled)
@@ -1933,8 +2018,9 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
   cudaStream_t s = S(stream);
   const int32_t n = (int32_t)pl.d.n;
   const int64_t len = (int64_t)ncomp * n;
-  // x lives past the seven solver vectors and 1 / diag
-  double *x = w.vecs + 8 * len;
+  // x lives past the seven solver vectors, 1 / diag and z
+  double *x = w.vecs + 9 * len;
+  double *z = w.vecs + 8 * len;
   return dispatch(pl, [&](auto v) {
     using V = decltype(v);
     BiVecs bv;
@@ -1948,12 +2034,16 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
     bv.dinv = w.vecs + 7 * len;
     const int gr = std::min(grid_for(pl.i1 - pl.i0), pl.red_blocks);
     const Rng rg = plan_range(pl);
-    TileGeo tg;
+    TileGeo tg, tgn;
     const bool tiled = tile_geo(pl, v, tg);
     const int tgrid = tiled ? std::min(tg.ntiles, pl.red_blocks) : 0;
+    // the production preconditioner: Neumann-2 where it runs, else Jacobi
+    const bool nm = nm_geo(pl, v, tgn);
+    const int ngrid = nm ? std::min(tgn.ntiles, 2 * pl.num_sms) : 0;
     PF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * len, s));
     // tol 0: the recurrence never converges inside the timed iterations
-    launch(k_bi_reset, 1, 1, s, st, ncomp, iters + 1, 1, 0.0, 1, 0x7u);
+    launch(k_bi_reset, 1, 1, s, st, ncomp, iters + 1, nm ? kPrecondNeumann2 : 1,
+           0.0, 1, 0x7u);
     launch(k_bi_bnorm, gr, kBlock, s, b, n, rg, st, w.partials, w.counters);
     halo(pl, s, {{x, ncomp}});
     if (transpose)
@@ -1970,7 +2060,11 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
       const int par = k & 1;
       halo(pl, s, {{bv.r, ncomp}, {bv.p[par], ncomp}});
       PF_CUDA(cudaEventRecord(ev[0], s));
-      if (tiled && transpose)
+      if (nm && transpose)
+        launch_nm<true, 0>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w, k == 0);
+      else if (nm)
+        launch_nm<false, 0>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w, k == 0);
+      else if (tiled && transpose)
         launch_tiled<true, 0>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
       else if (tiled)
         launch_tiled<false, 0>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
@@ -1982,7 +2076,11 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
                w.partials, w.counters);
       halo(pl, s, {{bv.v[par ^ 1], ncomp}});
       PF_CUDA(cudaEventRecord(ev[1], s));
-      if (tiled && transpose)
+      if (nm && transpose)
+        launch_nm<true, 1>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w);
+      else if (nm)
+        launch_nm<false, 1>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w);
+      else if (tiled && transpose)
         launch_tiled<true, 1>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
       else if (tiled)
         launch_tiled<false, 1>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
@@ -1993,8 +2091,12 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
         launch(k_bi_st<V, false>, gr, kBlock, s, v, a, bv, par, st,
                w.partials, w.counters);
       PF_CUDA(cudaEventRecord(ev[2], s));
-      launch(k_bi_xr, gr, kBlock, s, a, bv, par, x, n, rg, st, w.partials,
-             w.counters);
+      if (nm)
+        launch(k_bi_xr<true>, gr, kBlock, s, a, bv, par, z, n, rg, st,
+               w.partials, w.counters, (int)(k == 0));
+      else
+        launch(k_bi_xr<false>, gr, kBlock, s, a, bv, par, x, n, rg, st,
+               w.partials, w.counters, 0);
       PF_CUDA(cudaEventRecord(ev[3], s));
       PF_CUDA(cudaEventSynchronize(ev[3]));
       for (int j = 0; j < 3; ++j) {
@@ -2016,6 +2118,7 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
       return PF_ERR_ARG;
     }
     for (int j = 0; j < 4; ++j) ms_host[j] = tot[j] / iters;
+    ms_host[4] = nm ? kPrecondNeumann2 : 1;
     return PF_OK;
   });
 }

@@ -61,7 +61,7 @@ def _global_n(plan):
     return g.n if g is not None else plan.n
 
 
-PRECOND_NONE, PRECOND_JACOBI, PRECOND_MG = 0, 1, 2
+PRECOND_NONE, PRECOND_JACOBI, PRECOND_MG, PRECOND_NEUMANN2 = 0, 1, 2, 3
 
 
 def _precond_flag(precond):
@@ -74,6 +74,8 @@ def _precond_flag(precond):
         return PRECOND_JACOBI
     if precond in ("mg", "multigrid"):
         return PRECOND_MG
+    if precond in ("neumann2", "poly2"):
+        return PRECOND_NEUMANN2
     return -1        # auto
 
 
@@ -138,7 +140,10 @@ def bicgstab_solve(plan, data, b, x0=None, tol=None, maxiter=None,
         x.copy_(x0.reshape(k, n))
     reps = (_lib.SolverReportC * k)()
     pc = _precond_flag(precond)
-    pc = PRECOND_JACOBI if pc in (-1, PRECOND_MG) else pc
+    # auto / "ilu0": the fused two-sweep Jacobi polynomial where the plan
+    # runs it (the library degrades it to Jacobi elsewhere)
+    pc = PRECOND_NEUMANN2 if pc == -1 else \
+        PRECOND_JACOBI if pc == PRECOND_MG else pc
     _lib.call("pf_bicgstab_solve", plan.handle, _lib.ptr(data),
               int(bool(transpose)), k, _lib.ptr(b2), _lib.ptr(x),
               int(x0 is not None), tol, maxiter, pc,

@@ -24,7 +24,9 @@ def _system(shape, seed=0):
     return dom, c, b
 
 
-def _solve(dom, c, b, transpose, tiled, tol=1e-12):
+def _solve(dom, c, b, transpose, tiled, tol=1e-12, precond="jacobi"):
+    """Jacobi by default: the generic kernels run Jacobi, so iteration counts
+    compare one to one (the Neumann-2 passes: test_gpu_neumann.py)."""
     from paper_2505_16992_b200 import linalg
     plan = dom.device_plan(b.device)
     if tiled:
@@ -33,7 +35,7 @@ def _solve(dom, c, b, transpose, tiled, tol=1e-12):
         os.environ["PF_NO_TILED"] = "1"
     try:
         x, reps = linalg.bicgstab_solve(plan, c, b, tol=tol,
-                                        transpose=transpose)
+                                        transpose=transpose, precond=precond)
     finally:
         os.environ.pop("PF_NO_TILED", None)
     torch.cuda.synchronize()
@@ -83,6 +85,7 @@ def test_tiled_slab_matches_single_domain():
         with torch.cuda.stream(s):
             T._prewarm(ready)
             plan = slabs[r].device_plan(b.device)
+            # slab plans run the Neumann-2 request as Jacobi
             res[r] = linalg.bicgstab_solve(plan, cs[r], bs[r], tol=1e-12)
             s.synchronize()
 

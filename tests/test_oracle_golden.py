@@ -96,3 +96,20 @@ def test_oracle_krylov_restatement_converges_to_exact():
     y, ok, it = O.bicgstab(dom, t.C, t.rhs[:, 0], tol=1e-12)
     assert ok
     assert G.rel(y, t.u_star[:, 0]) < 1e-10
+
+
+@pytest.mark.parametrize("transpose", [False, True])
+def test_oracle_neumann2_restatement(transpose):
+    """The two-sweep Jacobi polynomial preconditioner of the product's
+    BiCGStab (csrc/bicg_nm.cuh) in the oracle's Krylov restatement: same
+    solution as the exact solve, fewer iterations than Jacobi."""
+    g = G.load("channel")
+    dom = G.build("channel")
+    C = g["s0_C"]
+    b = np.random.default_rng(0).standard_normal(dom.n)
+    ex = O.solve_exact(dom, C, b, transpose=transpose)
+    xj, okj, itj = O.bicgstab(dom, C, b, tol=1e-12, transpose=transpose)
+    xn, okn, itn = O.bicgstab(dom, C, b, tol=1e-12, precond="neumann2",
+                              transpose=transpose)
+    assert okj and okn and itn < itj
+    assert G.rel(xn, ex) < 1e-10

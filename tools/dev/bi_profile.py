@@ -15,7 +15,7 @@ c = piso.assemble_momentum(dom, u0, nu, dt)
 b = torch.randn((3, dom.n), dtype=torch.float64, device=dev)
 n = dom.n
 for trans in (0, 1):
-    ms = (ctypes.c_double * 4)()
+    ms = (ctypes.c_double * 5)()
     for rep in range(2):
         _lib.call("pf_bicgstab_profile", plan.handle, _lib.ptr(c), trans, 3, _lib.ptr(b), 8, _lib.ptr(plan.workspace), ms, plan.stream)
     gbs = [200 * n / (ms[0] * 1e6), 128 * n / (ms[1] * 1e6), 200 * n / (ms[2] * 1e6)]
