@@ -363,6 +363,23 @@ PF_API int pf_adj_momentum_cross(const pf_plan *plan, const double *u,
                                  double *dnu_dev, void *workspace,
                                  void *stream);
 
+/* ---- standalone building blocks (the public stage API) ------------------- */
+
+/* wide_grad, S/piso.py:172-209: out (d, n) = wide central differences of
+ * phi (n) along every grid axis; variant 0 "mirror", 1 "onesided", 2 "face"
+ * (bc_cells (2d, n): row 2a+s holds the prescribed face values of the cells
+ * missing neighbour (a, s); null for the other variants).  Not on slab
+ * plans. */
+PF_API int pf_wide_grad(const pf_plan *plan, const double *phi,
+                        int32_t variant, const double *bc_cells, double *out,
+                        void *stream);
+/* wide_grad_adjoint, S/piso.py:218-264: out (n) = the adjoint w.r.t. phi of
+ * cot (d, n); face variant: bc_cot (2d, n) receives the cotangent of the
+ * prescribed face values (may be null). */
+PF_API int pf_wide_grad_adjoint(const pf_plan *plan, const double *cot,
+                                int32_t variant, double *out, double *bc_cot,
+                                void *stream);
+
 /* y += alpha x over len entries (device vectors) */
 PF_API int pf_axpy(const pf_plan *plan, double alpha, const double *x,
                    double *y, int64_t len, void *stream);

@@ -119,6 +119,8 @@ _SIGS = {
     "pf_adj_momentum_cross": [c_ptr, c_ptr, c_dbl, c_ptr, c_ptr, c_int,
                               c_ptr, c_ptr, c_ptr],
     "pf_axpy": [c_ptr, c_dbl, c_ptr, c_ptr, c_i64, c_ptr],
+    "pf_wide_grad": [c_ptr, c_ptr, c_int, c_ptr, c_ptr, c_ptr],
+    "pf_wide_grad_adjoint": [c_ptr, c_ptr, c_int, c_ptr, c_ptr, c_ptr],
     "pf_advective_outflow_update": [c_ptr, c_ptr, c_ptr, c_dbl, c_ptr,
                                     ctypes.POINTER(c_dbl), c_ptr],
     "pf_reduce_sum": [c_ptr, c_ptr, c_i64, c_ptr, ctypes.POINTER(c_dbl),

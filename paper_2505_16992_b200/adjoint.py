@@ -224,6 +224,122 @@ def backward_step(domain, tape, cot, path=GradientPath.FULL, tol=None,
                      reports=reports)
 
 
+# ---------------------------------------------------------------------------
+# stage API (S/adjoint.py:78-205): the adjoint building blocks on their own.
+# backward_step chains the same kernels; these wrappers expose them with the
+# reference's arguments (per-cell device tensors; matrix cotangents in this
+# package's stencil / face layout instead of CSR pattern values).
+
+
+def backward_correct_velocity(domain, p, a_diag, cot_u):
+    """Reverse of u = h - A^-1 T^t grad_xi(p) (S/adjoint.py:78-91).
+    Returns (dA, dp, dh).  Kernel: pf_bwd_correct_velocity."""
+    from .piso import _cdiag
+    plan = domain.device_plan(cot_u.device)
+    n, d = domain.n, domain.dim
+    da = torch.zeros(n, dtype=F64, device=plan.device)
+    dp = torch.empty(n, dtype=F64, device=plan.device)
+    cu = soa(cot_u, n, d, plan.device)
+    _lib.call("pf_bwd_correct_velocity", plan.handle,
+              _lib.ptr(scalar_field(p, n, plan.device)),
+              _lib.ptr(_cdiag(a_diag, n, plan.device)), _lib.ptr(cu),
+              _lib.ptr(da), _lib.ptr(dp), _lib.ptr(None),
+              _lib.ptr(plan.workspace), plan.stream)
+    return da, dp, cu.clone().t()
+
+
+def _adj_divergence_rhs(domain, cot_b):
+    """Adjoint of divergence_rhs in (h, bc) (S/adjoint.py:137-153).
+    Returns (dh (n, d), [dbc (m, d) per boundary face])."""
+    plan = domain.device_plan(cot_b.device)
+    n, d = domain.n, domain.dim
+    dh = torch.zeros((d, n), dtype=F64, device=plan.device)
+    dbc = torch.zeros((d, plan.m), dtype=F64, device=plan.device) \
+        if plan.m else None
+    _lib.call("pf_adj_divergence_rhs", plan.handle,
+              _lib.ptr(scalar_field(cot_b, n, plan.device)), 1.0,
+              _lib.ptr(dh), _lib.ptr(dbc), plan.stream)
+    return dh.t(), bc_views(plan, dbc)
+
+
+def _adj_pressure_cross(domain, a_inv, p_prev, cot_out):
+    """Adjoint of the lagged non-orthogonal pressure fluxes
+    (S/adjoint.py:156-178).  Returns (dp_prev, d_ainv)."""
+    from .piso import _cdiag
+    plan = domain.device_plan(cot_out.device)
+    n = domain.n
+    dp = torch.zeros(n, dtype=F64, device=plan.device)
+    if not plan.cell_cross:
+        return dp, torch.zeros(n, dtype=F64, device=plan.device)
+    ainv = scalar_field(a_inv, n, plan.device)
+    a = 1.0 / ainv
+    da = torch.zeros(n, dtype=F64, device=plan.device)
+    _lib.call("pf_adj_pressure_cross", plan.handle,
+              _lib.ptr(_cdiag(a, n, plan.device)),
+              _lib.ptr(scalar_field(p_prev, n, plan.device)),
+              _lib.ptr(scalar_field(cot_out, n, plan.device)), 1.0,
+              _lib.ptr(da), _lib.ptr(dp), _lib.ptr(plan.workspace),
+              plan.stream)
+    # the kernel accumulates the cotangent of A; a_inv = 1 / A
+    return dp, -da * a * a
+
+
+def _adj_momentum_cross(domain, u_cross, nu, cot_out):
+    """Adjoint of the lagged non-orthogonal viscous fluxes
+    (S/adjoint.py:181-205).  Returns (du_cross (n, d), dnu)."""
+    plan = domain.device_plan(cot_out.device)
+    n, d = domain.n, domain.dim
+    du = torch.zeros((d, n), dtype=F64, device=plan.device)
+    if not plan.cell_cross:
+        return du.t(), 0.0
+    dnu = torch.zeros(1, dtype=F64, device=plan.device)
+    _lib.call("pf_adj_momentum_cross", plan.handle,
+              _lib.ptr(soa(u_cross, n, d, plan.device)), float(nu),
+              _lib.ptr(soa(cot_out, n, d, plan.device)), _lib.ptr(du), 1,
+              _lib.ptr(dnu), _lib.ptr(plan.workspace), plan.stream)
+    return du.t(), float(dnu.item())
+
+
+def backward_pressure_solve(domain, p_data, p_sol, cot_p, tol=None,
+                            maxiter=None, reports=None):
+    """Adjoint of the zero-mean pressure solve (S/adjoint.py:94-113):
+    project cot_p to zero mean, solve (-P) y = chat with the same operator,
+    dP = y (x) p on the pattern, db = -y.  ``p_data`` is the P stencil
+    (2d+1, n) (tape.p_data); dP is returned in face form (2d, n): dP[f, i]
+    = y_i (p_nb(i,f) - p_i), the on-pattern values folded with the diagonal
+    as backward_pressure_matrix consumes them.  Returns (dP, db)."""
+    plan = domain.device_plan(cot_p.device)
+    n, d = domain.n, domain.dim
+    chat = scalar_field(cot_p, n, plan.device)
+    chat = chat - chat.mean()
+    dkf = torch.zeros((2 * d, n), dtype=F64, device=plan.device)
+    if not bool(torch.any(chat != 0)):
+        return dkf, torch.zeros(n, dtype=F64, device=plan.device)
+    y, rep = cg_solve(plan, -p_data, chat, tol=tol, maxiter=maxiter,
+                      zero_mean=True, stage="adjoint_pressure")
+    if reports is not None:
+        reports.append(rep)
+    _lib.call("pf_bwd_pressure_outer", plan.handle, _lib.ptr(y),
+              _lib.ptr(scalar_field(p_sol, n, plan.device)), _lib.ptr(dkf),
+              plan.stream)
+    return dkf, -y
+
+
+def backward_pressure_matrix(domain, a_inv, dP):
+    """Chain dP (face form, from backward_pressure_solve) through the
+    face-mean pressure assembly back to the diagonal A (S/adjoint.py:
+    116-134): returns -a_inv^2 g_ainv, the cotangent of A."""
+    from .piso import _cdiag
+    plan = domain.device_plan(dP.device)
+    n = domain.n
+    ainv = scalar_field(a_inv, n, plan.device)
+    da = torch.zeros(n, dtype=F64, device=plan.device)
+    _lib.call("pf_bwd_pressure_matrix", plan.handle,
+              _lib.ptr(_cdiag(1.0 / ainv, n, plan.device)),
+              _lib.ptr(dP.contiguous()), _lib.ptr(da), plan.stream)
+    return da
+
+
 def backward_rollout(domain, tapes, cots, path=GradientPath.FULL, tol=None,
                      maxiter=None):
     """Reverse chain over recorded steps (S/adjoint.py:509-539): u is the
@@ -337,4 +453,6 @@ def gradcheck(fn, inputs, eps=None, mode="central", threshold=1e-4,
 
 
 __all__ = ["GradientPath", "GradState", "backward_step", "backward_rollout",
-           "GradcheckEntry", "GradcheckReport", "gradcheck"]
+           "GradcheckEntry", "GradcheckReport", "gradcheck",
+           "backward_correct_velocity", "backward_pressure_solve",
+           "backward_pressure_matrix"]

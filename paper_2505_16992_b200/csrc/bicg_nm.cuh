@@ -23,6 +23,14 @@
 // The iterate is kept in preconditioned form: x = x0 + M^-1 z with
 // z += alpha p + omega s (k_bi_xr<true>), and one closing pass (MODE 2)
 // forms x once per solve.
+//
+// Slab plans (one ghost plane per side): stage 1 at a ghost plane would
+// need the raw inputs two planes outside the slab.  Instead each pass first
+// runs in edge mode (`qedge`): stage 1 only, on the first and last owned
+// planes, stored to Q; the halo exchange moves those planes into the
+// neighbours' ghost planes of Q, and the main pass (`qghost` = Q) reads its
+// stage-1 value at a ghost plane from there.  Stage 2 needs a ghost plane's
+// q1 only at its own column (the X neighbour), so one plane of Q suffices.
 
 constexpr int kNY = kTY + 4, kNZ = kTZ + 4;           // tile + 2-cell halo
 constexpr int kNRing2 = kNY * kNZ - kTY * kTZ;        // 176 halo-2 cells
@@ -107,8 +115,12 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     k_bi_nm(TileGeo tg, const double *__restrict__ a, BiVecs w, int par,
             int64_t n, SolverState *st, double *partials, unsigned *counter,
             const double *__restrict__ zin = nullptr,
-            double *__restrict__ xout = nullptr) {
+            double *__restrict__ xout = nullptr,
+            const double *__restrict__ qghost = nullptr,
+            double *__restrict__ qedge = nullptr) {
   if (MODE != 2 && st->all_done) return;
+  // edge mode: stage 1 of one plane per chunk, to qedge (no stage 2)
+  const bool edge = qedge != nullptr;
   constexpr int K = MODE == 1 ? 9 : 3;
   constexpr bool kClose = MODE == 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -156,7 +168,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     const int ch = rest / tg.ty_tiles;
     const int32_t y0 = tyt * kTY - 2, z0 = tzt * kTZ - 2;  // plane origin
     const int32_t xs = tg.x0 + ch * tg.xc;
-    const int32_t xe = min(xs + tg.xc, tg.x1);
+    const int32_t xe = edge ? xs + 1 : min(xs + tg.xc, tg.x1);
     const int32_t y = y0 + oy, z = z0 + oz;
 
     // raw inputs of plane-cell (sy, sz) of plane x into sm.raw
@@ -252,19 +264,32 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     double ya[3] = {0, 0, 0}, yb[3] = {0, 0, 0}, yc[3] = {0, 0, 0};
     double qa[3] = {0, 0, 0}, qb[3] = {0, 0, 0}, qc[3] = {0, 0, 0};
     double cA[6] = {0, 0, 0, 0, 0, 0};  // own N row of plane q-2
-    const int32_t qbeg = kClose ? xs - 1 : xs - 2;
-    const int32_t qend = kClose ? xe : xe + 1;  // last converted plane
+    // stage-1-only passes (close, edge) smooth planes [xs, xe); the full
+    // passes [xs - 1, xe], except a slab's ghost planes, whose q1 comes
+    // from qghost (so the planes beyond them are never converted)
+    const bool one = kClose || edge;
+    const bool lo_g = qghost && xs == tg.x0, hi_g = qghost && xe == tg.x1;
+    const int32_t qbeg = one || lo_g ? xs - 1 : xs - 2;
+    const int32_t qconv = one || hi_g ? xe : xe + 1;  // last converted plane
+    const int32_t qend = one ? xe : xe + 1;
     __syncthreads();  // the previous tile is done with every buffer
     issue_plane(qbeg);
     for (int32_t q = qbeg; q <= qend; ++q) {
       // plane q-1's N rows (own cell, halo-1 cell) and q-2's r^: plain
       // loads, consumed after the barriers
       const int32_t x1 = q - 1, x2 = q - 2;
-      const bool do1 = x1 >= (kClose ? xs : xs - 1) && x1 <= (kClose ? xe - 1 : xe);
-      const bool do2 = !kClose && x2 >= xs;
+      const bool do1 = x1 >= (one ? xs : xs - 1) && x1 <= (one ? xe - 1 : xe);
+      const bool ghost1 = do1 && ((lo_g && x1 == xs - 1) || (hi_g && x1 == xe));
+      const bool do2 = !one && x2 >= xs;
       double cB[6] = {0, 0, 0, 0, 0, 0}, cR[6] = {0, 0, 0, 0, 0, 0};
       bool own1 = false, ring1_ok = false;
-      if (do1) {
+      if (ghost1) {
+        // the neighbour rank's stage 1 of this plane (own column only)
+        const int64_t ig = (int64_t)x1 * sX + (int64_t)y * sY + z;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          qc[c] = (c < nc && act[c]) ? __ldg(qghost + c * n + ig) : 0.0;
+      } else if (do1) {
         own1 = in_domain(x1, oy, oz);
         int32_t gx, gy, gz;
         coord(x1, oy, oz, gx, gy, gz);
@@ -287,15 +312,17 @@ __global__ void __launch_bounds__(kTileThreads, 2)
       cp_async_wait_all();
       __syncthreads();  // B_a: plane q's raw inputs have landed everywhere
       // convert plane q
-      convert_cell(mod3(q), q & 1, oy, oz, true, yc);
-      if (has_r2) {
-        double tmp[3];
-        convert_cell(mod3(q), q & 1, r2y, r2z, r2_in1, tmp);
+      if (q <= qconv) {
+        convert_cell(mod3(q), q & 1, oy, oz, true, yc);
+        if (has_r2) {
+          double tmp[3];
+          convert_cell(mod3(q), q & 1, r2y, r2z, r2_in1, tmp);
+        }
       }
       __syncthreads();  // B_b: g1(q) complete; the raw buffer is free
-      if (q + 1 <= qend) issue_plane(q + 1);
+      if (q + 1 <= qconv) issue_plane(q + 1);
       // stage 1 at plane q - 1
-      if (do1) {
+      if (do1 && !ghost1) {
         if (kClose) {
           // x += g1 - D^-1 N g1 at the own cell (tile cells only)
           smooth_cell(x1, oy, oz, cB, qc);
@@ -306,6 +333,12 @@ __global__ void __launch_bounds__(kTileThreads, 2)
             const int64_t o = c * n + i1;
             xout[o] += sm.g1[mod3(x1)][c][oy][oz] - qc[c];
           }
+        } else if (edge) {
+          smooth_cell(x1, oy, oz, cB, qc);
+          const int64_t i1 = (int64_t)x1 * sX + (int64_t)y * sY + z;
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            if (c < nc && act[c]) qedge[c * n + i1] = qc[c];
         } else {
           smooth_cell(x1, oy, oz, cB, qc);
           if (!own1)
@@ -361,7 +394,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     }
     cp_async_wait_all();
   }
-  if (kClose) return;
+  if (kClose || edge) return;
   double tot[K];
   if (!grid_reduce<K>(acc, partials, counter, tot)) return;
   if (MODE == 0) {

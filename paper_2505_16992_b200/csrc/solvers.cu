@@ -1620,12 +1620,20 @@ constexpr int kPrecondNeumann2 = 3;
 
 // tile geometry of the Neumann-2 passes: the tiled geometry with chunks
 // costed at xc + 4 planes (two prologue planes per stencil stage), two
-// CTAs per SM; single-device plans only
+// CTAs per SM.  Slab plans also get the edge-pass geometry (`edge`: one
+// chunk on the first and one on the last owned plane).
 template <class V>
-bool nm_geo(const Plan &pl, const V &v, TileGeo &tg) {
-  if (pl.slab || getenv("PF_NO_NEUMANN")) return false;
+bool nm_geo(const Plan &pl, const V &v, TileGeo &tg, TileGeo *edge = nullptr) {
+  if (getenv("PF_NO_NEUMANN")) return false;
   if (!tile_geo(pl, v, tg)) return false;
-  if (tg.X < 4) return false;
+  if (tg.X < 4 && !pl.slab) return false;
+  if (edge) {
+    *edge = tg;
+    const int32_t nxl = tg.x1 - tg.x0;
+    edge->xc = std::max(1, nxl - 1);
+    edge->chunks = nxl > 1 ? 2 : 1;
+    edge->ntiles = tg.ty_tiles * tg.tz_tiles * edge->chunks;
+  }
   const int32_t nx = tg.x1 - tg.x0;
   const int64_t R = 2 * (int64_t)pl.num_sms;
   const int64_t ncols = (int64_t)tg.ty_tiles * tg.tz_tiles;
@@ -1647,7 +1655,8 @@ template <bool kTrans, int MODE>
 void launch_nm(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
                const BiVecs &bv, int par, int64_t n, SolverState *st,
                Workspace &w, int first = 0, const double *zin = nullptr,
-               double *xout = nullptr) {
+               double *xout = nullptr, const double *qghost = nullptr,
+               double *qedge = nullptr) {
   auto go = [&](auto kernel) {
     static std::mutex mu;
     static std::set<const void *> done;
@@ -1661,7 +1670,7 @@ void launch_nm(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
     count_launch();
     kernel<<<grid, kTileThreads, kNmSmem, s>>>(tg, a, bv, par, n, st,
                                                w.partials, w.counters, zin,
-                                               xout);
+                                               xout, qghost, qedge);
   };
   if constexpr (MODE == 0) {
     if (first) {
@@ -1694,13 +1703,15 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   TileGeo tg, tgn;
   const bool tiled = tile_geo(pl, v, tg);
   const int tgrid = tiled ? std::min(tg.ntiles, pl.red_blocks) : 0;
-  // Neumann-2 (PRECOND_NEUMANN2) runs fused on single-device tiled boxes;
-  // elsewhere (generic grids, slab plans: their ghost region is one plane
-  // deep) the request degrades to Jacobi
-  const bool nm = precond == kPrecondNeumann2 && nm_geo(pl, v, tgn);
+  // Neumann-2 (PRECOND_NEUMANN2) runs fused on tiled boxes (slab plans
+  // with the edge passes); on generic grids the request degrades to Jacobi
+  TileGeo tge;
+  const bool nm = precond == kPrecondNeumann2 && nm_geo(pl, v, tgn, &tge);
   if (precond == kPrecondNeumann2 && !nm) precond = 1;
   const int ngrid = nm ? std::min(tgn.ntiles, 2 * pl.num_sms) : 0;
+  const int egrid = nm ? std::min(tge.ntiles, 2 * pl.num_sms) : 0;
   double *z = base + 8 * len;  // the preconditioned iterate (nm)
+  double *qg = pl.slab ? base + 9 * len : nullptr;  // slab edge stage 1
   launch(k_bi_reset, 1, 1, s, st, ncomp, maxiter, precond, tol, fresh, mask);
   // the tiled init pass forms |b| itself
   if (fresh && !tiled)
@@ -1736,9 +1747,14 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     for (int k = 0; k < bsz; ++k) {
       const int par = (launched + k) & 1;
       halo(pl, s, {{bv.r, ncomp}, {bv.p[par], ncomp}});
+      if (nm && qg) {
+        launch_nm<kTrans, 0>(tge, egrid, s, a, bv, par, (int64_t)n, st, w,
+                             launched + k == 0, nullptr, nullptr, nullptr, qg);
+        halo(pl, s, {{qg, ncomp}});
+      }
       if (nm)
         launch_nm<kTrans, 0>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w,
-                             launched + k == 0);
+                             launched + k == 0, nullptr, nullptr, qg);
       else if (tiled)
         launch_tiled<kTrans, 0>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w,
                                 nullptr, nullptr, 0, launched + k == 0);
@@ -1746,8 +1762,14 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
         launch(k_bi_pv<V, kTrans>, gr, kBlock, s, v, a, bv, par, st,
                w.partials, w.counters);
       halo(pl, s, {{bv.v[par ^ 1], ncomp}});
+      if (nm && qg) {
+        launch_nm<kTrans, 1>(tge, egrid, s, a, bv, par, (int64_t)n, st, w, 0,
+                             nullptr, nullptr, nullptr, qg);
+        halo(pl, s, {{qg, ncomp}});
+      }
       if (nm)
-        launch_nm<kTrans, 1>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w);
+        launch_nm<kTrans, 1>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w, 0,
+                             nullptr, nullptr, qg);
       else if (tiled)
         launch_tiled<kTrans, 1>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
       else
@@ -1772,7 +1794,10 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     for (int q = 0; q < ncomp; ++q) lock = std::max(lock, (int)hs.c[q].iter);
     pl.bi_hint[kTrans ? 1 : 0] = lock;
   }
-  if (nm) launch_nm<kTrans, 2>(tgn, ngrid, s, a, bv, 0, (int64_t)n, st, w, 0, z, x);
+  if (nm) {
+    halo(pl, s, {{z, ncomp}});
+    launch_nm<kTrans, 2>(tgn, ngrid, s, a, bv, 0, (int64_t)n, st, w, 0, z, x);
+  }
   launch(k_bi_finish, ge, kBlock, s, x, n, rg, st);
   halo(pl, s, {{x, ncomp}});
   if (tiled)
@@ -2038,8 +2063,11 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
     const bool tiled = tile_geo(pl, v, tg);
     const int tgrid = tiled ? std::min(tg.ntiles, pl.red_blocks) : 0;
     // the production preconditioner: Neumann-2 where it runs, else Jacobi
-    const bool nm = nm_geo(pl, v, tgn);
+    TileGeo tge;
+    const bool nm = nm_geo(pl, v, tgn, &tge);
     const int ngrid = nm ? std::min(tgn.ntiles, 2 * pl.num_sms) : 0;
+    const int egrid = nm ? std::min(tge.ntiles, 2 * pl.num_sms) : 0;
+    double *qg = pl.slab ? w.vecs + 10 * len : nullptr;
     PF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * len, s));
     // tol 0: the recurrence never converges inside the timed iterations
     launch(k_bi_reset, 1, 1, s, st, ncomp, iters + 1, nm ? kPrecondNeumann2 : 1,
@@ -2060,10 +2088,21 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
       const int par = k & 1;
       halo(pl, s, {{bv.r, ncomp}, {bv.p[par], ncomp}});
       PF_CUDA(cudaEventRecord(ev[0], s));
+      if (nm && qg) {
+        if (transpose)
+          launch_nm<true, 0>(tge, egrid, s, a, bv, par, (int64_t)n, st, w,
+                             k == 0, nullptr, nullptr, nullptr, qg);
+        else
+          launch_nm<false, 0>(tge, egrid, s, a, bv, par, (int64_t)n, st, w,
+                              k == 0, nullptr, nullptr, nullptr, qg);
+        halo(pl, s, {{qg, ncomp}});
+      }
       if (nm && transpose)
-        launch_nm<true, 0>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w, k == 0);
+        launch_nm<true, 0>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w,
+                           k == 0, nullptr, nullptr, qg);
       else if (nm)
-        launch_nm<false, 0>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w, k == 0);
+        launch_nm<false, 0>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w,
+                            k == 0, nullptr, nullptr, qg);
       else if (tiled && transpose)
         launch_tiled<true, 0>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
       else if (tiled)
@@ -2076,10 +2115,21 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
                w.partials, w.counters);
       halo(pl, s, {{bv.v[par ^ 1], ncomp}});
       PF_CUDA(cudaEventRecord(ev[1], s));
+      if (nm && qg) {
+        if (transpose)
+          launch_nm<true, 1>(tge, egrid, s, a, bv, par, (int64_t)n, st, w, 0,
+                             nullptr, nullptr, nullptr, qg);
+        else
+          launch_nm<false, 1>(tge, egrid, s, a, bv, par, (int64_t)n, st, w, 0,
+                              nullptr, nullptr, nullptr, qg);
+        halo(pl, s, {{qg, ncomp}});
+      }
       if (nm && transpose)
-        launch_nm<true, 1>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w);
+        launch_nm<true, 1>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w, 0,
+                           nullptr, nullptr, qg);
       else if (nm)
-        launch_nm<false, 1>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w);
+        launch_nm<false, 1>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w, 0,
+                            nullptr, nullptr, qg);
       else if (tiled && transpose)
         launch_tiled<true, 1>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
       else if (tiled)

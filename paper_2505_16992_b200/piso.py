@@ -286,6 +286,146 @@ def correct_velocity(domain, h, p, a_inv):
     return out.t()
 
 
+# ---------------------------------------------------------------------------
+# standalone building blocks of the reference's stage API (S/piso.py:128-264,
+# 322-342, 431-449); the step uses their fused forms
+
+WIDE_GRAD_VARIANTS = {"mirror": 0, "onesided": 1, "face": 2}
+
+
+def _variant(variant):
+    try:
+        return WIDE_GRAD_VARIANTS[variant]
+    except KeyError:
+        raise ValueError(variant) from None
+
+
+def boundary_flux(face, values):
+    """U^a at a boundary face from prescribed face velocities (m, d)
+    (S/piso.py:128-131)."""
+    dev = values.device
+    jac = torch.as_tensor(face.face_jac, dtype=F64, device=dev)
+    t = torch.as_tensor(np.ascontiguousarray(face.face_t[:, face.axis, :]),
+                        dtype=F64, device=dev)
+    return jac * (t * values).sum(dim=1)
+
+
+def face_grad(arr, axis):
+    """Derivative along one axis of a face-value grid: central inside, full
+    one-sided at the ends (S/piso.py:134-145)."""
+    a = arr.movedim(axis, 0)
+    out = torch.empty_like(a)
+    if a.shape[0] == 1:
+        out.zero_()
+    else:
+        out[1:-1] = 0.5 * (a[2:] - a[:-2])
+        out[0] = a[1] - a[0]
+        out[-1] = a[-1] - a[-2]
+    return out.movedim(0, axis)
+
+
+def face_grad_adjoint(cot, axis):
+    """Adjoint of :func:`face_grad` (S/piso.py:148-159)."""
+    c = cot.movedim(axis, 0)
+    out = torch.zeros_like(c)
+    if c.shape[0] > 1:
+        out[2:] += 0.5 * c[1:-1]
+        out[:-2] -= 0.5 * c[1:-1]
+        out[1] += c[0]
+        out[0] -= c[0]
+        out[-1] += c[-1]
+        out[-2] -= c[-1]
+    return out.movedim(0, axis)
+
+
+def wide_grad(domain, phi, variant, bc_cells=None):
+    """Wide central differences of a per-cell field along every grid axis
+    (S/piso.py:172-209): (n,) -> (n, d); (n, k) -> (n, d, k).  variant
+    "mirror" | "onesided" | "face" (``bc_cells``: {(axis, side): (n,)}
+    prescribed face values).  Kernel: pf_wide_grad."""
+    plan = _plan_of(domain, phi)
+    n, d = domain.n, domain.dim
+    v = _variant(variant)
+    bcc = None
+    if v == 2:
+        if bc_cells is None:
+            raise ValueError("the face variant needs bc_cells")
+        bcc = torch.stack([torch.as_tensor(bc_cells[(a, s_)], dtype=F64,
+                                           device=plan.device).reshape(n)
+                           for a in range(d) for s_ in (0, 1)]).contiguous()
+    cols = [phi] if phi.dim() == 1 else [phi[:, k] for k in
+                                         range(phi.shape[1])]
+    outs = []
+    for col in cols:
+        out = torch.empty((d, n), dtype=F64, device=plan.device)
+        _lib.call("pf_wide_grad", plan.handle,
+                  _lib.ptr(scalar_field(col, n, plan.device)), v,
+                  _lib.ptr(bcc), _lib.ptr(out), plan.stream)
+        outs.append(out.t())
+    return outs[0] if phi.dim() == 1 else torch.stack(outs, dim=2)
+
+
+def wide_grad_adjoint(domain, cot, variant, phi_ndim=1):
+    """Adjoint of :func:`wide_grad` w.r.t. phi (S/piso.py:218-258): cot
+    (n, d[, k]) -> (n[, k]); the face variant also returns {(axis, side):
+    (n,)} cotangents of the prescribed face values.  Kernel:
+    pf_wide_grad_adjoint."""
+    plan = _plan_of(domain, cot)
+    n, d = domain.n, domain.dim
+    v = _variant(variant)
+    cols = [cot] if cot.dim() == 2 else [cot[:, :, k] for k in
+                                         range(cot.shape[2])]
+    outs, bcs = [], []
+    for col in cols:
+        out = torch.empty(n, dtype=F64, device=plan.device)
+        bc = torch.empty((2 * d, n), dtype=F64, device=plan.device) \
+            if v == 2 else None
+        _lib.call("pf_wide_grad_adjoint", plan.handle,
+                  _lib.ptr(soa(col, n, d, plan.device)), v, _lib.ptr(out),
+                  _lib.ptr(bc), plan.stream)
+        outs.append(out)
+        bcs.append(bc)
+    res = outs[0] if cot.dim() == 2 else torch.stack(outs, dim=1)
+    if v != 2:
+        return res
+    bcr = bcs[0] if cot.dim() == 2 else torch.stack(bcs, dim=2)
+    return res, {(a, s_): bcr[2 * a + s_] for a in range(d) for s_ in (0, 1)}
+
+
+def _cdiag(a_diag, n, device):
+    """A stencil carrying only the diagonal row (kernels read A from row 0)."""
+    return scalar_field(a_diag, n, device).reshape(1, n).contiguous()
+
+
+def momentum_cross_rhs(domain, u, nu):
+    """Lagged non-orthogonal viscous fluxes divided by J (S/piso.py:322-342),
+    (n, d); zero on orthogonal grids.  Kernel: pf_momentum_cross_rhs."""
+    plan = _plan_of(domain, u)
+    n, d = domain.n, domain.dim
+    out = torch.zeros((d, n), dtype=F64, device=plan.device)
+    if plan.cell_cross:
+        _lib.call("pf_momentum_cross_rhs", plan.handle,
+                  _lib.ptr(soa(u, n, d, plan.device)), float(nu),
+                  _lib.ptr(out), _lib.ptr(plan.workspace), plan.stream)
+    return out.t()
+
+
+def pressure_cross_rhs(domain, a_inv, p):
+    """Lagged non-orthogonal pressure fluxes (S/piso.py:431-449), (n,);
+    zero on orthogonal grids.  Kernel: pf_pressure_cross_rhs."""
+    plan = _plan_of(domain, p)
+    n = domain.n
+    if not plan.cell_cross:
+        return torch.zeros(n, dtype=F64, device=plan.device)
+    c = _cdiag(1.0 / scalar_field(a_inv, n, plan.device), n, plan.device)
+    zero = torch.zeros(n, dtype=F64, device=plan.device)
+    out = torch.empty(n, dtype=F64, device=plan.device)
+    _lib.call("pf_pressure_cross_rhs", plan.handle, _lib.ptr(c),
+              _lib.ptr(scalar_field(p, n, plan.device)), _lib.ptr(zero),
+              _lib.ptr(out), _lib.ptr(plan.workspace), plan.stream)
+    return -out
+
+
 def divergence(domain, u, bc):
     """Per-cell physical divergence (S/piso.py:458-460)."""
     return divergence_rhs(domain, u, bc) / domain.device_plan(u.device).jac
@@ -476,4 +616,16 @@ __all__ = ["FlowState", "StepConfig", "StepDiagnostics", "CorrectorTape",
            "StepTape", "PisoWorkspace", "make_state", "contravariant_flux",
            "assemble_momentum", "assemble_pressure", "momentum_rhs",
            "divergence_rhs", "correct_velocity", "divergence",
-           "advective_outflow_update", "piso_step", "SolverError"]
+           "advective_outflow_update", "piso_step", "SolverError",
+           "boundary_flux", "face_grad", "face_grad_adjoint", "wide_grad",
+           "wide_grad_adjoint", "momentum_cross_rhs", "pressure_cross_rhs",
+           "reichardt_init", "wall_forcing_source", "adaptive_dt"]
+
+
+def __getattr__(name):
+    # the channel drivers live in channel.py (S/piso.py:512-546, 668-714)
+    if name in ("reichardt_init", "reichardt_profile", "wall_forcing_source",
+                "adaptive_dt"):
+        from . import channel
+        return getattr(channel, name)
+    raise AttributeError(name)

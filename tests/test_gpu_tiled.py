@@ -62,15 +62,17 @@ def test_tiled_bicgstab_matches_generic_and_exact(shape, transpose):
             < 1e-9
 
 
-def test_tiled_slab_matches_single_domain():
-    """The tiled passes on slab plans (ghost planes as the X neighbours)."""
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("precond", ["jacobi", "neumann2"])
+def test_tiled_slab_matches_single_domain(precond, world):
+    """The tiled passes on slab plans (ghost planes as the X neighbours;
+    Neumann-2: the edge passes' stage 1 through the ghost planes of Q)."""
     import threading
     from paper_2505_16992_b200 import linalg, piso, slab
     import test_gpu_slab as T
     dom, c, b = _system((8, 16, 32))
-    x_ref, r_ref = _solve(dom, c, b, False, tiled=True)
+    x_ref, r_ref = _solve(dom, c, b, False, tiled=True, precond=precond)
     u0 = None
-    world = 2
     slabs = [slab.SlabDomain(dom, r, world) for r in range(world)]
     slab.SlabComm.local_group(slabs, b.device)
     # the global system restricted to each slab (ghost rows included)
@@ -85,8 +87,8 @@ def test_tiled_slab_matches_single_domain():
         with torch.cuda.stream(s):
             T._prewarm(ready)
             plan = slabs[r].device_plan(b.device)
-            # slab plans run the Neumann-2 request as Jacobi
-            res[r] = linalg.bicgstab_solve(plan, cs[r], bs[r], tol=1e-12)
+            res[r] = linalg.bicgstab_solve(plan, cs[r], bs[r], tol=1e-12,
+                                           precond=precond)
             s.synchronize()
 
     ts = [threading.Thread(target=work, args=(r,)) for r in range(world)]
