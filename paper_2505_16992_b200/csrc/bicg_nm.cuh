@@ -32,36 +32,33 @@
 // stage-1 value at a ghost plane from there.  Stage 2 needs a ghost plane's
 // q1 only at its own column (the X neighbour), so one plane of Q suffices.
 
+//
+// Addressing: every in-plane offset is computed once per tile, per plane
+// only the wrapped X plane base changes; all array pointers (per component,
+// per stencil row) arrive pre-offset in the kernel parameters (NmArgs), so
+// a global address is one add on a constant-bank operand; shared-memory
+// ring slots are rotating base registers; the raw inputs move as 16-byte
+// pairs along Z (the 36-wide halo row and the tile origin are even, and a
+// pair never straddles a periodic seam or a wall).  The plane loop is
+// peeled (prologue planes convert only / convert + stage 1) and the common
+// case of all three components active is its own instantiation, so the
+// steady-state step carries no per-component or per-stage tests.
+
 constexpr int kNY = kTY + 4, kNZ = kTZ + 4;           // tile + 2-cell halo
-constexpr int kNRing2 = kNY * kNZ - kTY * kTZ;        // 176 halo-2 cells
+constexpr int kNP = kNY * kNZ;                         // 432 cells per plane
+constexpr int kNPairs = kNP / 2;                       // 216 Z-pairs
 constexpr int kNRing1 = (kTY + 2) * (kTZ + 2) - kTY * kTZ;  // 84 halo-1 cells
-constexpr int kNRing2First = kTileThreads - kNRing2;  // threads 80.. convert
-static_assert(kNRing1 <= kNRing2First + 4, "ring assignment");
+static_assert(kNZ % 2 == 0 && kNPairs <= kTileThreads, "pair layout");
 
-struct NmSmem {
-  double raw[10][kNY][kNZ];     // r x3, p x3 (pv) / v x3, v x3 (pv), 1/A
-  double g1[3][3][kNY][kNZ];    // D^-1 y, planes q % 3
-  double dv[2][kNY][kNZ];       // 1/A on the 1-halo, planes q % 2
-  double q1[2][3][kNY][kNZ];    // D^-1 N g1, planes q % 2
-};
-constexpr size_t kNmSmem = sizeof(NmSmem);
+// shared memory, in doubles: raw[10][kNP] | g1[3 slots][3][kNP] |
+// q1[4 slots][3][kNP] | beta/alpha, omega [2][3]
+// (q1 keeps four planes: stage 2 of plane q-3 reads q-4, q-3, q-2 while
+// stage 1 writes q-1, and reads its X neighbours from the ring)
+constexpr int kNmRaw = 0, kNmG1 = 10 * kNP, kNmQ1 = kNmG1 + 9 * kNP,
+              kNmCo = kNmQ1 + 12 * kNP, kNmEnd = kNmCo + 8;
+constexpr size_t kNmSmem = sizeof(double) * kNmEnd;   // 107,200 B
 
-// plane slot of a ring of three (planes run from -2)
-__device__ __forceinline__ int mod3(int32_t x) { return (x + 3) % 3; }
-
-// halo-2 ring cell k (0..175) of the (kNY, kNZ) plane
-__device__ __forceinline__ void nm_ring2(int k, int &sy, int &sz) {
-  if (k < 4 * kNZ) {
-    const int row = k / kNZ;
-    sy = row < 2 ? row : row + kTY;
-    sz = k % kNZ;
-  } else {
-    const int k2 = k - 4 * kNZ, c = k2 & 3;
-    sy = 2 + (k2 >> 2);
-    sz = c < 2 ? c : c + kTZ;
-  }
-}
-// halo-1 ring cell k (0..83)
+// halo-1 ring cell k (0..83) in plane coordinates
 __device__ __forceinline__ void nm_ring1(int k, int &sy, int &sz) {
   if (k < 2 * (kTZ + 2)) {
     sy = k < kTZ + 2 ? 1 : kTY + 2;
@@ -73,35 +70,80 @@ __device__ __forceinline__ void nm_ring1(int k, int &sy, int &sz) {
   }
 }
 
-// Off-diagonal coefficients of row (x, y, z) of A (kTrans: of A^T, gathered
-// from the neighbours' back faces); zero across walls.  Faces: -x +x -y +y
-// -z +z.
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
+               "l"(gmem)
+               : "memory");
+}
+
+// Pointers of one pass, pre-offset on the host (the kernel adds cell
+// indices only).  row[f]: stencil row of face f (-x +x -y +y -z +z) of A,
+// or for A^T the neighbour's back-face row, read at the neighbour.
+struct NmArgs {
+  const double *src[3][3];  // raw array k of component q: r, v, p | z
+  const double *dinv;
+  const double *row[6];
+  const double *rhat[3];
+  double *out1[3];          // pv: p'   | close: x   | edge: Q
+  double *out2[3];          // pv: v'   | st: t
+  const double *qghost[3];  // slab ghost-plane stage 1 (null: none)
+  int32_t X, Y, Z, px, py, pz;
+  int32_t sX;               // cells per X plane
+};
+
+// in-plane addressing of one stencil row (own or halo-1 cell): its offset
+// in the plane and, for the transposed gathers, its Y/Z neighbours' (-1
+// outside a walled box)
+struct NmRow {
+  int32_t off, ym, yp, zm, zp;
+  bool ok;  // inside the box (Y, Z)
+};
+
+__device__ __forceinline__ NmRow nm_row(const NmArgs &g, int32_t gy0,
+                                        int32_t gz0) {
+  NmRow r;
+  bool oy, oz, o;
+  const int32_t y = wrap(gy0, g.Y, g.py, oy);
+  const int32_t z = wrap(gz0, g.Z, g.pz, oz);
+  r.ok = oy && oz;
+  r.off = y * g.Z + z;
+  int32_t c = wrap(y - 1, g.Y, g.py, o);
+  r.ym = o ? c * g.Z + z : -1;
+  c = wrap(y + 1, g.Y, g.py, o);
+  r.yp = o ? c * g.Z + z : -1;
+  c = wrap(z - 1, g.Z, g.pz, o);
+  r.zm = o ? y * g.Z + c : -1;
+  c = wrap(z + 1, g.Z, g.pz, o);
+  r.zp = o ? y * g.Z + c : -1;
+  return r;
+}
+
+// plane base (first cell) of plane x, -1 outside a walled box
+__device__ __forceinline__ int32_t nm_pbase(const NmArgs &g, int32_t x) {
+  if (x < 0) return g.px ? (x + g.X) * g.sX : -1;
+  if (x >= g.X) return g.px ? (x - g.X) * g.sX : -1;
+  return x * g.sX;
+}
+
+// the six off-diagonal coefficients of a row at plane base b (kTrans: the
+// X neighbours' rows at plane bases bm / bp); zero across walls
 template <bool kTrans>
-__device__ __forceinline__ void nm_coefs(const TileGeo &tg,
-                                         const double *__restrict__ a,
-                                         int64_t n, int32_t x, int32_t y,
-                                         int32_t z, double (&cf)[6]) {
-  const int64_t sX = (int64_t)tg.Y * tg.Z, sY = tg.Z;
+__device__ __forceinline__ void nm_coefs(const NmArgs &g, int32_t b,
+                                         int32_t bm, int32_t bp,
+                                         const NmRow &rw, double (&cf)[6]) {
   if (!kTrans) {
-    const int64_t i = (int64_t)x * sX + (int64_t)y * sY + z;
+    const int32_t i = b + rw.off;
 #pragma unroll
-    for (int f = 0; f < 6; ++f) cf[f] = __ldg(a + (int64_t)(1 + f) * n + i);
+    for (int f = 0; f < 6; ++f) cf[f] = __ldg(g.row[f] + i);
     return;
   }
-  bool ok;
-  int32_t c;
-  c = wrap(x - 1, tg.X, tg.px, ok);
-  cf[0] = ok ? __ldg(a + 2 * n + c * sX + (int64_t)y * sY + z) : 0.0;
-  c = wrap(x + 1, tg.X, tg.px, ok);
-  cf[1] = ok ? __ldg(a + 1 * n + c * sX + (int64_t)y * sY + z) : 0.0;
-  c = wrap(y - 1, tg.Y, tg.py, ok);
-  cf[2] = ok ? __ldg(a + 4 * n + x * sX + (int64_t)c * sY + z) : 0.0;
-  c = wrap(y + 1, tg.Y, tg.py, ok);
-  cf[3] = ok ? __ldg(a + 3 * n + x * sX + (int64_t)c * sY + z) : 0.0;
-  c = wrap(z - 1, tg.Z, tg.pz, ok);
-  cf[4] = ok ? __ldg(a + 6 * n + x * sX + (int64_t)y * sY + c) : 0.0;
-  c = wrap(z + 1, tg.Z, tg.pz, ok);
-  cf[5] = ok ? __ldg(a + 5 * n + x * sX + (int64_t)y * sY + c) : 0.0;
+  cf[0] = bm >= 0 ? __ldg(g.row[0] + bm + rw.off) : 0.0;
+  cf[1] = bp >= 0 ? __ldg(g.row[1] + bp + rw.off) : 0.0;
+  cf[2] = rw.ym >= 0 ? __ldg(g.row[2] + b + rw.ym) : 0.0;
+  cf[3] = rw.yp >= 0 ? __ldg(g.row[3] + b + rw.yp) : 0.0;
+  cf[4] = rw.zm >= 0 ? __ldg(g.row[4] + b + rw.zm) : 0.0;
+  cf[5] = rw.zp >= 0 ? __ldg(g.row[5] + b + rw.zp) : 0.0;
 }
 
 // MODE 0 (pass pv): y = p' = r + beta (p - omega v) (kFirst: p' = r);
@@ -110,24 +152,23 @@ __device__ __forceinline__ void nm_coefs(const TileGeo &tg,
 //                   t.t, t.s -> early exit / omega
 // MODE 2 (close):   y = z (the preconditioned iterate); x += M^-1 z
 //                   (stage 1 only, no reduction)
-template <bool kTrans, int MODE, bool kFirst = false>
-__global__ void __launch_bounds__(kTileThreads, 2)
-    k_bi_nm(TileGeo tg, const double *__restrict__ a, BiVecs w, int par,
-            int64_t n, SolverState *st, double *partials, unsigned *counter,
-            const double *__restrict__ zin = nullptr,
-            double *__restrict__ xout = nullptr,
-            const double *__restrict__ qghost = nullptr,
-            double *__restrict__ qedge = nullptr) {
+// edge (MODE 0 / 1): stage 1 only on one plane per chunk, stored to Q
+template <bool kTrans, int MODE, bool kFirst = false, int kMinB = 2>
+__global__ void __launch_bounds__(kTileThreads, kMinB)
+    k_bi_nm(const __grid_constant__ TileGeo tg,
+            const __grid_constant__ NmArgs g, SolverState *st, double *partials,
+            unsigned *counter, int edge) {
   if (MODE != 2 && st->all_done) return;
-  // edge mode: stage 1 of one plane per chunk, to qedge (no stage 2)
-  const bool edge = qedge != nullptr;
   constexpr int K = MODE == 1 ? 9 : 3;
   constexpr bool kClose = MODE == 2;
+  // arrays per component in the raw buffer: r, v, p (pv) | r, v (st) | z
+  constexpr int kArr = kClose || (MODE == 0 && kFirst) ? 1 : MODE == 0 ? 3 : 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  NmSmem &sm = *reinterpret_cast<NmSmem *>(smem_raw);
+  double *const sm = reinterpret_cast<double *>(smem_raw);
   const int nc = st->ncomp;
-  int act[3];
-  double c0[3], c1[3];
+  bool act[3];
+  // the iteration scalars live in shared memory (read where y is formed)
+  double *const c0 = sm + kNmCo, *const c1 = sm + kNmCo + 3;
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
     // closing pass: the components that iterated and did not break down
@@ -135,265 +176,292 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     act[q] = q < nc && (kClose ? (st->c[q].active && !st->c[q].zero_rhs &&
                                   st->c[q].iter > 0 && !st->c[q].fail)
                                : !st->c[q].done);
+  }
+  if (threadIdx.x < 3) {
+    const int q = threadIdx.x;
     c0[q] = q < nc ? (MODE == 0 ? st->c[q].beta : st->c[q].alpha) : 0.0;
     c1[q] = q < nc && MODE == 0 ? st->c[q].omega : 0.0;
   }
-  const double *__restrict__ r = w.r;
-  const double *__restrict__ dinv = w.dinv;
-  const double *__restrict__ pin = w.p[par];
-  const double *__restrict__ vin = MODE == 0 ? w.v[par] : w.v[par ^ 1];
-  double *__restrict__ pout = w.p[par ^ 1];
-  double *__restrict__ vout = MODE == 0 ? w.v[par ^ 1] : w.t;
-  const int64_t sX = (int64_t)tg.Y * tg.Z, sY = tg.Z;
+  const bool one = kClose || edge;
   const int tid = threadIdx.x;
   const int tz = tid % kTZ, ty = tid / kTZ;
-  const int oy = ty + 2, oz = tz + 2;  // own cell in plane coordinates
-  // the halo-2 cell this thread converts and the halo-1 cell it smooths
-  const bool has_r2 = tid >= kNRing2First;
+  const int eo = (ty + 2) * kNZ + tz + 2;  // own cell's plane element
+  // the Z-pair this thread loads and converts, the halo-1 cell it smooths
+  const bool has_pair = tid < kNPairs;
+  const int psy = tid / (kNZ / 2), psz = 2 * (tid % (kNZ / 2));
+  const int ep = psy * kNZ + psz;
   const bool has_r1 = tid < kNRing1;
-  int r2y = 0, r2z = 0, r1y = 0, r1z = 0;
-  if (has_r2) nm_ring2(tid - kNRing2First, r2y, r2z);
+  int r1y = 0, r1z = 0;
   if (has_r1) nm_ring1(tid, r1y, r1z);
-  const bool r2_in1 = has_r2 && r2y >= 1 && r2y <= kTY + 2 && r2z >= 1 &&
-                      r2z <= kTZ + 2;
+  const int er = r1y * kNZ + r1z;
 
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = 0.0;
 
-  for (int tile = blockIdx.x; tile < tg.ntiles; tile += gridDim.x) {
-    const int tzt = tile % tg.tz_tiles;
-    const int rest = tile / tg.tz_tiles;
-    const int tyt = rest % tg.ty_tiles;
-    const int ch = rest / tg.ty_tiles;
-    const int32_t y0 = tyt * kTY - 2, z0 = tzt * kTZ - 2;  // plane origin
-    const int32_t xs = tg.x0 + ch * tg.xc;
-    const int32_t xe = edge ? xs + 1 : min(xs + tg.xc, tg.x1);
-    const int32_t y = y0 + oy, z = z0 + oz;
-
-    // raw inputs of plane-cell (sy, sz) of plane x into sm.raw
-    auto issue_cell = [&](int32_t x, int sy, int sz) {
-      bool okx, oky, okz;
-      const int32_t gx = wrap(x, tg.X, tg.px, okx);
-      const int32_t gy = wrap(y0 + sy, tg.Y, tg.py, oky);
-      const int32_t gz = wrap(z0 + sz, tg.Z, tg.pz, okz);
-      const bool ok = okx && oky && okz;
-      const int64_t j = (int64_t)gx * sX + (int64_t)gy * sY + gz;
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        if (q >= nc || !act[q]) continue;
-        const int64_t o = q * n + j;
-        if (!ok) {
-          sm.raw[q][sy][sz] = 0.0;
-          continue;
-        }
-        if (kClose) {
-          cp_async8(&sm.raw[q][sy][sz], zin + o);
-          continue;
-        }
-        cp_async8(&sm.raw[q][sy][sz], r + o);
-        if (!(MODE == 0 && kFirst)) {
-          cp_async8(&sm.raw[3 + q][sy][sz], vin + o);
-          if (MODE == 0) cp_async8(&sm.raw[6 + q][sy][sz], pin + o);
-        }
+  // the whole tile loop, specialised for "all three components active"
+  auto run = [&](auto all_t) {
+    constexpr bool kAll = decltype(all_t)::value;
+    auto on = [&](int c) { return kAll || act[c]; };
+    for (int tile = blockIdx.x; tile < tg.ntiles; tile += gridDim.x) {
+      const int tzt = tile % tg.tz_tiles;
+      const int rest = tile / tg.tz_tiles;
+      const int tyt = rest % tg.ty_tiles;
+      const int ch = rest / tg.ty_tiles;
+      const int32_t y0 = tyt * kTY - 2, z0 = tzt * kTZ - 2;  // plane origin
+      const int32_t xs = tg.x0 + ch * tg.xc;
+      const int32_t xe = edge ? xs + 1 : min(xs + tg.xc, tg.x1);
+      // in-plane addressing, fixed for the tile
+      const NmRow own = nm_row(g, y0 + ty + 2, z0 + tz + 2);
+      const NmRow ring = nm_row(g, y0 + r1y, z0 + r1z);
+      bool okp;
+      int32_t offp;
+      {
+        bool oy, oz;
+        const int32_t gy = wrap(y0 + psy, g.Y, g.py, oy);
+        const int32_t gz = wrap(z0 + psz, g.Z, g.pz, oz);
+        okp = has_pair && oy && oz;
+        offp = gy * g.Z + gz;
       }
-      if (ok)
-        cp_async8(&sm.raw[9][sy][sz], dinv + j);
-      else
-        sm.raw[9][sy][sz] = 0.0;
-    };
-    auto issue_plane = [&](int32_t x) {
-      issue_cell(x, oy, oz);
-      if (has_r2) issue_cell(x, r2y, r2z);
-      cp_async_commit();
-    };
-    // y (undivided) and g1 = y / A of plane-cell (sy, sz)
-    auto yval = [&](int sy, int sz, int q) {
-      const double rr = sm.raw[q][sy][sz];
-      if (kClose || (MODE == 0 && kFirst)) return rr;
-      const double vv = sm.raw[3 + q][sy][sz];
-      return MODE == 0 ? rr + c0[q] * (sm.raw[6 + q][sy][sz] - c1[q] * vv)
-                       : rr - c0[q] * vv;
-    };
-    auto convert_cell = [&](int slot3, int slot2, int sy, int sz, bool in1,
-                            double (&yv)[3]) {
-      const double dj = sm.raw[9][sy][sz];
+      // raw inputs of plane x: one 16-byte copy per array of the pair;
+      // zeros outside the box
+      auto issue_plane = [&](int32_t x) {
+        if (has_pair) {
+          const int32_t b = nm_pbase(g, x);
+          double *dst = sm + kNmRaw + ep;
+          if (b < 0 || !okp) {
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        yv[q] = 0.0;
-        if (q >= nc || !act[q]) continue;
-        yv[q] = yval(sy, sz, q);
-        sm.g1[slot3][q][sy][sz] = yv[q] * dj;
-      }
-      if (in1) sm.dv[slot2][sy][sz] = dj;
-    };
-    // D^-1 N g1 at plane-cell (sy, sz) of plane x (slot3 = x % 3)
-    auto smooth_cell = [&](int32_t x, int sy, int sz, const double (&cf)[6],
-                           double (&out)[3]) {
-      const int sm3 = mod3(x - 1), s0 = mod3(x), sp3 = mod3(x + 1);
-      const double dj = sm.dv[x & 1][sy][sz];
+            for (int k = 0; k < 10; ++k)
+              *reinterpret_cast<double2 *>(dst + k * kNP) =
+                  make_double2(0.0, 0.0);
+          } else {
+            const int32_t j = b + offp;
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        out[q] = 0.0;
-        if (q >= nc || !act[q]) continue;
-        const double h = cf[0] * sm.g1[sm3][q][sy][sz] +
-                         cf[1] * sm.g1[sp3][q][sy][sz] +
-                         cf[2] * sm.g1[s0][q][sy - 1][sz] +
-                         cf[3] * sm.g1[s0][q][sy + 1][sz] +
-                         cf[4] * sm.g1[s0][q][sy][sz - 1] +
-                         cf[5] * sm.g1[s0][q][sy][sz + 1];
-        out[q] = dj * h;
-      }
-    };
-    auto in_domain = [&](int32_t x, int sy, int sz) {
-      bool a1, a2, a3;
-      wrap(x, tg.X, tg.px, a1);
-      wrap(y0 + sy, tg.Y, tg.py, a2);
-      wrap(z0 + sz, tg.Z, tg.pz, a3);
-      return a1 && a2 && a3;
-    };
-    auto coord = [&](int32_t x, int sy, int sz, int32_t &gx, int32_t &gy,
-                     int32_t &gz) {
-      bool ok;
-      gx = wrap(x, tg.X, tg.px, ok);
-      gy = wrap(y0 + sy, tg.Y, tg.py, ok);
-      gz = wrap(z0 + sz, tg.Z, tg.pz, ok);
-    };
-
-    // own-cell registers: y of planes q-2, q-1, q; q1 of planes q-3, q-1
-    double ya[3] = {0, 0, 0}, yb[3] = {0, 0, 0}, yc[3] = {0, 0, 0};
-    double qa[3] = {0, 0, 0}, qb[3] = {0, 0, 0}, qc[3] = {0, 0, 0};
-    double cA[6] = {0, 0, 0, 0, 0, 0};  // own N row of plane q-2
-    // stage-1-only passes (close, edge) smooth planes [xs, xe); the full
-    // passes [xs - 1, xe], except a slab's ghost planes, whose q1 comes
-    // from qghost (so the planes beyond them are never converted)
-    const bool one = kClose || edge;
-    const bool lo_g = qghost && xs == tg.x0, hi_g = qghost && xe == tg.x1;
-    const int32_t qbeg = one || lo_g ? xs - 1 : xs - 2;
-    const int32_t qconv = one || hi_g ? xe : xe + 1;  // last converted plane
-    const int32_t qend = one ? xe : xe + 1;
-    __syncthreads();  // the previous tile is done with every buffer
-    issue_plane(qbeg);
-    for (int32_t q = qbeg; q <= qend; ++q) {
-      // plane q-1's N rows (own cell, halo-1 cell) and q-2's r^: plain
-      // loads, consumed after the barriers
-      const int32_t x1 = q - 1, x2 = q - 2;
-      const bool do1 = x1 >= (one ? xs : xs - 1) && x1 <= (one ? xe - 1 : xe);
-      const bool ghost1 = do1 && ((lo_g && x1 == xs - 1) || (hi_g && x1 == xe));
-      const bool do2 = !one && x2 >= xs;
-      double cB[6] = {0, 0, 0, 0, 0, 0}, cR[6] = {0, 0, 0, 0, 0, 0};
-      bool own1 = false, ring1_ok = false;
-      if (ghost1) {
-        // the neighbour rank's stage 1 of this plane (own column only)
-        const int64_t ig = (int64_t)x1 * sX + (int64_t)y * sY + z;
+            for (int q = 0; q < 3; ++q) {
+              if (!on(q)) continue;
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
-          qc[c] = (c < nc && act[c]) ? __ldg(qghost + c * n + ig) : 0.0;
-      } else if (do1) {
-        own1 = in_domain(x1, oy, oz);
-        int32_t gx, gy, gz;
-        coord(x1, oy, oz, gx, gy, gz);
-        if (own1) nm_coefs<kTrans>(tg, a, n, gx, gy, gz, cB);
-        if (has_r1) {
-          ring1_ok = in_domain(x1, r1y, r1z);
-          if (ring1_ok) {
-            coord(x1, r1y, r1z, gx, gy, gz);
-            nm_coefs<kTrans>(tg, a, n, gx, gy, gz, cR);
+              for (int k = 0; k < kArr; ++k)
+                cp_async16(dst + (3 * k + q) * kNP, g.src[k][q] + j);
+            }
+            cp_async16(dst + 9 * kNP, g.dinv + j);
           }
         }
-      }
-      double rh[3] = {0, 0, 0};
-      if (MODE == 0 && do2) {
-        const int64_t i2 = (int64_t)x2 * sX + (int64_t)y * sY + z;
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          if (c < nc && act[c]) rh[c] = __ldg(w.rhat + c * n + i2);
-      }
-      cp_async_wait_all();
-      __syncthreads();  // B_a: plane q's raw inputs have landed everywhere
-      // convert plane q
-      if (q <= qconv) {
-        convert_cell(mod3(q), q & 1, oy, oz, true, yc);
-        if (has_r2) {
-          double tmp[3];
-          convert_cell(mod3(q), q & 1, r2y, r2z, r2_in1, tmp);
-        }
-      }
-      __syncthreads();  // B_b: g1(q) complete; the raw buffer is free
-      if (q + 1 <= qconv) issue_plane(q + 1);
-      // stage 1 at plane q - 1
-      if (do1 && !ghost1) {
-        if (kClose) {
-          // x += g1 - D^-1 N g1 at the own cell (tile cells only)
-          smooth_cell(x1, oy, oz, cB, qc);
-          const int64_t i1 = (int64_t)x1 * sX + (int64_t)y * sY + z;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            if (c >= nc || !act[c]) continue;
-            const int64_t o = c * n + i1;
-            xout[o] += sm.g1[mod3(x1)][c][oy][oz] - qc[c];
+        cp_async_commit();
+      };
+      // y of element e of the raw buffer
+      auto yval = [&](int e, int q) {
+        const double *rw = sm + kNmRaw + e;
+        const double rr = rw[q * kNP];
+        if (kArr == 1) return rr;
+        const double vv = rw[(3 + q) * kNP];
+        return MODE == 0 ? rr + c0[q] * (rw[(6 + q) * kNP] - c1[q] * vv)
+                         : rr - c0[q] * vv;
+      };
+
+      // ring slots: g1 of planes q-3 / q-2 / q-1 and q1 of planes q-5 /
+      // q-4 / q-3 / q-2 at the start of step q; rotated every step
+      int g1a = kNmG1, g1b = g1a + 3 * kNP, g1c = g1b + 3 * kNP;
+      int q1a = kNmQ1, q1b = q1a + 3 * kNP, q1c = q1b + 3 * kNP,
+          q1d = q1c + 3 * kNP;
+      // own-cell y of planes q-3, q-2, q-1, q
+      double ya[3] = {0, 0, 0}, yb[3] = {0, 0, 0}, yc[3] = {0, 0, 0},
+             yd[3] = {0, 0, 0};
+
+      // stage-1-only passes (close, edge) smooth planes [xs, xe); the full
+      // passes [xs - 1, xe], except a slab's ghost planes, whose q1 comes
+      // from qghost (so the planes beyond them are never converted)
+      const bool lo_g = g.qghost[0] && xs == tg.x0;
+      const bool hi_g = g.qghost[0] && xe == tg.x1;
+      const int32_t qbeg = one || lo_g ? xs - 1 : xs - 2;
+      const int32_t qconv = one || hi_g ? xe : xe + 1;  // last converted
+
+      // One plane step q:
+      //   phase A (after B_a): convert plane q (g1, own y) and stage 2 of
+      //     plane q-3 (out = y - N q1) -- independent work, interleaved;
+      //   phase B (after B_b): stage 1 of plane q-1 (q1 = D^-1 N g1).
+      // S1 / S2 select the stages (peeled prologue and epilogue steps).
+      auto step = [&](int32_t q, auto s1_t, auto s2_t) {
+        constexpr bool S1 = decltype(s1_t)::value;
+        constexpr bool S2 = decltype(s2_t)::value;
+        const int32_t x1 = q - 1, x3 = q - 3;
+        const bool ghost1 = S1 && ((lo_g && x1 == xs - 1) ||
+                                   (hi_g && x1 == xe));
+        const int g1q = g1a;  // plane q goes to the oldest g1 slot
+        // plane x1's N rows and 1/A (own, halo-1), x3's N rows and r^:
+        // plain loads consumed after the barriers
+        double cB[6], cR[6], cA[6];
+        double djo = 0.0, djr = 0.0;
+        int32_t b1 = -1;
+        if (S1 && !ghost1) {
+          b1 = nm_pbase(g, x1);
+          if (b1 >= 0) {
+            const int32_t bm = kTrans ? nm_pbase(g, x1 - 1) : 0;
+            const int32_t bp = kTrans ? nm_pbase(g, x1 + 1) : 0;
+            nm_coefs<kTrans>(g, b1, bm, bp, own, cB);
+            djo = __ldg(g.dinv + b1 + own.off);
+            if (!one && has_r1 && ring.ok) {
+              nm_coefs<kTrans>(g, b1, bm, bp, ring, cR);
+              djr = __ldg(g.dinv + b1 + ring.off);
+            }
           }
-        } else if (edge) {
-          smooth_cell(x1, oy, oz, cB, qc);
-          const int64_t i1 = (int64_t)x1 * sX + (int64_t)y * sY + z;
-#pragma unroll
-          for (int c = 0; c < 3; ++c)
-            if (c < nc && act[c]) qedge[c * n + i1] = qc[c];
-        } else {
-          smooth_cell(x1, oy, oz, cB, qc);
-          if (!own1)
-            for (int c = 0; c < 3; ++c) qc[c] = 0.0;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) sm.q1[x1 & 1][c][oy][oz] = qc[c];
-          if (has_r1) {
-            double qr[3];
-            smooth_cell(x1, r1y, r1z, cR, qr);
+        }
+        double rh[3] = {0, 0, 0};
+        int32_t i3 = 0;
+        if (S2) {
+          const int32_t b3 = nm_pbase(g, x3);
+          i3 = b3 + own.off;
+          const int32_t bm = kTrans ? nm_pbase(g, x3 - 1) : 0;
+          const int32_t bp = kTrans ? nm_pbase(g, x3 + 1) : 0;
+          nm_coefs<kTrans>(g, b3, bm, bp, own, cA);
+          if (MODE == 0) {
 #pragma unroll
             for (int c = 0; c < 3; ++c)
-              sm.q1[x1 & 1][c][r1y][r1z] = ring1_ok ? qr[c] : 0.0;
+              if (on(c)) rh[c] = __ldg(g.rhat[c] + i3);
           }
         }
-      }
-      // stage 2 at plane q - 2: out = y - N q1.  Its in-plane q1 (slot
-      // x2 & 1) was written in the previous step, before this step's
-      // barriers; this step's stage 1 writes the other slot.
-      if (do2) {
-        const int64_t i2 = (int64_t)x2 * sX + (int64_t)y * sY + z;
-        const int s2 = x2 & 1;
+        if (ghost1) {
+          // the neighbour rank's stage 1 of this plane (own column: only
+          // stage 2's X neighbour reads it) into plane x1's q1 slot
+          const int32_t ig = nm_pbase(g, x1) + own.off;
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            sm[q1a + c * kNP + eo] = on(c) ? __ldg(g.qghost[c] + ig) : 0.0;
+        }
+        cp_async_wait_all();
+        __syncthreads();  // B_a: plane q's raw inputs have landed
+        // phase A
+        if (q <= qconv) {
+          if (has_pair) {
+            const double2 dj = *reinterpret_cast<const double2 *>(
+                sm + kNmRaw + 9 * kNP + ep);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              if (!on(c)) continue;
+              const double v0 = yval(ep, c), v1 = yval(ep + 1, c);
+              *reinterpret_cast<double2 *>(sm + g1q + c * kNP + ep) =
+                  make_double2(v0 * dj.x, v1 * dj.y);
+            }
+          }
+          if (!one) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) yd[c] = on(c) ? yval(eo, c) : 0.0;
+          }
+        }
+        if (S2) {
+          // q1 of planes x3 - 1, x3, x3 + 1: slots q1b, q1c, q1d
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            if (!on(c)) continue;
+            const double *qq = sm + q1c + c * kNP + eo;
+            const double off = cA[0] * sm[q1b + c * kNP + eo] +
+                               cA[1] * sm[q1d + c * kNP + eo] +
+                               cA[2] * qq[-kNZ] + cA[3] * qq[kNZ] +
+                               cA[4] * qq[-1] + cA[5] * qq[1];
+            const double out = ya[c] - off;
+            g.out2[c][i3] = out;
+            if (MODE == 0) {
+              g.out1[c][i3] = ya[c];
+              acc[c] += rh[c] * out;
+            } else {
+              acc[3 * c] += ya[c] * ya[c];
+              acc[3 * c + 1] += out * out;
+              acc[3 * c + 2] += out * ya[c];
+            }
+          }
+        }
+        __syncthreads();  // B_b: g1(q) complete; the raw buffer is free
+        if (q + 1 <= qconv) issue_plane(q + 1);
+        else cp_async_commit();
+        // phase B: stage 1 at x1 reads g1 of planes x1 - 1, x1, x1 + 1 =
+        // slots g1b, g1c, g1q, writes q1 slot q1a
+        if (S1 && !ghost1) {
+          const double *gm = sm + g1b, *gc = sm + g1c, *gp = sm + g1q;
+          const bool in1 = b1 >= 0;
+          double *qn = sm + q1a;
+          double qo[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            qo[c] = 0.0;
+            if (!on(c) || !in1) continue;
+            const int o = c * kNP + eo;
+            qo[c] = djo * (cB[0] * gm[o] + cB[1] * gp[o] +
+                           cB[2] * gc[o - kNZ] + cB[3] * gc[o + kNZ] +
+                           cB[4] * gc[o - 1] + cB[5] * gc[o + 1]);
+          }
+          if (kClose) {
+            const int32_t i1 = b1 + own.off;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              if (on(c)) g.out1[c][i1] += gc[c * kNP + eo] - qo[c];
+          } else if (one) {
+            const int32_t i1 = b1 + own.off;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              if (on(c)) g.out1[c][i1] = qo[c];
+          } else {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) qn[c * kNP + eo] = qo[c];
+            if (has_r1) {
+              const bool okr = in1 && ring.ok;
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                if (!on(c)) continue;
+                const int o = c * kNP + er;
+                qn[o] = okr ? djr * (cR[0] * gm[o] + cR[1] * gp[o] +
+                                     cR[2] * gc[o - kNZ] +
+                                     cR[3] * gc[o + kNZ] +
+                                     cR[4] * gc[o - 1] + cR[5] * gc[o + 1])
+                            : 0.0;
+              }
+            }
+          }
+        }
+        // rotate: g1 (a,b,c) <- (b,c,q); q1 (a,b,c,d) <- (b,c,d,a) once
+        // stage 1 wrote plane x1 into a; y (a,b,c,d) <- (b,c,d,-)
+        g1a = g1b;
+        g1b = g1c;
+        g1c = g1q;
+        if (S1) {
+          const int t = q1a;
+          q1a = q1b;
+          q1b = q1c;
+          q1c = q1d;
+          q1d = t;
+        }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          if (c >= nc || !act[c]) continue;
-          const double off = cA[0] * qa[c] + cA[1] * qc[c] +
-                             cA[2] * sm.q1[s2][c][oy - 1][oz] +
-                             cA[3] * sm.q1[s2][c][oy + 1][oz] +
-                             cA[4] * sm.q1[s2][c][oy][oz - 1] +
-                             cA[5] * sm.q1[s2][c][oy][oz + 1];
-          const double out = ya[c] - off;
-          const int64_t o = c * n + i2;
-          vout[o] = out;
-          if (MODE == 0) {
-            pout[o] = ya[c];
-            acc[c] += rh[c] * out;
-          } else {
-            acc[3 * c] += ya[c] * ya[c];
-            acc[3 * c + 1] += out * out;
-            acc[3 * c + 2] += out * ya[c];
-          }
+          ya[c] = yb[c];
+          yb[c] = yc[c];
+          yc[c] = yd[c];
         }
+      };
+
+      __syncthreads();  // the previous tile is done with every buffer
+      issue_plane(qbeg);
+      using T = std::true_type;
+      using F = std::false_type;
+      int32_t q = qbeg;
+      if (one) {
+        // stage 1 on [xs, xe): convert xs - 1 and xs, then xs + 1 .. xe
+        step(q++, F{}, F{});
+        step(q++, F{}, F{});
+        for (; q <= xe; ++q) step(q, T{}, F{});
+      } else {
+        // stage 1 of planes xs - 1 .. xe (steps xs .. xe + 1), stage 2 of
+        // xs .. xe - 1 (steps xs + 3 .. xe + 2)
+        for (; q < xs; ++q) step(q, F{}, F{});
+        for (; q <= min(xs + 2, xe + 1); ++q) step(q, T{}, F{});
+        for (; q <= xe + 1; ++q) step(q, T{}, T{});
+        step(q, F{}, T{});
       }
-      // rotate the own-cell rings
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        ya[c] = yb[c];
-        yb[c] = yc[c];
-        qa[c] = qb[c];
-        qb[c] = qc[c];
-      }
-#pragma unroll
-      for (int f = 0; f < 6; ++f) cA[f] = cB[f];
+      cp_async_wait_all();
     }
-    cp_async_wait_all();
-  }
+  };
+  if (act[0] && act[1] && act[2])
+    run(std::true_type{});
+  else
+    run(std::false_type{});
+
   if (kClose || edge) return;
   double tot[K];
   if (!grid_reduce<K>(acc, partials, counter, tot)) return;

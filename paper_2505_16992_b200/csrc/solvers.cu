@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <set>
+#include <type_traits>
 
 #include "cgstate.cuh"
 #include "common.cuh"
@@ -1622,6 +1623,17 @@ constexpr int kPrecondNeumann2 = 3;
 // costed at xc + 4 planes (two prologue planes per stencil stage), two
 // CTAs per SM.  Slab plans also get the edge-pass geometry (`edge`: one
 // chunk on the first and one on the last owned plane).
+// resident CTAs per SM of the Neumann-2 passes (PF_NM_MINB: 1 or 2).  One
+// CTA (up to 255 registers) measured best on C4: the 128-register cap of
+// two CTAs spills (pv 766-830 us vs 868-1289 us)
+inline int nm_minb() {
+  static const int m = [] {
+    const char *e = getenv("PF_NM_MINB");
+    return e && atoi(e) == 2 ? 2 : 1;
+  }();
+  return m;
+}
+
 template <class V>
 bool nm_geo(const Plan &pl, const V &v, TileGeo &tg, TileGeo *edge = nullptr) {
   if (getenv("PF_NO_NEUMANN")) return false;
@@ -1635,7 +1647,7 @@ bool nm_geo(const Plan &pl, const V &v, TileGeo &tg, TileGeo *edge = nullptr) {
     edge->ntiles = tg.ty_tiles * tg.tz_tiles * edge->chunks;
   }
   const int32_t nx = tg.x1 - tg.x0;
-  const int64_t R = 2 * (int64_t)pl.num_sms;
+  const int64_t R = nm_minb() * (int64_t)pl.num_sms;
   const int64_t ncols = (int64_t)tg.ty_tiles * tg.tz_tiles;
   int64_t best = -1;
   for (int32_t xc = 1; xc <= std::max(1, nx); ++xc) {
@@ -1657,6 +1669,27 @@ void launch_nm(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
                Workspace &w, int first = 0, const double *zin = nullptr,
                double *xout = nullptr, const double *qghost = nullptr,
                double *qedge = nullptr) {
+  NmArgs g{};
+  for (int q = 0; q < 3; ++q) {
+    const int64_t o = q * n;
+    g.src[0][q] = (MODE == 2 ? zin : bv.r) + o;
+    g.src[1][q] = (MODE == 0 ? bv.v[par] : bv.v[par ^ 1]) + o;
+    g.src[2][q] = bv.p[par] + o;
+    g.rhat[q] = bv.rhat + o;
+    g.out1[q] = (MODE == 2 ? xout : qedge ? qedge : bv.p[par ^ 1]) + o;
+    g.out2[q] = (MODE == 0 ? bv.v[par ^ 1] : bv.t) + o;
+    g.qghost[q] = qghost ? qghost + o : nullptr;
+  }
+  g.dinv = bv.dinv;
+  for (int f = 0; f < 6; ++f) g.row[f] = a + (1 + (kTrans ? f ^ 1 : f)) * n;
+  g.X = tg.X;
+  g.Y = tg.Y;
+  g.Z = tg.Z;
+  g.px = tg.px;
+  g.py = tg.py;
+  g.pz = tg.pz;
+  g.sX = tg.Y * tg.Z;
+  const int edge = qedge != nullptr;
   auto go = [&](auto kernel) {
     static std::mutex mu;
     static std::set<const void *> done;
@@ -1668,10 +1701,19 @@ void launch_nm(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
                              (int)kNmSmem);
     }
     count_launch();
-    kernel<<<grid, kTileThreads, kNmSmem, s>>>(tg, a, bv, par, n, st,
-                                               w.partials, w.counters, zin,
-                                               xout, qghost, qedge);
+    kernel<<<grid, kTileThreads, kNmSmem, s>>>(tg, g, st, w.partials,
+                                               w.counters, edge);
   };
+  if (nm_minb() == 1) {
+    if constexpr (MODE == 0) {
+      if (first) {
+        go(k_bi_nm<kTrans, MODE, true, 1>);
+        return;
+      }
+    }
+    go(k_bi_nm<kTrans, MODE, false, 1>);
+    return;
+  }
   if constexpr (MODE == 0) {
     if (first) {
       go(k_bi_nm<kTrans, MODE, true>);
@@ -1708,8 +1750,8 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   TileGeo tge;
   const bool nm = precond == kPrecondNeumann2 && nm_geo(pl, v, tgn, &tge);
   if (precond == kPrecondNeumann2 && !nm) precond = 1;
-  const int ngrid = nm ? std::min(tgn.ntiles, 2 * pl.num_sms) : 0;
-  const int egrid = nm ? std::min(tge.ntiles, 2 * pl.num_sms) : 0;
+  const int ngrid = nm ? std::min(tgn.ntiles, nm_minb() * pl.num_sms) : 0;
+  const int egrid = nm ? std::min(tge.ntiles, nm_minb() * pl.num_sms) : 0;
   double *z = base + 8 * len;  // the preconditioned iterate (nm)
   double *qg = pl.slab ? base + 9 * len : nullptr;  // slab edge stage 1
   launch(k_bi_reset, 1, 1, s, st, ncomp, maxiter, precond, tol, fresh, mask);
@@ -2065,8 +2107,8 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
     // the production preconditioner: Neumann-2 where it runs, else Jacobi
     TileGeo tge;
     const bool nm = nm_geo(pl, v, tgn, &tge);
-    const int ngrid = nm ? std::min(tgn.ntiles, 2 * pl.num_sms) : 0;
-    const int egrid = nm ? std::min(tge.ntiles, 2 * pl.num_sms) : 0;
+    const int ngrid = nm ? std::min(tgn.ntiles, nm_minb() * pl.num_sms) : 0;
+    const int egrid = nm ? std::min(tge.ntiles, nm_minb() * pl.num_sms) : 0;
     double *qg = pl.slab ? w.vecs + 10 * len : nullptr;
     PF_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * len, s));
     // tol 0: the recurrence never converges inside the timed iterations
