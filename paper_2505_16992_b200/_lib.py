@@ -6,6 +6,7 @@ tensors; the stream is torch's current stream on the tensors' device.
 """
 
 import ctypes
+import threading
 import os
 
 import torch
@@ -164,9 +165,17 @@ def load(path=LIB_PATH):
 
 
 def call(name, *args):
-    """Invoke an entry point; non-zero status raises LibraryError."""
+    """Invoke an entry point; non-zero status raises LibraryError.  The
+    tensors whose pointers were taken for this call (ptr) stay referenced
+    until it has enqueued its work: a temporary such as ``ptr(soa(h))``
+    would otherwise return its block to the caching allocator before the
+    call, and the next temporary of the same argument list could reuse
+    (and overwrite) it ahead of the kernel in stream order."""
     lib = load()
-    rc = getattr(lib, name)(*args)
+    try:
+        rc = getattr(lib, name)(*args)
+    finally:
+        _keep.refs = []
     if rc != 0:
         msg = lib.pf_last_error().decode(errors="replace")
         raise LibraryError(f"{name} failed (status {rc}): {msg}")
@@ -180,10 +189,18 @@ def require_cuda(device):
             "there is no CPU fallback")
 
 
+_keep = threading.local()
+
+
 def ptr(t):
-    """Device pointer of a tensor (None -> NULL)."""
+    """Device pointer of a tensor (None -> NULL); the tensor is kept alive
+    until the next call() returns (per host thread)."""
     if t is None:
         return None
+    refs = getattr(_keep, "refs", None)
+    if refs is None:
+        refs = _keep.refs = []
+    refs.append(t)
     return c_ptr(t.data_ptr())
 
 

@@ -845,17 +845,23 @@ constexpr size_t kTileSmem = sizeof(TileSmem);
 //                   t.s
 // MODE 3 (verify):  g = x, sums |b - A x|^2 of every component (runs after
 //                   convergence too)
+// MODE 4 (close):  g = z / A, x += g - A^-1 N g = x0 + M^-1 z (the
+//                   Neumann-2 preconditioned iterate, bicg_nm.cuh); a
+//                   one-stage stencil, so the efficient single-halo pass
+//                   forms it (no reduction)
 template <bool kTrans, int MODE, int kMinB = 1, bool kFirst = false>
 __global__ void __launch_bounds__(kTileThreads, kMinB)
     k_bi_tiled(TileGeo tg, const double *__restrict__ a, BiVecs w, int par,
                int64_t n, SolverState *st, double *partials,
                unsigned *counter, const double *__restrict__ xin = nullptr,
-               const double *__restrict__ bin = nullptr, int nverify = 0) {
-  if (MODE != 3 && st->all_done) return;
+               const double *__restrict__ bin = nullptr, int nverify = 0,
+               double *__restrict__ xout = nullptr) {
+  if (MODE != 3 && MODE != 4 && st->all_done) return;
   // compile-time: a runtime branch here slows the transposed pass ~15 %
   constexpr bool fresh = MODE == 0 && kFirst;
   constexpr int K = MODE == 1 ? 9 : MODE == 2 ? 6 : 3;
-  constexpr bool kX = MODE >= 2;  // the input is the iterate x itself
+  constexpr bool kX = MODE >= 2;  // the input is the iterate x (or z) itself
+  constexpr bool kZ = MODE == 4;  // ... divided by A (the close pass)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem &sm = *reinterpret_cast<TileSmem *>(smem_raw);
   const int nc = MODE == 3 ? nverify : st->ncomp;
@@ -865,6 +871,9 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
     act[q] = q < nc && (MODE == 3 || !st->c[q].done);
+    if (MODE == 4)  // the components that iterated and did not break down
+      act[q] = q < nc && st->c[q].active && !st->c[q].zero_rhs &&
+               st->c[q].iter > 0 && !st->c[q].fail;
     if (MODE == 0) {
       c0[q] = q < nc ? st->c[q].beta : 0.0;
       c1[q] = q < nc ? st->c[q].omega : 0.0;
@@ -914,7 +923,7 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
         if (MODE == 0) sm.raw[b][6 + q][sy][sz] = 0.0;
       }
     }
-    if (kX) return;
+    if (kX && !kZ) return;
     if (ok)
       cp_async8(&sm.raw[b][9][sy][sz], dinv + j);
     else
@@ -922,6 +931,15 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
   };
   // g (and the undivided value) of slot (sy, sz) of raw buffer b
   auto G = [&](int b, int sy, int sz, double (&g)[3], double (&pv)[3]) {
+    if (kZ) {
+      const double dj = sm.raw[b][9][sy][sz];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        pv[q] = (q < nc && act[q]) ? sm.raw[b][q][sy][sz] : 0.0;
+        g[q] = pv[q] * dj;
+      }
+      return;
+    }
     if (kX) {
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
@@ -1039,16 +1057,29 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
 #pragma unroll
       for (int q = 0; q < 3; ++q)
         rh[q] = (MODE == 0 && q < nc && act[q]) ? w.rhat[q * n + i]
-                : (kX && q < nc && act[q]) ? bin[q * n + i]
-                                           : 0.0;
+                : (kX && !kZ && q < nc && act[q]) ? bin[q * n + i]
+                                                  : 0.0;
       cp_async_wait_all();  // my copies of plane x + 1 have landed
       __syncthreads();      // everyone's have; g of plane x is complete
       convert(x + 1, gn, pn);
       if (x + 2 <= xe) issue_plane(x + 2);
       const int gb = x & 1;
+      if (kZ) {
+        const double di = w.dinv[i];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          if (q >= nc || !act[q]) continue;
+          const double off = cf[0] * gm[q] + cf[1] * gn[q] +
+                             cf[2] * sm.g[gb][q][ty][tz + 1] +
+                             cf[3] * sm.g[gb][q][ty + 2][tz + 1] +
+                             cf[4] * sm.g[gb][q][ty + 1][tz] +
+                             cf[5] * sm.g[gb][q][ty + 1][tz + 2];
+          xout[q * n + i] += gc[q] - di * off;
+        }
+      }
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        if (q >= nc || !act[q]) continue;
+        if (kZ || q >= nc || !act[q]) continue;
         const double yv = aii * gc[q] + cf[0] * gm[q] + cf[1] * gn[q] +
                           cf[2] * sm.g[gb][q][ty][tz + 1] +
                           cf[3] * sm.g[gb][q][ty + 2][tz + 1] +
@@ -1084,6 +1115,7 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
     }
     cp_async_wait_all();
   }
+  if (kZ) return;
   double tot[K];
   if (!grid_reduce<K>(acc, partials, counter, tot)) return;
   if (MODE == 3) {
@@ -1523,7 +1555,7 @@ void launch_tiled(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
                   const BiVecs &bv, int par, int64_t n, SolverState *st,
                   Workspace &w, const double *xin = nullptr,
                   const double *bin = nullptr, int nverify = 0,
-                  int first = 0) {
+                  int first = 0, double *xout = nullptr) {
   // 2 CTAs per SM (<= 128 registers, 2 x 71 KB of shared memory) measured
   // best on C4: pass pv 5.3 TB/s, pass st 4.3 TB/s (1 CTA: 3.8 / 2.9; 3 CTAs
   // with the 80-register cap: 3.5 / 3.2).  PF_TILE_MINB overrides.
@@ -1546,7 +1578,7 @@ void launch_tiled(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
     count_launch();
     kernel<<<grid, kTileThreads, kTileSmem, s>>>(tg, a, bv, par, n, st,
                                                  w.partials, w.counters, xin,
-                                                 bin, nverify);
+                                                 bin, nverify, xout);
   };
   if (MODE == 0 && first) {
     if (minb >= 3)
@@ -1837,8 +1869,10 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     pl.bi_hint[kTrans ? 1 : 0] = lock;
   }
   if (nm) {
+    // x = x0 + M^-1 z: a one-stage stencil, on the single-halo tiled pass
     halo(pl, s, {{z, ncomp}});
-    launch_nm<kTrans, 2>(tgn, ngrid, s, a, bv, 0, (int64_t)n, st, w, 0, z, x);
+    launch_tiled<kTrans, 4>(tg, tgrid, s, a, bv, 0, (int64_t)n, st, w, z,
+                            nullptr, 0, 0, x);
   }
   launch(k_bi_finish, ge, kBlock, s, x, n, rg, st);
   halo(pl, s, {{x, ncomp}});
