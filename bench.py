@@ -589,7 +589,47 @@ def measure_roofline(args, dom, plan, state, nu, dt, dev, per_step):
                         for nm in sorted(allk, key=lambda x: -share[x])},
             "pressure_cg_iteration": {
                 "preconditioner": plan.geom_kind if mg else "jacobi",
-                "ms": it_ms, "ms_graph_replay": float(ms[10])}}
+                "ms": it_ms, "ms_graph_replay": float(ms[10])},
+            "whole_step": whole_step_bytes(d, per_step, n, peak,
+                                           nm_bi="k_bi_nm_pv" in "".join(bi))}
+
+
+def whole_step_bytes(d, per_step, n, peak, nm_bi):
+    """SURVEY.md §8(d)'s whole-step figure: sum over the step's kernels of
+    algorithmic bytes/cell x invocations (from the step's own iteration
+    counts), times the cells, over the measured step time.  Per-op bytes
+    (fp64, s = 8, q = 2d+1 stencil rows):
+      momentum assembly + rhs 16 s; pressure assembly (2d+2) s;
+      BiCGStab per lock-step iteration: this repo's three passes (Neumann-2
+        520 B, Jacobi 528 B in 3D) + per solve the init pass (reads b, x,
+        C; writes r, r^, 1/A), the verification (b, x, C) and, Neumann-2,
+        the close pass (z, 1/A, N, x);
+      per corrector: h-stage + divergence (q+3d+1) s, correction (2d+2) s;
+      CG per iteration: SpMV_P (d+2) s + update 6 s + preconditioner
+        (spectral: 11 s, 4 Fourier / line sweeps over the n/2-complex
+        spectrum) + direction 3 s; per solve ~12 s of setup passes;
+      adjoint: (4q+6d+8) s per corrector, (3q+4d+4) s for the predictor
+        and assembly adjoints.
+    Counts per step: 1 forward + 1 adjoint BiCGStab solve (d components
+    batched), 2 correctors, the CG iterations reported."""
+    s, q = 8, 2 * d + 1
+    bi_it = kernel_bytes("k_bi_nm_pv", d) + kernel_bytes("k_bi_nm_st", d) \
+        + kernel_bytes("k_bi_xr_z", d) if nm_bi else \
+        kernel_bytes("k_bi_pv", d) + kernel_bytes("k_bi_st", d) \
+        + kernel_bytes("k_bi_xr", d)
+    bi_solve = s * (q + 5 * d + 1) + s * (q + 2 * d) \
+        + (s * (q - 1 + 4 * d + 1) if nm_bi else 0)
+    n_corr = 2
+    fwd = 16 * s + (2 * d + 2) * s + n_corr * ((q + 3 * d + 1) * s
+                                                + (2 * d + 2) * s)
+    adj = n_corr * (4 * q + 6 * d + 8) * s + (3 * q + 4 * d + 4) * s
+    cg_it = (d + 2) * s + 6 * s + 11 * s + 3 * s
+    b = (fwd + adj + bi_it * (per_step["bi_fwd"] + per_step["bi_adj"])
+         + 2 * bi_solve + cg_it * per_step["cg"] + 4 * n_corr * 12 * s / 2)
+    gbs = b * n / (per_step["ms"] * 1e-3) / 1e9
+    return {"bytes_per_cell": b, "achieved_gbs": gbs, "peak": peak,
+            "frac": gbs / peak,
+            "model": "SURVEY.md §8(d) per-op bytes x this step's counts"}
 
 
 def run_c5train(args, world, rank, local, dev):

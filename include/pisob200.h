@@ -380,6 +380,26 @@ PF_API int pf_wide_grad_adjoint(const pf_plan *plan, const double *cot,
                                 int32_t variant, double *out, double *bc_cot,
                                 void *stream);
 
+/* ---- channel drivers (S/piso.py:512-546) ---------------------------------- */
+
+/* adaptive_dt's CFL peak, S/piso.py:512-520: *out_dev = max over the owned
+ * cells of sum_a |U^a| / J (collective on slab plans: the global max). */
+PF_API int pf_cfl_peak(const pf_plan *plan, const double *u, void *workspace,
+                       double *out_dev, void *stream);
+/* wall_shear_mean + wall_forcing_source, S/piso.py:523-542: for each of
+ * nwall walls (entries seg[w] .. seg[w+1] of cells / dist: the first cell
+ * row and its distance to the wall face) the mean of u[c, flow] / dist;
+ * out_dev (d) = (0, .., nu mean_w |mean_w| / delta, .., 0) at flow_axis.
+ * seg is a device array of nwall + 1 offsets (m = seg[nwall]), cnt (nwall,
+ * device) the row sizes the sums are divided by (collective on slab plans:
+ * the sums span the ranks, cnt holds the global sizes). */
+PF_API int pf_wall_forcing(const pf_plan *plan, const double *u,
+                           int32_t flow_axis, const int32_t *cells,
+                           const double *dist, const int32_t *seg,
+                           const double *cnt, int32_t nwall, int32_t m,
+                           double nu, double delta, double *out_dev,
+                           void *workspace, void *stream);
+
 /* y += alpha x over len entries (device vectors) */
 PF_API int pf_axpy(const pf_plan *plan, double alpha, const double *x,
                    double *y, int64_t len, void *stream);

@@ -121,6 +121,9 @@ _SIGS = {
                               c_ptr, c_ptr, c_ptr],
     "pf_axpy": [c_ptr, c_dbl, c_ptr, c_ptr, c_i64, c_ptr],
     "pf_wide_grad": [c_ptr, c_ptr, c_int, c_ptr, c_ptr, c_ptr],
+    "pf_cfl_peak": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
+    "pf_wall_forcing": [c_ptr, c_ptr, c_int, c_ptr, c_ptr, c_ptr, c_ptr,
+                        c_int, c_int, c_dbl, c_dbl, c_ptr, c_ptr, c_ptr],
     "pf_wide_grad_adjoint": [c_ptr, c_ptr, c_int, c_ptr, c_ptr, c_ptr],
     "pf_advective_outflow_update": [c_ptr, c_ptr, c_ptr, c_dbl, c_ptr,
                                     ctypes.POINTER(c_dbl), c_ptr],
@@ -202,6 +205,25 @@ def ptr(t):
         refs = _keep.refs = []
     refs.append(t)
     return c_ptr(t.data_ptr())
+
+
+class nvtx:
+    """NVTX range around a stage (SURVEY §5 tracing): visible in nsys /
+    ncu --nvtx timelines; PF_NVTX=0 turns the ranges off."""
+    on = os.environ.get("PF_NVTX", "1") != "0"
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        if nvtx.on:
+            torch.cuda.nvtx.range_push(self.name)
+        return self
+
+    def __exit__(self, *exc):
+        if nvtx.on:
+            torch.cuda.nvtx.range_pop()
+        return False
 
 
 def stream_of(device):

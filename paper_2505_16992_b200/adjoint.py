@@ -452,6 +452,11 @@ def gradcheck(fn, inputs, eps=None, mode="central", threshold=1e-4,
     return rep
 
 
+
+from .piso import _traced  # noqa: E402
+
+backward_step = _traced(backward_step, "backward_step")
+
 __all__ = ["GradientPath", "GradState", "backward_step", "backward_rollout",
            "GradcheckEntry", "GradcheckReport", "gradcheck",
            "backward_correct_velocity", "backward_pressure_solve",

@@ -217,7 +217,11 @@ class WallForcing:
     (wall_shear_mean / wall_forcing_source, S/piso.py:523-542), evaluated on
     the device from the first cell row next to every Dirichlet wall."""
 
-    def __init__(self, domain, device, wall_axis=1, flow_axis=0, delta=1.0):
+    def __init__(self, domain, device, wall_axis=1, flow_axis=0, delta=1.0,
+                 owned=None, counts=None):
+        """owned: optional (lo, hi) cell range the rows are restricted to,
+        counts: the per-wall row sizes to divide by (slab.SlabWallForcing:
+        the rank's owned cells, the global sizes)."""
         self.flow_axis = flow_axis
         self.delta = delta
         self.d = domain.dim
@@ -225,26 +229,47 @@ class WallForcing:
                  if f.kind == "dirichlet" and f.axis == wall_axis]
         if not walls:
             raise ValueError("no wall faces on that axis")
-        self.cells, self.inv_dist = [], []
+        cells, dists, seg = [], [], [0]
         for f in walls:
             cen = domain._cell_centres_of(
                 next(b for b in range(len(domain.blocks))
                      if domain.offsets[b] <= f.cells[0]
                      < domain.offsets[b + 1]), f.cells)
             dist = np.linalg.norm(cen - f.face_centers, axis=1)
-            self.cells.append(torch.as_tensor(f.cells, device=device))
-            self.inv_dist.append(torch.as_tensor(dist, dtype=F64,
-                                                 device=device))
+            c = np.asarray(f.cells)
+            if owned is not None:
+                keep = (c >= owned[0]) & (c < owned[1])
+                c, dist = c[keep], dist[keep]
+            dists.append(dist)
+            cells.append(c)
+            seg.append(seg[-1] + len(c))
+        self.domain = domain
+        self.cells = torch.as_tensor(np.concatenate(cells).astype(np.int32),
+                                     device=device)
+        self.dist = torch.as_tensor(np.concatenate(dists), dtype=F64,
+                                    device=device)
+        self.seg = torch.as_tensor(np.asarray(seg, dtype=np.int32),
+                                   device=device)
+        sizes = np.diff(seg).astype(np.float64) if counts is None \
+            else np.asarray(counts, dtype=np.float64)
+        self.cnt = torch.as_tensor(sizes, dtype=F64, device=device)
+        self.nwall, self.m = len(walls), seg[-1]
 
     def __call__(self, u, nu):
-        """(d,) device tensor source for the step whose input is u (n, d)."""
-        col = u[:, self.flow_axis]
-        vals = [torch.mean(col[c] / dist).abs()
-                for c, dist in zip(self.cells, self.inv_dist)]
-        shear = torch.stack(vals).mean()
-        s = torch.zeros(self.d, dtype=F64, device=u.device)
-        s[self.flow_axis] = nu * shear / self.delta
-        return s
+        """(d,) device tensor source for the step whose input is u (n, d):
+        one fused reduction kernel (pf_wall_forcing)."""
+        from . import _lib
+        from .piso import soa
+        plan = self.domain.device_plan(u.device)
+        out = torch.empty(self.d, dtype=F64, device=plan.device)
+        _lib.call("pf_wall_forcing", plan.handle,
+                  _lib.ptr(soa(u, self.domain.n, self.d, plan.device)),
+                  self.flow_axis, _lib.ptr(self.cells), _lib.ptr(self.dist),
+                  _lib.ptr(self.seg), _lib.ptr(self.cnt), self.nwall, self.m,
+                  float(nu),
+                  float(self.delta), _lib.ptr(out), _lib.ptr(plan.workspace),
+                  plan.stream)
+        return out
 
 
 def wall_forcing_source(domain, u, nu, wall_axis=1, flow_axis=0, delta=1.0):
@@ -255,19 +280,16 @@ def wall_forcing_source(domain, u, nu, wall_axis=1, flow_axis=0, delta=1.0):
 
 def adaptive_dt(domain, u, cfl_max, dt_max, remaining=None):
     """Largest dt with sum_a |U^a| / J <= cfl_max (S/piso.py:512-520)."""
-    from .piso import contravariant_flux
+    from . import _lib
+    from .piso import soa
     plan = domain.device_plan(u.device)
-    rate = contravariant_flux(domain, u).abs().sum(dim=1) / plan.jac
-    if getattr(plan, "comm", None) is not None:
-        # slab: the peak over this rank's owned cells, then the max over the
-        # ranks, so every rank takes the same dt (one global system)
-        from . import slab as _slab
-        lo, hi = domain.plane, domain.plane * (domain.nxl + 1)
-        peak_t = rate[lo:hi].max().reshape(1).clone()
-        _slab.allreduce_(plan, peak_t, op="max")
-        peak = float(peak_t.item())
-    else:
-        peak = float(rate.max())
+    # one fused kernel over the owned cells (pf_cfl_peak); on slab plans
+    # its reduction spans the ranks, so every rank takes the same dt
+    peak_t = torch.empty(1, dtype=F64, device=plan.device)
+    _lib.call("pf_cfl_peak", plan.handle,
+              _lib.ptr(soa(u, domain.n, domain.dim, plan.device)),
+              _lib.ptr(plan.workspace), _lib.ptr(peak_t), plan.stream)
+    peak = float(peak_t.item())
     dt = dt_max if peak == 0.0 else min(dt_max, cfl_max / peak)
     if remaining is not None:
         dt = min(dt, remaining)

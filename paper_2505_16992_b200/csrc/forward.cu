@@ -467,6 +467,99 @@ extern "C" int pf_divergence_max(const pf_plan *plan, const double *u,
   return d2h(pl, out_host, w.scalars, sizeof(double), S(stream));
 }
 
+// ---------------------------------------------------------------------------
+// channel drivers (S/piso.py:512-546): adaptive_dt's CFL peak and the
+// per-step wall forcing, each one fused reduction
+
+namespace pf {
+
+// max over owned cells of sum_a |U^a| / J (adaptive_dt, S/piso.py:512-520)
+template <class V>
+__global__ void __launch_bounds__(kBlock)
+    k_cfl_peak(V v, const double *__restrict__ u, double *partials,
+               unsigned *counter, double *out) {
+  constexpr int D = V::kDim;
+  double acc[1] = {0.0};
+  RANGE_LOOP(i, v.rng()) {
+    double r = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) r += fabs(v.flux(u, a, i));
+    acc[0] = fmax(acc[0], r / v.J(i));
+  }
+  double tot[1];
+  if (grid_reduce<1, true>(acc, partials, counter, tot)) *out = tot[0];
+}
+
+constexpr int kMaxWalls = 8;
+
+// wall_shear_mean / wall_forcing_source (S/piso.py:523-542): per wall w the
+// mean of u[c, flow] / dist over its first cell row (sum / cnt[w]: on slab
+// plans the sums span the ranks, cnt is the global row size), then
+// source[flow] = nu mean_w |mean_w| / delta, the other components 0
+__global__ void __launch_bounds__(kBlock)
+    k_wall_forcing(const double *__restrict__ u, int64_t n, int flow, int d,
+                   const int32_t *__restrict__ cells,
+                   const double *__restrict__ dist, const int32_t *seg,
+                   const double *cnt, int nwall, double nu, double delta,
+                   double *out,
+                   double *partials, unsigned *counter) {
+  double acc[kMaxWalls];
+#pragma unroll
+  for (int k = 0; k < kMaxWalls; ++k) acc[k] = 0.0;
+  const int32_t m = seg[nwall];
+  for (int32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += gridDim.x * blockDim.x) {
+    int w = 0;
+    while (w + 1 < nwall && e >= seg[w + 1]) ++w;
+    const double val = u[flow * n + cells[e]] / dist[e];
+#pragma unroll
+    for (int k = 0; k < kMaxWalls; ++k)
+      if (k == w) acc[k] += val;
+  }
+  double tot[kMaxWalls];
+  if (grid_reduce<kMaxWalls>(acc, partials, counter, tot)) {
+    double sh = 0.0;
+    for (int w = 0; w < nwall; ++w)
+      sh += fabs(tot[w] / cnt[w]);
+    sh /= nwall;
+    for (int c = 0; c < d; ++c) out[c] = c == flow ? nu * sh / delta : 0.0;
+  }
+}
+
+}  // namespace pf
+
+extern "C" int pf_cfl_peak(const pf_plan *plan, const double *u,
+                           void *workspace, double *out_dev, void *stream) {
+  PF_REQUIRE(plan && u && workspace && out_dev, "pf_cfl_peak: null argument");
+  const Plan &pl = P(plan);
+  Workspace w = carve(workspace, pl.d.n, pl.d.dim);
+  return dispatch(pl, [&](auto v) {
+    launch(k_cfl_peak<decltype(v)>, red_grid(pl, v.owned()), kBlock,
+           S(stream), v, u, w.partials, w.counters, out_dev);
+    PF_LAUNCH_CHECK("k_cfl_peak");
+    return PF_OK;
+  });
+}
+
+extern "C" int pf_wall_forcing(const pf_plan *plan, const double *u,
+                               int32_t flow_axis, const int32_t *cells,
+                               const double *dist, const int32_t *seg,
+                               const double *cnt, int32_t nwall, int32_t m,
+                               double nu,
+                               double delta, double *out_dev, void *workspace,
+                               void *stream) {
+  PF_REQUIRE(plan && u && cells && dist && seg && cnt && out_dev && workspace &&
+                 nwall >= 1 && nwall <= kMaxWalls && m >= 1,
+             "pf_wall_forcing: bad argument");
+  const Plan &pl = P(plan);
+  Workspace w = carve(workspace, pl.d.n, pl.d.dim);
+  launch(k_wall_forcing, red_grid(pl, m), kBlock, S(stream), u, pl.d.n,
+         (int)flow_axis, (int)pl.d.dim, cells, dist, seg, cnt, (int)nwall, nu,
+         delta, out_dev, w.partials, w.counters);
+  PF_LAUNCH_CHECK("k_wall_forcing");
+  return PF_OK;
+}
+
 extern "C" int pf_stencil_matvec(const pf_plan *plan, const double *a,
                                  int32_t transpose, int32_t ncomp,
                                  const double *x, double *y, void *stream) {

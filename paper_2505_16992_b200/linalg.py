@@ -111,10 +111,12 @@ def cg_solve(plan, data, b, x0=None, tol=None, maxiter=None,
                              "domain")
         mgw = plan.mg_workspace
     rep = _lib.SolverReportC()
-    _lib.call("pf_cg_solve", plan.handle, _lib.ptr(data), _lib.ptr(b),
-              float(b_scale), _lib.ptr(x), int(x0 is not None), tol, maxiter,
-              int(bool(zero_mean)), pc, _lib.ptr(plan.workspace),
-              _lib.ptr(mgw), ctypes.byref(rep), plan.stream)
+    with _lib.nvtx(stage):
+        _lib.call("pf_cg_solve", plan.handle, _lib.ptr(data), _lib.ptr(b),
+                  float(b_scale), _lib.ptr(x), int(x0 is not None), tol,
+                  maxiter, int(bool(zero_mean)), pc,
+                  _lib.ptr(plan.workspace), _lib.ptr(mgw), ctypes.byref(rep),
+                  plan.stream)
     report = _report(rep, stage)
     if not report.converged and raise_on_fail:
         raise SolverError(report)
@@ -144,10 +146,11 @@ def bicgstab_solve(plan, data, b, x0=None, tol=None, maxiter=None,
     # runs it (the library degrades it to Jacobi elsewhere)
     pc = PRECOND_NEUMANN2 if pc == -1 else \
         PRECOND_JACOBI if pc == PRECOND_MG else pc
-    _lib.call("pf_bicgstab_solve", plan.handle, _lib.ptr(data),
-              int(bool(transpose)), k, _lib.ptr(b2), _lib.ptr(x),
-              int(x0 is not None), tol, maxiter, pc,
-              _lib.ptr(plan.workspace), reps, plan.stream)
+    with _lib.nvtx(stages[0] if stages else stage):
+        _lib.call("pf_bicgstab_solve", plan.handle, _lib.ptr(data),
+                  int(bool(transpose)), k, _lib.ptr(b2), _lib.ptr(x),
+                  int(x0 is not None), tol, maxiter, pc,
+                  _lib.ptr(plan.workspace), reps, plan.stream)
     if stages is None:
         stages = [stage] * k
     reports = [_report(reps[q], stages[q]) for q in range(k)]

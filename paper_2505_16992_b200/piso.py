@@ -612,6 +612,19 @@ def piso_step(domain, state, cfg, workspace=None, tape=None):
     return new_state, diag
 
 
+
+def _traced(fn, name):
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        with _lib.nvtx(name):
+            return fn(*args, **kwargs)
+    return wrapper
+
+
+piso_step = _traced(piso_step, "piso_step")
+
 __all__ = ["FlowState", "StepConfig", "StepDiagnostics", "CorrectorTape",
            "StepTape", "PisoWorkspace", "make_state", "contravariant_flux",
            "assemble_momentum", "assemble_pressure", "momentum_rhs",

@@ -271,35 +271,23 @@ def halo_exchange(plan, *arrays):
 
 
 class SlabWallForcing:
-    """channel.WallForcing on a slab: the per-wall means of u/dist over the
-    owned wall cells, summed over the ranks (S/piso.py:523-542)."""
+    """channel.WallForcing on a slab: the per-wall sums of u/dist over the
+    rank's owned wall cells, added over the ranks inside the fused kernel's
+    reduction and divided by the global row sizes (S/piso.py:523-542)."""
 
     def __init__(self, slab, device, wall_axis=1, flow_axis=0, delta=1.0):
         from .channel import WallForcing
-        self._wf = WallForcing(slab, device, wall_axis, flow_axis, delta)
-        self.slab = slab
-        self.d = slab.dim
-        self.flow_axis, self.delta = flow_axis, delta
         lo, hi = slab.plane, slab.plane * (slab.nxl + 1)
-        self.masks = []
-        for cells in self._wf.cells:
-            self.masks.append(((cells >= lo) & (cells < hi)))
-        self.counts = [float(slab.nx * int(m.sum()) // max(slab.nxl, 1))
-                       for m in self.masks]
-        self.plan = slab.device_plan(device)
+        # the global row size of each wall: its owned cells x nx / nxl
+        probe = WallForcing(slab, device, wall_axis, flow_axis, delta,
+                            owned=(lo, hi))
+        owned = np.diff(probe.seg.cpu().numpy())
+        counts = [float(slab.nx * int(k) // max(slab.nxl, 1)) for k in owned]
+        self._wf = WallForcing(slab, device, wall_axis, flow_axis, delta,
+                               owned=(lo, hi), counts=counts)
 
     def __call__(self, u, nu):
-        col = u[:, self.flow_axis]
-        sums = torch.stack([
-            torch.where(m, col[c] / dist, torch.zeros_like(dist)).sum()
-            for c, dist, m in zip(self._wf.cells, self._wf.inv_dist,
-                                  self.masks)]).contiguous()
-        allreduce_(self.plan, sums)
-        vals = [(sums[k] / self.counts[k]).abs() for k in range(len(sums))]
-        shear = torch.stack(vals).mean()
-        s = torch.zeros(self.d, dtype=torch.float64, device=u.device)
-        s[self.flow_axis] = nu * shear / self.delta
-        return s
+        return self._wf(u, nu)
 
 
 __all__ = ["slab_bounds", "SlabDomain", "SlabComm", "SlabWallForcing",
