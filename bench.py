@@ -458,12 +458,9 @@ KERNEL_BYTES = {
 # xr: diag 8 + per comp x r/w, p, r, v, t, rhat read, r written (64)
 BI_BYTES = {"k_bi_pv": 56 + 3 * 48, "k_bi_st": 56 + 3 * 24,
             "k_bi_xr": 8 + 3 * 64,
-            # Neumann-2 passes: 6 off-diagonal rows + 1/A (no diagonal row);
-            # per component pv reads r, p, v, r^ and writes p', v'; st reads
-            # r, v' and writes t; xr on z reads z, p', r, v', t, r^ and
-            # writes z, r (no 1/A)
-            "k_bi_nm_pv": 48 + 8 + 3 * 48, "k_bi_nm_st": 48 + 8 + 3 * 24,
-            "k_bi_xr_z": 3 * 64}
+            # Neumann-2 passes (kernel_bytes): 6 off-diagonal rows + 1/A
+            "k_bi_nm_rpv": 48 + 8 + 3 * 80, "k_bi_nm_st": 48 + 8 + 3 * 32}
+
 
 def kernel_bytes(nm, d):
     """Algorithmic bytes per cell of kernel `nm` in d dimensions (the
@@ -471,8 +468,12 @@ def kernel_bytes(nm, d):
     form d faces, the multigrid transfers 1/2^d coarse values)."""
     rows = 2 * d + 1
     bi = {"k_bi_pv": 8 * rows + d * 48, "k_bi_st": 8 * rows + d * 24,
-          "k_bi_xr": 8 + d * 64, "k_bi_nm_pv": 16 * d + 8 + d * 48,
-          "k_bi_nm_st": 16 * d + 8 + d * 24, "k_bi_xr_z": d * 64}
+          "k_bi_xr": 8 + d * 64,
+          # Neumann-2: 2d off-diagonal rows + 1/A; per component the merged
+          # pass reads r, v, p, t, r^, z and writes r', z, p', v'; st reads
+          # r, v', r^ and writes t
+          "k_bi_nm_rpv": 16 * d + 8 + d * 80,
+          "k_bi_nm_st": 16 * d + 8 + d * 32}
     if nm in bi:
         return bi[nm]
     co = 8.0 / 2 ** d
@@ -539,10 +540,12 @@ def measure_roofline(args, dom, plan, state, nu, dt, dev, per_step):
         bm = (ctypes.c_double * 5)()
         _lib.call("pf_bicgstab_profile", plan.handle, _lib.ptr(c), trans, d,
                   _lib.ptr(bb), 8, _lib.ptr(plan.workspace), bm, plan.stream)
-        names = (("k_bi_nm_pv", "k_bi_nm_st", "k_bi_xr_z") if bm[4] == 3
+        # Neumann-2: the x/r update rides in the next pv pass (k_bi_nm_rpv)
+        names = (("k_bi_nm_rpv", "k_bi_nm_st", None) if bm[4] == 3
                  else ("k_bi_pv", "k_bi_st", "k_bi_xr"))
         for j, nm in enumerate(names):
-            bi[nm + tag] = float(bm[j])
+            if nm is not None:
+                bi[nm + tag] = float(bm[j])
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -591,7 +594,7 @@ def measure_roofline(args, dom, plan, state, nu, dt, dev, per_step):
                 "preconditioner": plan.geom_kind if mg else "jacobi",
                 "ms": it_ms, "ms_graph_replay": float(ms[10])},
             "whole_step": whole_step_bytes(d, per_step, n, peak,
-                                           nm_bi="k_bi_nm_pv" in "".join(bi))}
+                                           nm_bi="k_bi_nm_rpv" in "".join(bi))}
 
 
 def whole_step_bytes(d, per_step, n, peak, nm_bi):
@@ -600,8 +603,9 @@ def whole_step_bytes(d, per_step, n, peak, nm_bi):
     counts), times the cells, over the measured step time.  Per-op bytes
     (fp64, s = 8, q = 2d+1 stencil rows):
       momentum assembly + rhs 16 s; pressure assembly (2d+2) s;
-      BiCGStab per lock-step iteration: this repo's three passes (Neumann-2
-        520 B, Jacobi 528 B in 3D) + per solve the init pass (reads b, x,
+      BiCGStab per lock-step iteration: this repo's passes (Neumann-2: the
+        merged x/r + pv pass and st, 448 B; Jacobi: pv, st, x/r, 528 B in
+        3D) + per solve the init pass (reads b, x,
         C; writes r, r^, 1/A), the verification (b, x, C) and, Neumann-2,
         the close pass (z, 1/A, N, x);
       per corrector: h-stage + divergence (q+3d+1) s, correction (2d+2) s;
@@ -613,8 +617,8 @@ def whole_step_bytes(d, per_step, n, peak, nm_bi):
     Counts per step: 1 forward + 1 adjoint BiCGStab solve (d components
     batched), 2 correctors, the CG iterations reported."""
     s, q = 8, 2 * d + 1
-    bi_it = kernel_bytes("k_bi_nm_pv", d) + kernel_bytes("k_bi_nm_st", d) \
-        + kernel_bytes("k_bi_xr_z", d) if nm_bi else \
+    bi_it = kernel_bytes("k_bi_nm_rpv", d) + kernel_bytes("k_bi_nm_st", d) \
+        if nm_bi else \
         kernel_bytes("k_bi_pv", d) + kernel_bytes("k_bi_st", d) \
         + kernel_bytes("k_bi_xr", d)
     bi_solve = s * (q + 5 * d + 1) + s * (q + 2 * d) \

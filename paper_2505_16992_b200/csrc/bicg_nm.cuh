@@ -20,9 +20,15 @@
 // leaves the SM.  Only the six off-diagonal rows of A are read (N); the
 // diagonal enters through 1/A_jj.  Two barriers per plane step.
 //
-// The iterate is kept in preconditioned form: x = x0 + M^-1 z with
-// z += alpha p + omega s (k_bi_xr<true>), and one closing pass (MODE 2)
-// forms x once per solve.
+// The iterate is kept in preconditioned form: x = x0 + M^-1 z, and one
+// closing pass forms x once per solve.  The x/r update of iteration k is
+// folded into the pv pass of iteration k+1 (MODE 3): that pass forms
+// s = r - alpha v, r' = s - omega t and p' = r' + beta (p - omega v) at
+// every stencil point from r, v, p, t, stores r' and z += alpha p + omega s
+// at its own cells, and applies A M^-1 to p'.  beta needs r^.r' before the
+// pass: the st pass sums r^.s and r^.t too, and r^.r' = r^.s - omega r^.t
+// (linearity; S/linalg.py:206-209 forms the same dot directly).  Per
+// iteration the passes move 296 + 152 B/cell instead of 200 + 128 + 192.
 //
 // Slab plans (one ghost plane per side): stage 1 at a ghost plane would
 // need the raw inputs two planes outside the slab.  Instead each pass first
@@ -50,13 +56,14 @@ constexpr int kNPairs = kNP / 2;                       // 216 Z-pairs
 constexpr int kNRing1 = (kTY + 2) * (kTZ + 2) - kTY * kTZ;  // 84 halo-1 cells
 static_assert(kNZ % 2 == 0 && kNPairs <= kTileThreads, "pair layout");
 
-// shared memory, in doubles: raw[10][kNP] | g1[3 slots][3][kNP] |
-// q1[4 slots][3][kNP] | beta/alpha, omega [2][3]
+// shared memory, in doubles: raw[13][kNP] (r, v, p, t x 3, 1/A) |
+// g1[3 slots][3][kNP] | q1[4 slots][3][kNP] | iteration scalars [3][3]
 // (q1 keeps four planes: stage 2 of plane q-3 reads q-4, q-3, q-2 while
 // stage 1 writes q-1, and reads its X neighbours from the ring)
-constexpr int kNmRaw = 0, kNmG1 = 10 * kNP, kNmQ1 = kNmG1 + 9 * kNP,
-              kNmCo = kNmQ1 + 12 * kNP, kNmEnd = kNmCo + 8;
-constexpr size_t kNmSmem = sizeof(double) * kNmEnd;   // 107,200 B
+constexpr int kNmRawN = 13, kNmDi = 12;  // raw arrays; 1/A's slot
+constexpr int kNmRaw = 0, kNmG1 = kNmRawN * kNP, kNmQ1 = kNmG1 + 9 * kNP,
+              kNmCo = kNmQ1 + 12 * kNP, kNmEnd = kNmCo + 10;
+constexpr size_t kNmSmem = sizeof(double) * kNmEnd;   // 117,584 B
 
 // halo-1 ring cell k (0..83) in plane coordinates
 __device__ __forceinline__ void nm_ring1(int k, int &sy, int &sz) {
@@ -81,7 +88,9 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 // indices only).  row[f]: stencil row of face f (-x +x -y +y -z +z) of A,
 // or for A^T the neighbour's back-face row, read at the neighbour.
 struct NmArgs {
-  const double *src[3][3];  // raw array k of component q: r, v, p | z
+  const double *src[4][3];  // raw array k of component q: r, v, p, t | z
+  double *rout[3];          // MODE 3: r' (the other r buffer)
+  double *zio[3];           // MODE 3: the preconditioned iterate z
   const double *dinv;
   const double *row[6];
   const double *rhat[3];
@@ -152,6 +161,9 @@ __device__ __forceinline__ void nm_coefs(const NmArgs &g, int32_t b,
 //                   t.t, t.s -> early exit / omega
 // MODE 2 (close):   y = z (the preconditioned iterate); x += M^-1 z
 //                   (stage 1 only, no reduction)
+// MODE 3 (x/r + pv): iteration k's update fused into iteration k+1's pv
+//                   (above): r', z and p', v' = A M^-1 p'; sums r^.v',
+//                   |r'|^2 -> convergence, alpha
 // edge (MODE 0 / 1): stage 1 only on one plane per chunk, stored to Q
 template <bool kTrans, int MODE, bool kFirst = false, int kMinB = 2>
 __global__ void __launch_bounds__(kTileThreads, kMinB)
@@ -159,16 +171,21 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
             const __grid_constant__ NmArgs g, SolverState *st, double *partials,
             unsigned *counter, int edge) {
   if (MODE != 2 && st->all_done) return;
-  constexpr int K = MODE == 1 ? 9 : 3;
+  constexpr int K = MODE == 1 ? 15 : MODE == 3 ? 6 : 3;
   constexpr bool kClose = MODE == 2;
-  // arrays per component in the raw buffer: r, v, p (pv) | r, v (st) | z
-  constexpr int kArr = kClose || (MODE == 0 && kFirst) ? 1 : MODE == 0 ? 3 : 2;
+  constexpr bool kRpv = MODE == 3;
+  // arrays per component in the raw buffer: r, v, p (pv) | r, v (st) | z |
+  // r, v, p, t (x/r + pv)
+  constexpr int kArr = kClose || (MODE == 0 && kFirst) ? 1
+                       : MODE == 0 ? 3 : MODE == 3 ? 4 : 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double *const sm = reinterpret_cast<double *>(smem_raw);
   const int nc = st->ncomp;
-  bool act[3];
-  // the iteration scalars live in shared memory (read where y is formed)
-  double *const c0 = sm + kNmCo, *const c1 = sm + kNmCo + 3;
+  bool act[3], pend[3];
+  // the iteration scalars live in shared memory (read where y is formed):
+  // pv: beta, omega | st: alpha | x/r + pv: alpha, omega, beta
+  double *const c0 = sm + kNmCo, *const c1 = sm + kNmCo + 3,
+               *const c2 = sm + kNmCo + 6;
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
     // closing pass: the components that iterated and did not break down
@@ -176,11 +193,15 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
     act[q] = q < nc && (kClose ? (st->c[q].active && !st->c[q].zero_rhs &&
                                   st->c[q].iter > 0 && !st->c[q].fail)
                                : !st->c[q].done);
+    // x/r + pv: components that converged at s only take z += alpha p
+    pend[q] = kRpv && q < nc && st->c[q].pending;
   }
   if (threadIdx.x < 3) {
     const int q = threadIdx.x;
-    c0[q] = q < nc ? (MODE == 0 ? st->c[q].beta : st->c[q].alpha) : 0.0;
-    c1[q] = q < nc && MODE == 0 ? st->c[q].omega : 0.0;
+    const bool ok = q < nc;
+    c0[q] = !ok ? 0.0 : MODE == 0 ? st->c[q].beta : st->c[q].alpha;
+    c1[q] = ok && (MODE == 0 || kRpv) ? st->c[q].omega : 0.0;
+    c2[q] = ok && kRpv ? st->c[q].beta : 0.0;
   }
   const bool one = kClose || edge;
   const int tid = threadIdx.x;
@@ -231,19 +252,19 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
           double *dst = sm + kNmRaw + ep;
           if (b < 0 || !okp) {
 #pragma unroll
-            for (int k = 0; k < 10; ++k)
+            for (int k = 0; k < kNmRawN; ++k)
               *reinterpret_cast<double2 *>(dst + k * kNP) =
                   make_double2(0.0, 0.0);
           } else {
             const int32_t j = b + offp;
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
-              if (!on(q)) continue;
+              if (!on(q) && !pend[q]) continue;
 #pragma unroll
               for (int k = 0; k < kArr; ++k)
                 cp_async16(dst + (3 * k + q) * kNP, g.src[k][q] + j);
             }
-            cp_async16(dst + 9 * kNP, g.dinv + j);
+            cp_async16(dst + kNmDi * kNP, g.dinv + j);
           }
         }
         cp_async_commit();
@@ -254,6 +275,11 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
         const double rr = rw[q * kNP];
         if (kArr == 1) return rr;
         const double vv = rw[(3 + q) * kNP];
+        if (kRpv) {
+          const double om = c1[q];
+          const double rn = (rr - c0[q] * vv) - om * rw[(9 + q) * kNP];
+          return rn + c2[q] * (rw[(6 + q) * kNP] - om * vv);
+        }
         return MODE == 0 ? rr + c0[q] * (rw[(6 + q) * kNP] - c1[q] * vv)
                          : rr - c0[q] * vv;
       };
@@ -313,7 +339,7 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
           const int32_t bm = kTrans ? nm_pbase(g, x3 - 1) : 0;
           const int32_t bp = kTrans ? nm_pbase(g, x3 + 1) : 0;
           nm_coefs<kTrans>(g, b3, bm, bp, own, cA);
-          if (MODE == 0) {
+          {
 #pragma unroll
             for (int c = 0; c < 3; ++c)
               if (on(c)) rh[c] = __ldg(g.rhat[c] + i3);
@@ -333,7 +359,7 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
         if (q <= qconv) {
           if (has_pair) {
             const double2 dj = *reinterpret_cast<const double2 *>(
-                sm + kNmRaw + 9 * kNP + ep);
+                sm + kNmRaw + kNmDi * kNP + ep);
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
               if (!on(c)) continue;
@@ -345,6 +371,33 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
           if (!one) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) yd[c] = on(c) ? yval(eo, c) : 0.0;
+          }
+          if constexpr (MODE == 0 && kFirst) if (!edge && q >= xs && q < xe) {
+            // the first iteration starts the preconditioned iterate z at 0
+            const int32_t io = nm_pbase(g, q) + own.off;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              if (c < nc && g.zio[c]) g.zio[c][io] = 0.0;
+          }
+          if constexpr (kRpv) if (!edge && q >= xs && q < xe) {
+            // iteration k's x/r update at the own cell of an owned plane
+            const double *rw = sm + kNmRaw + eo;
+            const int32_t io = nm_pbase(g, q) + own.off;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              if (!on(c) && !pend[c]) continue;
+              const double al = c0[c], pp = rw[(6 + c) * kNP];
+              if (on(c)) {
+                const double om = c1[c];
+                const double sv = rw[c * kNP] - al * rw[(3 + c) * kNP];
+                const double rn = sv - om * rw[(9 + c) * kNP];
+                g.rout[c][io] = rn;
+                g.zio[c][io] += al * pp + om * sv;
+                acc[3 + c] += rn * rn;
+              } else {
+                g.zio[c][io] += al * pp;
+              }
+            }
           }
         }
         if (S2) {
@@ -359,13 +412,15 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
                                cA[4] * qq[-1] + cA[5] * qq[1];
             const double out = ya[c] - off;
             g.out2[c][i3] = out;
-            if (MODE == 0) {
+            if constexpr (MODE == 0 || kRpv) {
               g.out1[c][i3] = ya[c];
               acc[c] += rh[c] * out;
             } else {
-              acc[3 * c] += ya[c] * ya[c];
-              acc[3 * c + 1] += out * out;
-              acc[3 * c + 2] += out * ya[c];
+              acc[5 * c] += ya[c] * ya[c];
+              acc[5 * c + 1] += out * out;
+              acc[5 * c + 2] += out * ya[c];
+              acc[5 * c + 3] += rh[c] * ya[c];   // r^.s
+              acc[5 * c + 4] += rh[c] * out;     // r^.t
             }
           }
         }
@@ -461,11 +516,46 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
     run(std::true_type{});
   else
     run(std::false_type{});
+  (void)pend;
 
   if (kClose || edge) return;
   double tot[K];
   if (!grid_reduce<K>(acc, partials, counter, tot)) return;
-  if (MODE == 0) {
+  if constexpr (kRpv) {
+    // iteration k completes: convergence on r', else iteration k + 1's
+    // alpha (its rho is the st pass's rho_next, which beta used)
+    int all = 1;
+    for (int q = 0; q < nc; ++q) {
+      CompState &c = st->c[q];
+      if (pend[q]) c.pending = 0;
+      if (act[q]) {
+        c.res = sqrt(tot[3 + q]);
+        if (c.res <= c.tol_abs) {
+          c.converged = 1;
+          c.done = 1;
+        } else if (c.iter >= c.maxiter) {
+          c.done = 1;
+        } else if (c.brk_next) {
+          c.fail = 1;
+          c.done = 1;
+        } else {
+          c.rho = c.rho_new;
+          c.iter += 1;
+          c.rho_new = c.rho_next;
+          if (fabs(tot[q]) < DBL_MIN) {
+            c.fail = 1;
+            c.done = 1;
+          } else {
+            c.alpha = c.rho_new / tot[q];
+          }
+        }
+      }
+      if (!c.done) all = 0;
+    }
+    st->all_done = all;
+    return;
+  }
+  if constexpr (MODE == 0) {
     int all = 1;
     for (int q = 0; q < nc; ++q) {
       CompState &c = st->c[q];
@@ -480,21 +570,26 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
       if (!c.done) all = 0;
     }
     st->all_done = all;
-  } else {
-    // all_done is left alone: k_bi_xr applies the early-exit update
+  } else if constexpr (MODE == 1) {
+    // all_done is left alone: the x/r + pv pass applies the early-exit
+    // update; rho_next = r^.r' and beta for that pass
     for (int q = 0; q < nc; ++q) {
       CompState &c = st->c[q];
       if (!act[q]) continue;
-      c.res = sqrt(tot[3 * q]);
+      c.res = sqrt(tot[5 * q]);
       if (c.res <= c.tol_abs) {
         c.converged = 1;
         c.done = 1;
         c.pending = 1;
-      } else if (tot[3 * q + 1] < DBL_MIN) {
+      } else if (tot[5 * q + 1] < DBL_MIN) {
         c.fail = 1;
         c.done = 1;
       } else {
-        c.omega = tot[3 * q + 2] / tot[3 * q + 1];
+        c.omega = tot[5 * q + 2] / tot[5 * q + 1];
+        c.rho_next = tot[5 * q + 3] - c.omega * tot[5 * q + 4];
+        c.brk_next = fabs(c.rho_next) < DBL_MIN || fabs(c.omega) < DBL_MIN;
+        c.beta = c.brk_next ? 0.0
+                            : (c.rho_next / c.rho_new) * (c.alpha / c.omega);
       }
     }
   }

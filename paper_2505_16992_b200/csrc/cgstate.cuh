@@ -8,9 +8,13 @@ namespace pf {
 
 struct CompState {
   double bnorm, tol_abs, res, rho, rho_new, alpha, omega, beta;
-  double zbar, rz, xmean, true_res, bmean, rmean, tol, pad1;
+  // rho_next: r^.r of the next iteration, formed by the merged BiCGStab
+  // passes from the st-pass sums (r^.s - omega r^.t) before r is
+  double zbar, rz, xmean, true_res, bmean, rmean, tol, rho_next;
   int32_t iter, maxiter, done, converged, fail, zero_rhs, pending, active;
-  int32_t project_x, pad2[7];
+  // brk_next: rho_next or omega vanished -- a breakdown unless the update
+  // that follows converges
+  int32_t project_x, brk_next, pad2[6];
 };
 
 struct SolverState {

@@ -378,6 +378,9 @@ struct BiVecs {
   double *r, *rhat, *t;   // each (ncomp, n)
   double *p[2], *v[2];    // ping-pong by iteration parity
   double *dinv;           // (n) Jacobi: 1 / A_ii (ones when unpreconditioned)
+  double *rb[2] = {nullptr, nullptr};  // merged Neumann-2 passes: r by
+                                       // parity (rb[0] = r)
+  double *z = nullptr;    // Neumann-2: the preconditioned iterate
 };
 
 __global__ void k_bi_reset(SolverState *st, int ncomp, int maxiter,
@@ -1695,21 +1698,27 @@ bool nm_geo(const Plan &pl, const V &v, TileGeo &tg, TileGeo *edge = nullptr) {
   return true;
 }
 
+// rpar: which r buffer (bv.rb) the pass reads (MODE 1, 3); MODE 3 writes
+// the other
 template <bool kTrans, int MODE>
 void launch_nm(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
                const BiVecs &bv, int par, int64_t n, SolverState *st,
                Workspace &w, int first = 0, const double *zin = nullptr,
                double *xout = nullptr, const double *qghost = nullptr,
-               double *qedge = nullptr) {
+               double *qedge = nullptr, int rpar = 0) {
   NmArgs g{};
+  const double *rin = bv.rb[0] ? bv.rb[rpar] : bv.r;
   for (int q = 0; q < 3; ++q) {
     const int64_t o = q * n;
-    g.src[0][q] = (MODE == 2 ? zin : bv.r) + o;
-    g.src[1][q] = (MODE == 0 ? bv.v[par] : bv.v[par ^ 1]) + o;
+    g.src[0][q] = (MODE == 2 ? zin : rin) + o;
+    g.src[1][q] = (MODE == 0 || MODE == 3 ? bv.v[par] : bv.v[par ^ 1]) + o;
     g.src[2][q] = bv.p[par] + o;
+    g.src[3][q] = bv.t + o;
+    g.rout[q] = bv.rb[0] ? bv.rb[rpar ^ 1] + o : nullptr;
+    g.zio[q] = bv.z ? bv.z + o : nullptr;
     g.rhat[q] = bv.rhat + o;
     g.out1[q] = (MODE == 2 ? xout : qedge ? qedge : bv.p[par ^ 1]) + o;
-    g.out2[q] = (MODE == 0 ? bv.v[par ^ 1] : bv.t) + o;
+    g.out2[q] = (MODE == 0 || MODE == 3 ? bv.v[par ^ 1] : bv.t) + o;
     g.qghost[q] = qghost ? qghost + o : nullptr;
   }
   g.dinv = bv.dinv;
@@ -1755,6 +1764,64 @@ void launch_nm(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
   go(k_bi_nm<kTrans, MODE, false>);
 }
 
+// One Neumann-2 BiCGStab iteration i (0-based): the pv pass (i = 0) or
+// the merged pass (iteration i-1's x/r update + iteration i's pv), then
+// the st pass; slab plans first run each stencil pass's edge planes and
+// exchange them (Q).  r ping-pongs: iteration i reads rb[i & 1].
+template <bool kTrans>
+void nm_iteration(const Plan &pl, const TileGeo &tgn, const TileGeo &tge,
+                  int ngrid, int egrid, cudaStream_t s, const double *a,
+                  const BiVecs &bv, int i, int64_t n, int ncomp,
+                  SolverState *st, Workspace &w, double *qg) {
+  const int par = i & 1;
+  if (i == 0) {
+    halo(pl, s, {{bv.rb[0], ncomp}, {bv.p[par], ncomp}});
+    if (qg) {
+      launch_nm<kTrans, 0>(tge, egrid, s, a, bv, par, n, st, w, 1, nullptr,
+                           nullptr, nullptr, qg);
+      halo(pl, s, {{qg, ncomp}});
+    }
+    launch_nm<kTrans, 0>(tgn, ngrid, s, a, bv, par, n, st, w, 1, nullptr,
+                         nullptr, qg);
+  } else {
+    const int rp = (i - 1) & 1;
+    halo(pl, s, {{bv.rb[rp], ncomp}, {bv.p[par], ncomp}, {bv.t, ncomp}});
+    if (qg) {
+      launch_nm<kTrans, 3>(tge, egrid, s, a, bv, par, n, st, w, 0, nullptr,
+                           nullptr, nullptr, qg, rp);
+      halo(pl, s, {{qg, ncomp}});
+    }
+    launch_nm<kTrans, 3>(tgn, ngrid, s, a, bv, par, n, st, w, 0, nullptr,
+                         nullptr, qg, nullptr, rp);
+  }
+  halo(pl, s, {{bv.v[par ^ 1], ncomp}, {bv.rb[par], ncomp}});
+  if (qg) {
+    launch_nm<kTrans, 1>(tge, egrid, s, a, bv, par, n, st, w, 0, nullptr,
+                         nullptr, nullptr, qg, par);
+    halo(pl, s, {{qg, ncomp}});
+  }
+  launch_nm<kTrans, 1>(tgn, ngrid, s, a, bv, par, n, st, w, 0, nullptr,
+                       nullptr, qg, nullptr, par);
+}
+
+// after `launched` iterations: the x/r update of the last one
+template <bool kTrans>
+void nm_finish(const Plan &pl, const TileGeo &tgn, const TileGeo &tge,
+               int ngrid, int egrid, cudaStream_t s, const double *a,
+               const BiVecs &bv, int launched, int64_t n, int ncomp,
+               SolverState *st, Workspace &w, double *qg) {
+  if (launched < 1) return;
+  const int i = launched, par = i & 1, rp = (i - 1) & 1;
+  halo(pl, s, {{bv.rb[rp], ncomp}, {bv.p[par], ncomp}, {bv.t, ncomp}});
+  if (qg) {
+    launch_nm<kTrans, 3>(tge, egrid, s, a, bv, par, n, st, w, 0, nullptr,
+                         nullptr, nullptr, qg, rp);
+    halo(pl, s, {{qg, ncomp}});
+  }
+  launch_nm<kTrans, 3>(tgn, ngrid, s, a, bv, par, n, st, w, 0, nullptr,
+                       nullptr, qg, nullptr, rp);
+}
+
 template <class V, bool kTrans>
 int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
             SolverState &hs, const double *a, const double *b, double *x,
@@ -1786,6 +1853,11 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   const int egrid = nm ? std::min(tge.ntiles, nm_minb() * pl.num_sms) : 0;
   double *z = base + 8 * len;  // the preconditioned iterate (nm)
   double *qg = pl.slab ? base + 9 * len : nullptr;  // slab edge stage 1
+  if (nm) {
+    bv.rb[0] = bv.r;
+    bv.rb[1] = base + 10 * len;
+    bv.z = z;
+  }
   launch(k_bi_reset, 1, 1, s, st, ncomp, maxiter, precond, tol, fresh, mask);
   // the tiled init pass forms |b| itself
   if (fresh && !tiled)
@@ -1819,42 +1891,27 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
                                             : next_batch(launched, 0),
                              maxiter - launched);
     for (int k = 0; k < bsz; ++k) {
-      const int par = (launched + k) & 1;
-      halo(pl, s, {{bv.r, ncomp}, {bv.p[par], ncomp}});
-      if (nm && qg) {
-        launch_nm<kTrans, 0>(tge, egrid, s, a, bv, par, (int64_t)n, st, w,
-                             launched + k == 0, nullptr, nullptr, nullptr, qg);
-        halo(pl, s, {{qg, ncomp}});
+      const int i = launched + k, par = i & 1;
+      if (nm) {
+        nm_iteration<kTrans>(pl, tgn, tge, ngrid, egrid, s, a, bv, i,
+                             (int64_t)n, ncomp, st, w, qg);
+        continue;
       }
-      if (nm)
-        launch_nm<kTrans, 0>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w,
-                             launched + k == 0, nullptr, nullptr, qg);
-      else if (tiled)
+      halo(pl, s, {{bv.r, ncomp}, {bv.p[par], ncomp}});
+      if (tiled)
         launch_tiled<kTrans, 0>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w,
-                                nullptr, nullptr, 0, launched + k == 0);
+                                nullptr, nullptr, 0, i == 0);
       else
         launch(k_bi_pv<V, kTrans>, gr, kBlock, s, v, a, bv, par, st,
                w.partials, w.counters);
       halo(pl, s, {{bv.v[par ^ 1], ncomp}});
-      if (nm && qg) {
-        launch_nm<kTrans, 1>(tge, egrid, s, a, bv, par, (int64_t)n, st, w, 0,
-                             nullptr, nullptr, nullptr, qg);
-        halo(pl, s, {{qg, ncomp}});
-      }
-      if (nm)
-        launch_nm<kTrans, 1>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w, 0,
-                             nullptr, nullptr, qg);
-      else if (tiled)
+      if (tiled)
         launch_tiled<kTrans, 1>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
       else
         launch(k_bi_st<V, kTrans>, gr, kBlock, s, v, a, bv, par, st,
                w.partials, w.counters);
-      if (nm)
-        launch(k_bi_xr<true>, gr, kBlock, s, a, bv, par, z, n, rg, st,
-               w.partials, w.counters, (int)(launched + k == 0));
-      else
-        launch(k_bi_xr<false>, gr, kBlock, s, a, bv, par, x, n, rg, st,
-               w.partials, w.counters, 0);
+      launch(k_bi_xr<false>, gr, kBlock, s, a, bv, par, x, n, rg, st,
+             w.partials, w.counters, 0);
     }
     PF_LAUNCH_CHECK("bicgstab iterations");
     launched += bsz;
@@ -1869,6 +1926,10 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     pl.bi_hint[kTrans ? 1 : 0] = lock;
   }
   if (nm) {
+    // the last iteration's x/r update (a merged pass whose pv part goes
+    // unused; it returns at once when a poll already saw convergence)
+    nm_finish<kTrans>(pl, tgn, tge, ngrid, egrid, s, a, bv, launched,
+                      (int64_t)n, ncomp, st, w, qg);
     // x = x0 + M^-1 z: a one-stage stencil, on the single-halo tiled pass
     halo(pl, s, {{z, ncomp}});
     launch_tiled<kTrans, 4>(tg, tgrid, s, a, bv, 0, (int64_t)n, st, w, z,
@@ -2160,26 +2221,91 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
     cudaEvent_t ev[4];
     for (auto &e : ev) PF_CUDA(cudaEventCreate(&e));
     double tot[4] = {0, 0, 0, 0};
-    for (int k = 0; k < iters; ++k) {
+    if (nm) {
+      // Neumann-2: iteration 0 (pv) untimed, then per iteration the merged
+      // x/r + pv pass and the st pass (no separate x/r pass)
+      bv.rb[0] = bv.r;
+      bv.rb[1] = w.vecs + 11 * len;
+      bv.z = z;
+      auto one = [&](int k, bool timed) -> int {
+        const int par = k & 1;
+        if (timed) PF_CUDA(cudaEventRecord(ev[0], s));
+        if (k == 0) {
+          halo(pl, s, {{bv.rb[0], ncomp}, {bv.p[par], ncomp}});
+          if (qg) {
+            if (transpose)
+              launch_nm<true, 0>(tge, egrid, s, a, bv, par, (int64_t)n, st, w,
+                                 1, nullptr, nullptr, nullptr, qg);
+            else
+              launch_nm<false, 0>(tge, egrid, s, a, bv, par, (int64_t)n, st,
+                                  w, 1, nullptr, nullptr, nullptr, qg);
+            halo(pl, s, {{qg, ncomp}});
+          }
+          if (transpose)
+            launch_nm<true, 0>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w, 1,
+                               nullptr, nullptr, qg);
+          else
+            launch_nm<false, 0>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w,
+                                1, nullptr, nullptr, qg);
+        } else {
+          const int rp = (k - 1) & 1;
+          halo(pl, s, {{bv.rb[rp], ncomp}, {bv.p[par], ncomp}, {bv.t, ncomp}});
+          if (qg) {
+            if (transpose)
+              launch_nm<true, 3>(tge, egrid, s, a, bv, par, (int64_t)n, st, w,
+                                 0, nullptr, nullptr, nullptr, qg, rp);
+            else
+              launch_nm<false, 3>(tge, egrid, s, a, bv, par, (int64_t)n, st,
+                                  w, 0, nullptr, nullptr, nullptr, qg, rp);
+            halo(pl, s, {{qg, ncomp}});
+          }
+          if (transpose)
+            launch_nm<true, 3>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w, 0,
+                               nullptr, nullptr, qg, nullptr, rp);
+          else
+            launch_nm<false, 3>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w,
+                                0, nullptr, nullptr, qg, nullptr, rp);
+        }
+        if (timed) PF_CUDA(cudaEventRecord(ev[1], s));
+        halo(pl, s, {{bv.v[par ^ 1], ncomp}, {bv.rb[par], ncomp}});
+        if (qg) {
+          if (transpose)
+            launch_nm<true, 1>(tge, egrid, s, a, bv, par, (int64_t)n, st, w, 0,
+                               nullptr, nullptr, nullptr, qg, par);
+          else
+            launch_nm<false, 1>(tge, egrid, s, a, bv, par, (int64_t)n, st, w,
+                                0, nullptr, nullptr, nullptr, qg, par);
+          halo(pl, s, {{qg, ncomp}});
+        }
+        if (transpose)
+          launch_nm<true, 1>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w, 0,
+                             nullptr, nullptr, qg, nullptr, par);
+        else
+          launch_nm<false, 1>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w, 0,
+                              nullptr, nullptr, qg, nullptr, par);
+        if (!timed) return PF_OK;
+        PF_CUDA(cudaEventRecord(ev[2], s));
+        PF_CUDA(cudaEventRecord(ev[3], s));
+        PF_CUDA(cudaEventSynchronize(ev[3]));
+        for (int j = 0; j < 3; ++j) {
+          float ms = 0.f;
+          PF_CUDA(cudaEventElapsedTime(&ms, ev[j], ev[j + 1]));
+          tot[j] += ms;
+        }
+        float ms = 0.f;
+        PF_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[3]));
+        tot[3] += ms;
+        return PF_OK;
+      };
+      int rc = one(0, false);
+      for (int k = 1; k <= iters && !rc; ++k) rc = one(k, true);
+      if (rc) return rc;
+    }
+    for (int k = 0; k < iters && !nm; ++k) {
       const int par = k & 1;
       halo(pl, s, {{bv.r, ncomp}, {bv.p[par], ncomp}});
       PF_CUDA(cudaEventRecord(ev[0], s));
-      if (nm && qg) {
-        if (transpose)
-          launch_nm<true, 0>(tge, egrid, s, a, bv, par, (int64_t)n, st, w,
-                             k == 0, nullptr, nullptr, nullptr, qg);
-        else
-          launch_nm<false, 0>(tge, egrid, s, a, bv, par, (int64_t)n, st, w,
-                              k == 0, nullptr, nullptr, nullptr, qg);
-        halo(pl, s, {{qg, ncomp}});
-      }
-      if (nm && transpose)
-        launch_nm<true, 0>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w,
-                           k == 0, nullptr, nullptr, qg);
-      else if (nm)
-        launch_nm<false, 0>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w,
-                            k == 0, nullptr, nullptr, qg);
-      else if (tiled && transpose)
+      if (tiled && transpose)
         launch_tiled<true, 0>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
       else if (tiled)
         launch_tiled<false, 0>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
@@ -2191,22 +2317,7 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
                w.partials, w.counters);
       halo(pl, s, {{bv.v[par ^ 1], ncomp}});
       PF_CUDA(cudaEventRecord(ev[1], s));
-      if (nm && qg) {
-        if (transpose)
-          launch_nm<true, 1>(tge, egrid, s, a, bv, par, (int64_t)n, st, w, 0,
-                             nullptr, nullptr, nullptr, qg);
-        else
-          launch_nm<false, 1>(tge, egrid, s, a, bv, par, (int64_t)n, st, w, 0,
-                              nullptr, nullptr, nullptr, qg);
-        halo(pl, s, {{qg, ncomp}});
-      }
-      if (nm && transpose)
-        launch_nm<true, 1>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w, 0,
-                           nullptr, nullptr, qg);
-      else if (nm)
-        launch_nm<false, 1>(tgn, ngrid, s, a, bv, par, (int64_t)n, st, w, 0,
-                            nullptr, nullptr, qg);
-      else if (tiled && transpose)
+      if (tiled && transpose)
         launch_tiled<true, 1>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
       else if (tiled)
         launch_tiled<false, 1>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w);
@@ -2217,11 +2328,7 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
         launch(k_bi_st<V, false>, gr, kBlock, s, v, a, bv, par, st,
                w.partials, w.counters);
       PF_CUDA(cudaEventRecord(ev[2], s));
-      if (nm)
-        launch(k_bi_xr<true>, gr, kBlock, s, a, bv, par, z, n, rg, st,
-               w.partials, w.counters, (int)(k == 0));
-      else
-        launch(k_bi_xr<false>, gr, kBlock, s, a, bv, par, x, n, rg, st,
+      launch(k_bi_xr<false>, gr, kBlock, s, a, bv, par, x, n, rg, st,
                w.partials, w.counters, 0);
       PF_CUDA(cudaEventRecord(ev[3], s));
       PF_CUDA(cudaEventSynchronize(ev[3]));
