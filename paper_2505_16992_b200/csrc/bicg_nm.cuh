@@ -345,6 +345,18 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
               if (on(c)) rh[c] = __ldg(g.rhat[c] + i3);
           }
         }
+        // x/r + pv: the own cell's z of plane q, loaded ahead of the
+        // barriers (its latency would otherwise sit inside phase A)
+        double zq[3] = {0, 0, 0};
+        int32_t iq = 0;
+        if constexpr (kRpv) {
+          if (!edge && q >= xs && q < xe) {
+            iq = nm_pbase(g, q) + own.off;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              if (on(c) || pend[c]) zq[c] = g.zio[c][iq];
+          }
+        }
         if (ghost1) {
           // the neighbour rank's stage 1 of this plane (own column: only
           // stage 2's X neighbour reads it) into plane x1's q1 slot
@@ -382,7 +394,7 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
           if constexpr (kRpv) if (!edge && q >= xs && q < xe) {
             // iteration k's x/r update at the own cell of an owned plane
             const double *rw = sm + kNmRaw + eo;
-            const int32_t io = nm_pbase(g, q) + own.off;
+            const int32_t io = iq;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
               if (!on(c) && !pend[c]) continue;
@@ -392,10 +404,10 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
                 const double sv = rw[c * kNP] - al * rw[(3 + c) * kNP];
                 const double rn = sv - om * rw[(9 + c) * kNP];
                 g.rout[c][io] = rn;
-                g.zio[c][io] += al * pp + om * sv;
+                g.zio[c][io] = zq[c] + (al * pp + om * sv);
                 acc[3 + c] += rn * rn;
               } else {
-                g.zio[c][io] += al * pp;
+                g.zio[c][io] = zq[c] + al * pp;
               }
             }
           }
