@@ -291,13 +291,19 @@ PF_API int pf_bicgstab_profile(const pf_plan *plan, const double *a,
 PF_API int pf_bwd_correct_velocity(const pf_plan *plan, const double *p,
                             const double *c, const double *cu, double *da,
                             double *cot_p, const double *extra_cot_p,
-                            void *workspace, void *stream);
+                            int32_t overwrite, void *workspace, void *stream);
 
 /* dKf[f][i] += y_i (p_nb - p_i): face cotangents of the pressure stencil from
  * one adjoint pressure solve -- outer_on_pattern(y, p) S/adjoint.py:113
- * folded with the diagonal as backward_pressure_matrix consumes it. */
+ * folded with the diagonal as backward_pressure_matrix consumes it.
+ *
+ * overwrite != 0 (here and in pf_bwd_correct_velocity, pf_bwd_h_stage,
+ * pf_adj_momentum_rhs): the first writer of an accumulator stores instead
+ * of adding (boundary faces get 0), so the caller need not zero-fill it;
+ * owned cells only. */
 PF_API int pf_bwd_pressure_outer(const pf_plan *plan, const double *y,
-                          const double *p, double *dkf, void *stream);
+                          const double *p, double *dkf, int32_t overwrite,
+                          void *stream);
 
 /* dA += backward_pressure_matrix(a_inv, dP), S/adjoint.py:116-134 */
 PF_API int pf_bwd_pressure_matrix(const pf_plan *plan, const double *c,
@@ -314,8 +320,8 @@ PF_API int pf_adj_divergence_rhs(const pf_plan *plan, const double *cot_b,
  * dC_off += outer(-A^-1 g_h, u_hin); cu = (C^t - A)(-A^-1 g_h). */
 PF_API int pf_bwd_h_stage(const pf_plan *plan, const double *c, const double *g_h,
                    const double *h, const double *u_hin, double *da,
-                   double *g_rhs, double *dc, double *cu_out, void *workspace,
-                   void *stream);
+                   double *g_rhs, double *dc, double *cu_out,
+                   int32_t overwrite, void *workspace, void *stream);
 
 /* dC += outer(-y, u_star) on the pattern (diagonal included) -- the matrix
  * cotangent of the momentum solve, S/adjoint.py:380 */
@@ -327,8 +333,8 @@ PF_API int pf_bwd_momentum_outer(const pf_plan *plan, const double *y,
  * double accumulated in stream order. */
 PF_API int pf_adj_momentum_rhs(const pf_plan *plan, const double *cot_rhs,
                         const double *bc, double nu, double dt, double *du_n,
-                        double *dbc, double *dnu_dev, void *workspace,
-                        void *stream);
+                        double *dbc, double *dnu_dev, int32_t overwrite,
+                        void *workspace, void *stream);
 
 /* _adj_assemble_momentum, S/adjoint.py:307-340: du_n += J T^t g_flux(dC),
  * *dnu_dev += viscous part. */

@@ -101,15 +101,15 @@ _SIGS = {
     "pf_bicgstab_profile": [c_ptr, c_ptr, c_int, c_int, c_ptr, c_int, c_ptr,
                             ctypes.POINTER(c_dbl), c_ptr],
     "pf_bwd_correct_velocity": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
-                                c_ptr, c_ptr, c_ptr],
-    "pf_bwd_pressure_outer": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
+                                c_ptr, c_int, c_ptr, c_ptr],
+    "pf_bwd_pressure_outer": [c_ptr, c_ptr, c_ptr, c_ptr, c_int, c_ptr],
     "pf_bwd_pressure_matrix": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
     "pf_adj_divergence_rhs": [c_ptr, c_ptr, c_dbl, c_ptr, c_ptr, c_ptr],
     "pf_bwd_h_stage": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
-                       c_ptr, c_ptr, c_ptr, c_ptr],
+                       c_ptr, c_ptr, c_int, c_ptr, c_ptr],
     "pf_bwd_momentum_outer": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
     "pf_adj_momentum_rhs": [c_ptr, c_ptr, c_ptr, c_dbl, c_dbl, c_ptr, c_ptr,
-                            c_ptr, c_ptr, c_ptr],
+                            c_ptr, c_int, c_ptr, c_ptr],
     "pf_adj_assemble_momentum": [c_ptr, c_ptr, c_dbl, c_ptr, c_ptr, c_ptr,
                                  c_ptr],
     "pf_momentum_cross_rhs": [c_ptr, c_ptr, c_dbl, c_ptr, c_ptr, c_ptr],

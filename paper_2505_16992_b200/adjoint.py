@@ -97,10 +97,15 @@ def backward_step(domain, tape, cot, path=GradientPath.FULL, tol=None,
     n_corr = len(tape.correctors)
     reports = []
 
-    dC = torch.zeros((2 * d + 1, n), dtype=F64, device=dev)
+    # first writers store (overwrite flag) instead of the kernels adding to
+    # zero-filled accumulators; slab plans keep the fill (ghost planes are
+    # not written by the owned-range kernels)
+    ow = 0 if plan.slab else 1
+    alloc = torch.zeros if plan.slab else torch.empty
+    dC = alloc((2 * d + 1, n), dtype=F64, device=dev)
     dA = dC[0]                       # dC[diag] += dA (S/adjoint.py:492)
-    dKf = torch.zeros((2 * d, n), dtype=F64, device=dev)
-    g_rhs = torch.zeros((d, n), dtype=F64, device=dev)
+    dKf = alloc((2 * d, n), dtype=F64, device=dev)
+    g_rhs = alloc((d, n), dtype=F64, device=dev)
     dbc = torch.zeros((d, plan.m), dtype=F64, device=dev) if plan.m else None
     dnu = torch.zeros(1, dtype=F64, device=dev)
 
@@ -113,9 +118,10 @@ def backward_step(domain, tape, cot, path=GradientPath.FULL, tol=None,
     for m in reversed(range(n_corr)):
         corr = tape.correctors[m]
         p_m = corr.p_iters[-1]
+        first = ow if m == n_corr - 1 else 0
         _lib.call("pf_bwd_correct_velocity", plan.handle, _lib.ptr(p_m),
                   _lib.ptr(C), _lib.ptr(cu), _lib.ptr(dA), _lib.ptr(cot_p),
-                  _lib.ptr(cp_out if m == n_corr - 1 else None),
+                  _lib.ptr(cp_out if m == n_corr - 1 else None), first,
                   _lib.ptr(plan.workspace), hs)
         g_h = cu                     # dh = cu; the divergence adjoint adds
         n_it = len(corr.p_iters)
@@ -128,7 +134,8 @@ def backward_step(domain, tape, cot, path=GradientPath.FULL, tol=None,
                               zero_mean=True, stage="adjoint_pressure")
             reports.append(rep)
             _lib.call("pf_bwd_pressure_outer", plan.handle, _lib.ptr(y),
-                      _lib.ptr(corr.p_iters[it]), _lib.ptr(dKf), hs)
+                      _lib.ptr(corr.p_iters[it]), _lib.ptr(dKf),
+                      0 if pressure_done else ow, hs)
             pressure_done = True
             # forward solved (-P) p = proj(-b): db = -y
             _lib.call("pf_adj_divergence_rhs", plan.handle, _lib.ptr(y),
@@ -144,7 +151,9 @@ def backward_step(domain, tape, cot, path=GradientPath.FULL, tol=None,
                 if rep.iterations or rep.residual:
                     reports.append(rep)
                 _lib.call("pf_bwd_pressure_outer", plan.handle, _lib.ptr(y),
-                          _lib.ptr(corr.p_iters[it]), _lib.ptr(dKf), hs)
+                          _lib.ptr(corr.p_iters[it]), _lib.ptr(dKf),
+                          0 if pressure_done else ow, hs)
+                pressure_done = True
                 _lib.call("pf_axpy", plan.handle, -1.0, _lib.ptr(y),
                           _lib.ptr(cot_b0), n, hs)
                 if it > 0:
@@ -161,7 +170,7 @@ def backward_step(domain, tape, cot, path=GradientPath.FULL, tol=None,
         _lib.call("pf_bwd_h_stage", plan.handle, _lib.ptr(C), _lib.ptr(g_h),
                   _lib.ptr(soa(corr.h, n, d, dev)),
                   _lib.ptr(soa(corr.u_hin, n, d, dev)), _lib.ptr(dA),
-                  _lib.ptr(g_rhs), _lib.ptr(dC), _lib.ptr(cu_next),
+                  _lib.ptr(g_rhs), _lib.ptr(dC), _lib.ptr(cu_next), first,
                   _lib.ptr(plan.workspace), hs)
         cu, cu_next = cu_next, cu
 
@@ -170,7 +179,8 @@ def backward_step(domain, tape, cot, path=GradientPath.FULL, tol=None,
                   _lib.ptr(dKf), _lib.ptr(dA), hs)
 
     # predictor (S/adjoint.py:343-405)
-    du_n = torch.zeros((d, n), dtype=F64, device=dev)
+    du_n = alloc((d, n), dtype=F64, device=dev)
+    du_first = ow
     bcd = getattr(tape, "_bc_dm", None)
     if bcd is None and plan.m:
         from .piso import bc_soa
@@ -183,7 +193,7 @@ def backward_step(domain, tape, cot, path=GradientPath.FULL, tol=None,
     dsource = None
     cot_us = cu
     for it in its:
-        grhs = torch.zeros((d, n), dtype=F64, device=dev)
+        grhs = None
         if path.advection_solve:
             y, reps = bicgstab_solve(plan, C, cot_us, tol=tol,
                                      maxiter=maxiter, transpose=True,
@@ -193,12 +203,15 @@ def backward_step(domain, tape, cot, path=GradientPath.FULL, tol=None,
             _lib.call("pf_bwd_momentum_outer", plan.handle, _lib.ptr(y),
                       _lib.ptr(u_star), _lib.ptr(dC), hs)
             grhs = y
+        if grhs is None:
+            grhs = torch.zeros((d, n), dtype=F64, device=dev)
         if it == n_outer - 1:
             grhs.add_(g_rhs)
         _lib.call("pf_adj_momentum_rhs", plan.handle, _lib.ptr(grhs),
                   _lib.ptr(bcd), float(tape.nu), float(tape.dt),
-                  _lib.ptr(du_n), _lib.ptr(dbc), _lib.ptr(dnu),
+                  _lib.ptr(du_n), _lib.ptr(dbc), _lib.ptr(dnu), du_first,
                   _lib.ptr(plan.workspace), hs)
+        du_first = 0
         dsource = grhs if dsource is None else dsource.add_(grhs)
         if plan.cell_cross:
             u_in = soa(tape.mom_inputs[it], n, d, dev)
@@ -243,7 +256,7 @@ def backward_correct_velocity(domain, p, a_diag, cot_u):
     _lib.call("pf_bwd_correct_velocity", plan.handle,
               _lib.ptr(scalar_field(p, n, plan.device)),
               _lib.ptr(_cdiag(a_diag, n, plan.device)), _lib.ptr(cu),
-              _lib.ptr(da), _lib.ptr(dp), _lib.ptr(None),
+              _lib.ptr(da), _lib.ptr(dp), _lib.ptr(None), 0,
               _lib.ptr(plan.workspace), plan.stream)
     return da, dp, cu.clone().t()
 
@@ -321,7 +334,7 @@ def backward_pressure_solve(domain, p_data, p_sol, cot_p, tol=None,
         reports.append(rep)
     _lib.call("pf_bwd_pressure_outer", plan.handle, _lib.ptr(y),
               _lib.ptr(scalar_field(p_sol, n, plan.device)), _lib.ptr(dkf),
-              plan.stream)
+              0, plan.stream)
     return dkf, -y
 
 

@@ -22,7 +22,7 @@ template <class V>
 __global__ void __launch_bounds__(kBlock)
     k_bwd_cv_cell(V v, const double *__restrict__ p,
                   const double *__restrict__ c, const double *__restrict__ cu,
-                  double *__restrict__ da, double *__restrict__ cot_gp) {
+                  double *__restrict__ da, double *__restrict__ cot_gp, int ow) {
   constexpr int D = V::kDim;
   const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= v.i1) return;
@@ -50,7 +50,10 @@ __global__ void __launch_bounds__(kBlock)
     dot += cuk * e;
     cue[k] = -ainv * cuk;
   }
-  da[i] += dot * (ainv * ainv);
+  if (ow)
+    da[i] = dot * (ainv * ainv);
+  else
+    da[i] += dot * (ainv * ainv);
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     double s = 0.0;
@@ -96,7 +99,8 @@ __global__ void __launch_bounds__(kBlock)
 template <class V>
 __global__ void __launch_bounds__(kBlock)
     k_bwd_p_outer(V v, const double *__restrict__ y,
-                  const double *__restrict__ p, double *__restrict__ dkf) {
+                  const double *__restrict__ p, double *__restrict__ dkf,
+                  int ow) {
   constexpr int D = V::kDim;
   const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= v.i1) return;
@@ -106,7 +110,10 @@ __global__ void __launch_bounds__(kBlock)
 #pragma unroll
   for (int f = 0; f < 2 * D; ++f) {
     const Face fc = v.topo.face(cell, f);
-    if (fc.nb >= 0) dkf[(int64_t)f * n + i] += yi * p[fc.nb] - yi * pi;
+    if (ow)
+      dkf[(int64_t)f * n + i] = fc.nb >= 0 ? yi * p[fc.nb] - yi * pi : 0.0;
+    else if (fc.nb >= 0)
+      dkf[(int64_t)f * n + i] += yi * p[fc.nb] - yi * pi;
   }
 }
 
@@ -190,7 +197,7 @@ __global__ void __launch_bounds__(kBlock)
                  const double *__restrict__ g_h, const double *__restrict__ h,
                  const double *__restrict__ u_hin, double *__restrict__ da,
                  double *__restrict__ g_rhs, double *__restrict__ dc,
-                 double *__restrict__ cot_hu) {
+                 double *__restrict__ cot_hu, int ow) {
   constexpr int D = V::kDim;
   const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= v.i1) return;
@@ -204,7 +211,10 @@ __global__ void __launch_bounds__(kBlock)
     const double gq = g_h[q * n + i];
     dot += gq * h[q * n + i];
     const double gr = ainv * gq;
-    g_rhs[q * n + i] += gr;
+    if (ow)
+      g_rhs[q * n + i] = gr;
+    else
+      g_rhs[q * n + i] += gr;
     chu[q] = -gr;
     cot_hu[q * n + i] = -gr;
   }
@@ -212,11 +222,17 @@ __global__ void __launch_bounds__(kBlock)
 #pragma unroll
   for (int f = 0; f < 2 * D; ++f) {
     const Face fc = v.topo.face(cell, f);
-    if (fc.nb < 0) continue;
+    if (fc.nb < 0) {
+      if (ow) dc[(int64_t)(1 + f) * n + i] = 0.0;
+      continue;
+    }
     double s = 0.0;
 #pragma unroll
     for (int q = 0; q < D; ++q) s += chu[q] * u_hin[q * n + fc.nb];
-    dc[(int64_t)(1 + f) * n + i] += s;
+    if (ow)
+      dc[(int64_t)(1 + f) * n + i] = s;
+    else
+      dc[(int64_t)(1 + f) * n + i] += s;
   }
 }
 
@@ -281,13 +297,18 @@ __global__ void __launch_bounds__(kBlock)
 template <class V>
 __global__ void __launch_bounds__(kBlock)
     k_adj_rhs_cells(V v, const double *__restrict__ cot, double dt,
-                    double *__restrict__ du_n) {
+                    double *__restrict__ du_n, int ow) {
   constexpr int D = V::kDim;
   const int32_t i = v.i0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= v.i1) return;
   const int64_t n = v.n;
 #pragma unroll
-  for (int q = 0; q < D; ++q) du_n[q * n + i] += cot[q * n + i] / dt;
+  for (int q = 0; q < D; ++q) {
+    if (ow)
+      du_n[q * n + i] = cot[q * n + i] / dt;
+    else
+      du_n[q * n + i] += cot[q * n + i] / dt;
+  }
 }
 
 template <class V>
@@ -450,7 +471,8 @@ extern "C" int pf_bwd_correct_velocity(const pf_plan *plan, const double *p,
                                        const double *c, const double *cu,
                                        double *da, double *cot_p,
                                        const double *extra_cot_p,
-                                       void *workspace, void *stream) {
+                                       int32_t overwrite, void *workspace,
+                                       void *stream) {
   PF_REQUIRE(plan && p && c && cu && da && cot_p && workspace,
              "pf_bwd_correct_velocity: null argument");
   const Plan &pl = P(plan);
@@ -460,7 +482,7 @@ extern "C" int pf_bwd_correct_velocity(const pf_plan *plan, const double *p,
     const int D = decltype(v)::kDim;
     halo(pl, S(stream), {{const_cast<double *>(p), 1}});
     launch(k_bwd_cv_cell<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, p, c, cu, da,
-                                                           cot_gp);
+                                                           cot_gp, (int)overwrite);
     halo(pl, S(stream), {{cot_gp, D}});
     launch(k_bwd_cv_gather<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, cot_gp,
                                                              extra_cot_p, cot_p);
@@ -471,11 +493,12 @@ extern "C" int pf_bwd_correct_velocity(const pf_plan *plan, const double *p,
 
 extern "C" int pf_bwd_pressure_outer(const pf_plan *plan, const double *y,
                                      const double *p, double *dkf,
-                                     void *stream) {
+                                     int32_t overwrite, void *stream) {
   PF_REQUIRE(plan && y && p && dkf, "pf_bwd_pressure_outer: null argument");
   return dispatch(P(plan), [&](auto v) {
     halo(P(plan), S(stream), {{const_cast<double *>(p), 1}});
-    launch(k_bwd_p_outer<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, y, p, dkf);
+    launch(k_bwd_p_outer<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, y, p, dkf,
+           (int)overwrite);
     PF_LAUNCH_CHECK("bwd_pressure_outer");
     return PF_OK;
   });
@@ -511,8 +534,8 @@ extern "C" int pf_adj_divergence_rhs(const pf_plan *plan, const double *cot_b,
 extern "C" int pf_bwd_h_stage(const pf_plan *plan, const double *c,
                               const double *g_h, const double *h,
                               const double *u_hin, double *da, double *g_rhs,
-                              double *dc, double *cu_out, void *workspace,
-                              void *stream) {
+                              double *dc, double *cu_out, int32_t overwrite,
+                              void *workspace, void *stream) {
   PF_REQUIRE(plan && c && g_h && h && u_hin && da && g_rhs && dc && cu_out &&
                  workspace,
              "pf_bwd_h_stage: null argument");
@@ -523,7 +546,7 @@ extern "C" int pf_bwd_h_stage(const pf_plan *plan, const double *c,
     const int D = decltype(v)::kDim;
     halo(pl, S(stream), {{const_cast<double *>(u_hin), D}});
     launch(k_bwd_h_cell<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, c, g_h, h, u_hin,
-                                                          da, g_rhs, dc, cot_hu);
+                                                          da, g_rhs, dc, cot_hu, (int)overwrite);
     halo(pl, S(stream), {{cot_hu, D}});
     launch(k_bwd_h_gather<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, c, cot_hu,
                                                             cu_out);
@@ -548,7 +571,8 @@ extern "C" int pf_bwd_momentum_outer(const pf_plan *plan, const double *y,
 extern "C" int pf_adj_momentum_rhs(const pf_plan *plan, const double *cot_rhs,
                                    const double *bc, double nu, double dt,
                                    double *du_n, double *dbc, double *dnu_dev,
-                                   void *workspace, void *stream) {
+                                   int32_t overwrite, void *workspace,
+                                   void *stream) {
   PF_REQUIRE(plan && cot_rhs && du_n && dnu_dev && workspace,
              "pf_adj_momentum_rhs: null argument");
   const Plan &pl = P(plan);
@@ -556,7 +580,7 @@ extern "C" int pf_adj_momentum_rhs(const pf_plan *plan, const double *cot_rhs,
   Workspace w = carve(workspace, pl.d.n, pl.d.dim);
   return dispatch(pl, [&](auto v) {
     launch(k_adj_rhs_cells<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), v, cot_rhs, dt,
-                                                             du_n);
+                                                             du_n, (int)overwrite);
     if (v.m > 0) {
       const int g = std::min(grid_for(v.m), pl.red_blocks);
       launch(k_adj_rhs_faces<decltype(v)>, g, kBlock, S(stream), 

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <set>
+#include <string>
 #include <type_traits>
 
 #include "cgstate.cuh"
@@ -2199,9 +2200,12 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
     TileGeo tg, tgn;
     const bool tiled = tile_geo(pl, v, tg);
     const int tgrid = tiled ? std::min(tg.ntiles, pl.red_blocks) : 0;
-    // the production preconditioner: Neumann-2 where it runs, else Jacobi
+    // the production preconditioner: Jacobi, or Neumann-2 where it runs
+    // when PF_MOMENTUM_PRECOND=neumann2 (the Python default follows it)
     TileGeo tge;
-    const bool nm = nm_geo(pl, v, tgn, &tge);
+    const char *mp = getenv("PF_MOMENTUM_PRECOND");
+    const bool nm = mp && std::string(mp) == "neumann2" &&
+                    nm_geo(pl, v, tgn, &tge);
     const int ngrid = nm ? std::min(tgn.ntiles, nm_minb() * pl.num_sms) : 0;
     const int egrid = nm ? std::min(tge.ntiles, nm_minb() * pl.num_sms) : 0;
     double *qg = pl.slab ? w.vecs + 10 * len : nullptr;

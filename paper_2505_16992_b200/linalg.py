@@ -11,6 +11,7 @@ runs unpreconditioned).  All iteration happens inside ``libpisob200.so``.
 """
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -62,6 +63,7 @@ def _global_n(plan):
 
 
 PRECOND_NONE, PRECOND_JACOBI, PRECOND_MG, PRECOND_NEUMANN2 = 0, 1, 2, 3
+_DEFAULT_MOM_PRECOND = os.environ.get("PF_MOMENTUM_PRECOND", "jacobi")
 
 
 def _precond_flag(precond):
@@ -142,10 +144,15 @@ def bicgstab_solve(plan, data, b, x0=None, tol=None, maxiter=None,
         x.copy_(x0.reshape(k, n))
     reps = (_lib.SolverReportC * k)()
     pc = _precond_flag(precond)
-    # auto / "ilu0": the fused two-sweep Jacobi polynomial where the plan
-    # runs it (the library degrades it to Jacobi elsewhere)
-    pc = PRECOND_NEUMANN2 if pc == -1 else \
-        PRECOND_JACOBI if pc == PRECOND_MG else pc
+    # auto / "ilu0": Jacobi, unless PF_MOMENTUM_PRECOND=neumann2.  The fused
+    # two-sweep polynomial halves the iterations (C4: 15 -> 8 per step) but
+    # its passes are latency-bound: same-box A/B, C4 step 34.8 ms vs 34.0
+    # ms with Jacobi (profiles/r2_ab_c4.txt); it stays selectable
+    if pc == -1:
+        pc = PRECOND_NEUMANN2 if _DEFAULT_MOM_PRECOND == "neumann2" \
+            else PRECOND_JACOBI
+    elif pc == PRECOND_MG:
+        pc = PRECOND_JACOBI
     with _lib.nvtx(stages[0] if stages else stage):
         _lib.call("pf_bicgstab_solve", plan.handle, _lib.ptr(data),
                   int(bool(transpose)), k, _lib.ptr(b2), _lib.ptr(x),
