@@ -473,11 +473,7 @@ def kernel_bytes(nm, d):
           # pass reads r, v, p, t, r^, z and writes r', z, p', v'; st reads
           # r, v', r^ and writes t
           "k_bi_nm_rpv": 16 * d + 8 + d * 80,
-          "k_bi_nm_st": 16 * d + 8 + d * 32,
-          # merged Jacobi passes: 2d+1 rows + 1/A; the merged pass reads r,
-          # v, p, t, r^ and x, writes r', p', v', x; st reads r, v', r^,
-          # writes t
-          "k_bi_rpv": 8 * rows + 8 + d * 80, "k_bi_stm": 8 * rows + 8 + d * 32}
+          "k_bi_nm_st": 16 * d + 8 + d * 32}
     if nm in bi:
         return bi[nm]
     co = 8.0 / 2 ** d
@@ -544,9 +540,8 @@ def measure_roofline(args, dom, plan, state, nu, dt, dev, per_step):
         bm = (ctypes.c_double * 5)()
         _lib.call("pf_bicgstab_profile", plan.handle, _lib.ptr(c), trans, d,
                   _lib.ptr(bb), 8, _lib.ptr(plan.workspace), bm, plan.stream)
-        # merged passes: the x/r update rides in the next pv pass
+        # Neumann-2: the x/r update rides in the next pv pass (k_bi_nm_rpv)
         names = (("k_bi_nm_rpv", "k_bi_nm_st", None) if bm[4] == 3
-                 else ("k_bi_rpv", "k_bi_stm", None) if bm[4] == 5
                  else ("k_bi_pv", "k_bi_st", "k_bi_xr"))
         for j, nm in enumerate(names):
             if nm is not None:
@@ -599,11 +594,10 @@ def measure_roofline(args, dom, plan, state, nu, dt, dev, per_step):
                 "preconditioner": plan.geom_kind if mg else "jacobi",
                 "ms": it_ms, "ms_graph_replay": float(ms[10])},
             "whole_step": whole_step_bytes(d, per_step, n, peak,
-                                           nm_bi="k_bi_nm_rpv" in "".join(bi),
-                                           merged="k_bi_rpv" in "".join(bi))}
+                                           nm_bi="k_bi_nm_rpv" in "".join(bi))}
 
 
-def whole_step_bytes(d, per_step, n, peak, nm_bi, merged=False):
+def whole_step_bytes(d, per_step, n, peak, nm_bi):
     """SURVEY.md §8(d)'s whole-step figure: sum over the step's kernels of
     algorithmic bytes/cell x invocations (from the step's own iteration
     counts), times the cells, over the measured step time.  Per-op bytes
@@ -625,8 +619,6 @@ def whole_step_bytes(d, per_step, n, peak, nm_bi, merged=False):
     s, q = 8, 2 * d + 1
     bi_it = kernel_bytes("k_bi_nm_rpv", d) + kernel_bytes("k_bi_nm_st", d) \
         if nm_bi else \
-        kernel_bytes("k_bi_rpv", d) + kernel_bytes("k_bi_stm", d) \
-        if merged else \
         kernel_bytes("k_bi_pv", d) + kernel_bytes("k_bi_st", d) \
         + kernel_bytes("k_bi_xr", d)
     bi_solve = s * (q + 5 * d + 1) + s * (q + 2 * d) \

@@ -830,8 +830,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // Shared memory of the tiled passes: the raw inputs of two planes (tile +
 // halo, filled by cp.async one plane ahead) and the preconditioned values
 // g of two planes (double buffered, so a plane step needs one barrier).
-// r x3, v x3, p x3, t x3 (the merged pass), 1/A (slot kDi)
-constexpr int kRawArrays = 13, kDi = 12;
+constexpr int kRawArrays = 10;  // r x3, p x3, v x3, 1/A (pass st: r, v, 1/A)
 constexpr int kTP = (kTY + 2) * (kTZ + 2);
 struct TileSmem {
   double raw[2][kRawArrays][kTY + 2][kTZ + 2];
@@ -854,65 +853,45 @@ constexpr size_t kTileSmem = sizeof(TileSmem);
 //                   Neumann-2 preconditioned iterate, bicg_nm.cuh); a
 //                   one-stage stencil, so the efficient single-halo pass
 //                   forms it (no reduction)
-// MODE 5 (merged x/r + pv): iteration k's update folded into iteration
-//                   k+1's pv: s = r - alpha v, r' = s - omega t, p' = r' +
-//                   beta (p - omega v) at every stencil point; at the own
-//                   cell r' and x += alpha p / A + omega s / A; outputs p',
-//                   v' = A M^-1 p'; sums r^.v', |r'|^2 (304 B/cell, and no
-//                   separate x/r pass: 456 B per iteration instead of 528)
-// MODE 6 (merged st): MODE 1 on the r buffer of this iteration, plus r^.s
-//                   and r^.t -> rho_next = r^.r' and beta for MODE 5
 template <bool kTrans, int MODE, int kMinB = 1, bool kFirst = false>
 __global__ void __launch_bounds__(kTileThreads, kMinB)
     k_bi_tiled(TileGeo tg, const double *__restrict__ a, BiVecs w, int par,
                int64_t n, SolverState *st, double *partials,
                unsigned *counter, const double *__restrict__ xin = nullptr,
                const double *__restrict__ bin = nullptr, int nverify = 0,
-               double *__restrict__ xout = nullptr,
-               const double *__restrict__ rin = nullptr,
-               double *__restrict__ rout = nullptr) {
+               double *__restrict__ xout = nullptr) {
   if (MODE != 3 && MODE != 4 && st->all_done) return;
   // compile-time: a runtime branch here slows the transposed pass ~15 %
   constexpr bool fresh = MODE == 0 && kFirst;
-  constexpr bool kM = MODE == 5;              // merged x/r + pv
-  constexpr bool kS = MODE == 1 || MODE == 6;  // st passes
-  constexpr bool kPV = MODE == 0 || kM;        // pv passes
-  constexpr int K = MODE == 1 ? 9 : MODE == 6 ? 15 : (MODE == 2 || kM) ? 6 : 3;
-  constexpr bool kX = MODE >= 2 && MODE <= 4;  // the input is x (or z)
+  constexpr int K = MODE == 1 ? 9 : MODE == 2 ? 6 : 3;
+  constexpr bool kX = MODE >= 2;  // the input is the iterate x (or z) itself
   constexpr bool kZ = MODE == 4;  // ... divided by A (the close pass)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem &sm = *reinterpret_cast<TileSmem *>(smem_raw);
   const int nc = MODE == 3 ? nverify : st->ncomp;
   const int pc_on = st->precond;
-  int act[3], pend[3];
-  double c0[3], c1[3], c2[3];
+  int act[3];
+  double c0[3], c1[3];
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
     act[q] = q < nc && (MODE == 3 || !st->c[q].done);
     if (MODE == 4)  // the components that iterated and did not break down
       act[q] = q < nc && st->c[q].active && !st->c[q].zero_rhs &&
                st->c[q].iter > 0 && !st->c[q].fail;
-    // merged pass: components that converged at s take x += alpha p / A
-    pend[q] = kM && q < nc && st->c[q].pending;
-    c2[q] = 0.0;
     if (MODE == 0) {
       c0[q] = q < nc ? st->c[q].beta : 0.0;
       c1[q] = q < nc ? st->c[q].omega : 0.0;
-    } else if (kM) {
-      c0[q] = q < nc ? st->c[q].alpha : 0.0;
-      c1[q] = q < nc ? st->c[q].omega : 0.0;
-      c2[q] = q < nc ? st->c[q].beta : 0.0;
     } else {
       c0[q] = q < nc ? st->c[q].alpha : 0.0;
       c1[q] = 0.0;
     }
   }
-  const double *__restrict__ r = rin ? rin : w.r;
+  const double *__restrict__ r = w.r;
   const double *__restrict__ dinv = w.dinv;
-  const double *__restrict__ pin = kPV ? w.p[par] : nullptr;
-  const double *__restrict__ vin = kPV ? w.v[par] : w.v[par ^ 1];
+  const double *__restrict__ pin = MODE == 0 ? w.p[par] : nullptr;
+  const double *__restrict__ vin = MODE == 0 ? w.v[par] : w.v[par ^ 1];
   double *__restrict__ pout = w.p[par ^ 1];
-  double *__restrict__ vout = kPV ? w.v[par ^ 1] : w.t;
+  double *__restrict__ vout = MODE == 0 ? w.v[par ^ 1] : w.t;
   const int64_t sX = (int64_t)tg.Y * tg.Z, sY = tg.Z;
   const int tz = threadIdx.x % kTZ, ty = threadIdx.x / kTZ;
 
@@ -927,7 +906,7 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
     const int64_t j = (int64_t)x * sX + (int64_t)y * sY + z;
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      if (q >= nc || !(act[q] || pend[q])) continue;
+      if (q >= nc || !act[q]) continue;
       const int64_t o = q * n + j;
       if (kX) {
         if (ok)
@@ -940,26 +919,24 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
         cp_async8(&sm.raw[b][q][sy][sz], r + o);
         if (!fresh) {
           cp_async8(&sm.raw[b][3 + q][sy][sz], vin + o);
-          if (kPV) cp_async8(&sm.raw[b][6 + q][sy][sz], pin + o);
-          if (kM) cp_async8(&sm.raw[b][9 + q][sy][sz], w.t + o);
+          if (MODE == 0) cp_async8(&sm.raw[b][6 + q][sy][sz], pin + o);
         }
       } else {
         sm.raw[b][q][sy][sz] = 0.0;
         sm.raw[b][3 + q][sy][sz] = 0.0;
-        if (kPV) sm.raw[b][6 + q][sy][sz] = 0.0;
-        if (kM) sm.raw[b][9 + q][sy][sz] = 0.0;
+        if (MODE == 0) sm.raw[b][6 + q][sy][sz] = 0.0;
       }
     }
     if (kX && !kZ) return;
     if (ok)
-      cp_async8(&sm.raw[b][kDi][sy][sz], dinv + j);
+      cp_async8(&sm.raw[b][9][sy][sz], dinv + j);
     else
-      sm.raw[b][kDi][sy][sz] = 0.0;
+      sm.raw[b][9][sy][sz] = 0.0;
   };
   // g (and the undivided value) of slot (sy, sz) of raw buffer b
   auto G = [&](int b, int sy, int sz, double (&g)[3], double (&pv)[3]) {
     if (kZ) {
-      const double dj = sm.raw[b][kDi][sy][sz];
+      const double dj = sm.raw[b][9][sy][sz];
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         pv[q] = (q < nc && act[q]) ? sm.raw[b][q][sy][sz] : 0.0;
@@ -974,7 +951,7 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
       }
       return;
     }
-    const double dj = sm.raw[b][kDi][sy][sz];
+    const double dj = sm.raw[b][9][sy][sz];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
       g[q] = pv[q] = 0.0;
@@ -983,10 +960,6 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
       double val;
       if (fresh) {
         val = rr;  // r + beta (0 - omega 0)
-      } else if (kM) {
-        const double vv = sm.raw[b][3 + q][sy][sz];
-        const double rn = (rr - c0[q] * vv) - c1[q] * sm.raw[b][9 + q][sy][sz];
-        val = rn + c2[q] * (sm.raw[b][6 + q][sy][sz] - c1[q] * vv);
       } else {
         const double vv = sm.raw[b][3 + q][sy][sz];
         val = MODE == 0
@@ -1049,50 +1022,14 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
       }
     };
 
-    // merged pass: iteration k's x/r update at the own cell of owned plane
-    // xq, from its raw buffer (xpre: x of that cell, loaded ahead)
-    auto pointwise = [&](int32_t xq, const double (&xpre)[3]) {
-      if (!kM || xq >= xe) return;
-      const int b = xq & 1;
-      const double dj = sm.raw[b][kDi][ty + 1][tz + 1];
-      const int64_t iq = (int64_t)xq * sX + (int64_t)y * sY + z;
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        if (q >= nc || !(act[q] || pend[q])) continue;
-        const double al = c0[q], pp = sm.raw[b][6 + q][ty + 1][tz + 1];
-        const int64_t o = q * n + iq;
-        if (act[q]) {
-          const double sv = sm.raw[b][q][ty + 1][tz + 1] -
-                            al * sm.raw[b][3 + q][ty + 1][tz + 1];
-          const double rn = sv - c1[q] * sm.raw[b][9 + q][ty + 1][tz + 1];
-          rout[o] = rn;
-          xout[o] = xpre[q] + al * (pp * dj) + c1[q] * (sv * dj);
-          acc[3 + q] += rn * rn;
-        } else {
-          xout[o] = xpre[q] + al * (pp * dj);
-        }
-      }
-    };
-    auto xload = [&](int32_t xq, double (&xp)[3]) {
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        xp[q] = 0.0;
-        if (kM && xq < xe && q < nc && (act[q] || pend[q]))
-          xp[q] = xout[q * n + (int64_t)xq * sX + (int64_t)y * sY + z];
-      }
-    };
-
     double gm[3], gc[3], gn[3], pc[3], pn[3], tmp[3];
     __syncthreads();  // the previous tile is done with both buffers
     issue_plane(xs - 1);
     issue_plane(xs);
-    double xpre[3];
-    xload(xs, xpre);
     cp_async_wait_all();
     __syncthreads();
     G((xs - 1) & 1, ty + 1, tz + 1, gm, tmp);
     convert(xs, gc, pc);
-    pointwise(xs, xpre);
     __syncthreads();  // raw buffer (xs - 1) & 1 is free again
     issue_plane(xs + 1);
     for (int32_t x = xs; x < xe; ++x) {
@@ -1123,14 +1060,12 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
       double rh[3];
 #pragma unroll
       for (int q = 0; q < 3; ++q)
-        rh[q] = ((kPV || MODE == 6) && q < nc && act[q]) ? w.rhat[q * n + i]
+        rh[q] = (MODE == 0 && q < nc && act[q]) ? w.rhat[q * n + i]
                 : (kX && !kZ && q < nc && act[q]) ? bin[q * n + i]
                                                   : 0.0;
-      xload(x + 1, xpre);
       cp_async_wait_all();  // my copies of plane x + 1 have landed
       __syncthreads();      // everyone's have; g of plane x is complete
       convert(x + 1, gn, pn);
-      pointwise(x + 1, xpre);
       if (x + 2 <= xe) issue_plane(x + 2);
       const int gb = x & 1;
       if (kZ) {
@@ -1155,22 +1090,15 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
                           cf[4] * sm.g[gb][q][ty + 1][tz] +
                           cf[5] * sm.g[gb][q][ty + 1][tz + 2];
         const int64_t o = q * n + i;
-        if constexpr (kPV) {
+        if (MODE == 0) {
           vout[o] = yv;
           pout[o] = pc[q];
           acc[q] += rh[q] * yv;
-        } else if constexpr (MODE == 1) {
+        } else if (MODE == 1) {
           vout[o] = yv;
           acc[3 * q] += pc[q] * pc[q];
           acc[3 * q + 1] += yv * yv;
           acc[3 * q + 2] += yv * pc[q];
-        } else if constexpr (MODE == 6) {
-          vout[o] = yv;
-          acc[5 * q] += pc[q] * pc[q];
-          acc[5 * q + 1] += yv * yv;
-          acc[5 * q + 2] += yv * pc[q];
-          acc[5 * q + 3] += rh[q] * pc[q];   // r^.s
-          acc[5 * q + 4] += rh[q] * yv;      // r^.t
         } else {
           const double rr = rh[q] - yv;  // b - A x
           if (MODE == 2) {
@@ -1194,63 +1122,6 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
   if (kZ) return;
   double tot[K];
   if (!grid_reduce<K>(acc, partials, counter, tot)) return;
-  if constexpr (kM) {
-    // iteration k completes: convergence on r', else iteration k + 1's
-    // alpha (its rho is the st pass's rho_next, which beta used)
-    int all = 1;
-    for (int q = 0; q < nc; ++q) {
-      CompState &c = st->c[q];
-      if (pend[q]) c.pending = 0;
-      if (act[q]) {
-        c.res = sqrt(tot[3 + q]);
-        if (c.res <= c.tol_abs) {
-          c.converged = 1;
-          c.done = 1;
-        } else if (c.iter >= c.maxiter) {
-          c.done = 1;
-        } else if (c.brk_next) {
-          c.fail = 1;
-          c.done = 1;
-        } else {
-          c.rho = c.rho_new;
-          c.iter += 1;
-          c.rho_new = c.rho_next;
-          if (fabs(tot[q]) < DBL_MIN) {
-            c.fail = 1;
-            c.done = 1;
-          } else {
-            c.alpha = c.rho_new / tot[q];
-          }
-        }
-      }
-      if (!c.done) all = 0;
-    }
-    st->all_done = all;
-    return;
-  }
-  if constexpr (MODE == 6) {
-    // all_done is left alone: the merged pass applies the early-exit update
-    for (int q = 0; q < nc; ++q) {
-      CompState &c = st->c[q];
-      if (!act[q]) continue;
-      c.res = sqrt(tot[5 * q]);
-      if (c.res <= c.tol_abs) {
-        c.converged = 1;
-        c.done = 1;
-        c.pending = 1;
-      } else if (tot[5 * q + 1] < DBL_MIN) {
-        c.fail = 1;
-        c.done = 1;
-      } else {
-        c.omega = tot[5 * q + 2] / tot[5 * q + 1];
-        c.rho_next = tot[5 * q + 3] - c.omega * tot[5 * q + 4];
-        c.brk_next = fabs(c.rho_next) < DBL_MIN || fabs(c.omega) < DBL_MIN;
-        c.beta = c.brk_next ? 0.0
-                            : (c.rho_next / c.rho_new) * (c.alpha / c.omega);
-      }
-    }
-    return;
-  }
   if (MODE == 3) {
     for (int q = 0; q < nc; ++q) st->c[q].true_res = sqrt(tot[q]);
     return;
@@ -1688,8 +1559,7 @@ void launch_tiled(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
                   const BiVecs &bv, int par, int64_t n, SolverState *st,
                   Workspace &w, const double *xin = nullptr,
                   const double *bin = nullptr, int nverify = 0,
-                  int first = 0, double *xout = nullptr,
-                  const double *rin = nullptr, double *rout = nullptr) {
+                  int first = 0, double *xout = nullptr) {
   // 2 CTAs per SM (<= 128 registers, 2 x 71 KB of shared memory) measured
   // best on C4: pass pv 5.3 TB/s, pass st 4.3 TB/s (1 CTA: 3.8 / 2.9; 3 CTAs
   // with the 80-register cap: 3.5 / 3.2).  PF_TILE_MINB overrides.
@@ -1712,8 +1582,7 @@ void launch_tiled(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
     count_launch();
     kernel<<<grid, kTileThreads, kTileSmem, s>>>(tg, a, bv, par, n, st,
                                                  w.partials, w.counters, xin,
-                                                 bin, nverify, xout, rin,
-                                                 rout);
+                                                 bin, nverify, xout);
   };
   if (MODE == 0 && first) {
     if (minb >= 3)
@@ -1954,43 +1823,6 @@ void nm_finish(const Plan &pl, const TileGeo &tgn, const TileGeo &tge,
                        nullptr, qg, nullptr, rp);
 }
 
-// One merged Jacobi BiCGStab iteration i (0-based) on the tiled passes:
-// the pv pass (i = 0) or the merged pass (iteration i-1's x/r update +
-// iteration i's pv; MODE 5), then the merged st pass (MODE 6).  r
-// ping-pongs: iteration i reads rb[i & 1].
-template <bool kTrans>
-void jm_iteration(const Plan &pl, const TileGeo &tg, int tgrid,
-                  cudaStream_t s, const double *a, const BiVecs &bv, int i,
-                  int64_t n, int ncomp, SolverState *st, Workspace &w,
-                  double *x) {
-  const int par = i & 1;
-  if (i == 0) {
-    halo(pl, s, {{bv.rb[0], ncomp}, {bv.p[par], ncomp}});
-    launch_tiled<kTrans, 0>(tg, tgrid, s, a, bv, par, n, st, w, nullptr,
-                            nullptr, 0, 1);
-  } else {
-    const int rp = (i - 1) & 1;
-    halo(pl, s, {{bv.rb[rp], ncomp}, {bv.p[par], ncomp}, {bv.t, ncomp}});
-    launch_tiled<kTrans, 5>(tg, tgrid, s, a, bv, par, n, st, w, nullptr,
-                            nullptr, 0, 0, x, bv.rb[rp], bv.rb[rp ^ 1]);
-  }
-  halo(pl, s, {{bv.v[par ^ 1], ncomp}, {bv.rb[par], ncomp}});
-  launch_tiled<kTrans, 6>(tg, tgrid, s, a, bv, par, n, st, w, nullptr,
-                          nullptr, 0, 0, nullptr, bv.rb[par]);
-}
-
-// after `launched` merged iterations: the x/r update of the last one
-template <bool kTrans>
-void jm_finish(const Plan &pl, const TileGeo &tg, int tgrid, cudaStream_t s,
-               const double *a, const BiVecs &bv, int launched, int64_t n,
-               int ncomp, SolverState *st, Workspace &w, double *x) {
-  if (launched < 1) return;
-  const int i = launched, par = i & 1, rp = (i - 1) & 1;
-  halo(pl, s, {{bv.rb[rp], ncomp}, {bv.p[par], ncomp}, {bv.t, ncomp}});
-  launch_tiled<kTrans, 5>(tg, tgrid, s, a, bv, par, n, st, w, nullptr,
-                          nullptr, 0, 0, x, bv.rb[rp], bv.rb[rp ^ 1]);
-}
-
 template <class V, bool kTrans>
 int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
             SolverState &hs, const double *a, const double *b, double *x,
@@ -2022,13 +1854,10 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   const int egrid = nm ? std::min(tge.ntiles, nm_minb() * pl.num_sms) : 0;
   double *z = base + 8 * len;  // the preconditioned iterate (nm)
   double *qg = pl.slab ? base + 9 * len : nullptr;  // slab edge stage 1
-  // tiled plans run the merged passes (Neumann-2 or Jacobi; PF_NO_MERGE=1:
-  // the three-pass Jacobi iteration)
-  const bool jm = tiled && !nm && getenv("PF_NO_MERGE") == nullptr;
-  if (nm || jm) {
+  if (nm) {
     bv.rb[0] = bv.r;
     bv.rb[1] = base + 10 * len;
-    bv.z = nm ? z : nullptr;
+    bv.z = z;
   }
   launch(k_bi_reset, 1, 1, s, st, ncomp, maxiter, precond, tol, fresh, mask);
   // the tiled init pass forms |b| itself
@@ -2069,11 +1898,6 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
                              (int64_t)n, ncomp, st, w, qg);
         continue;
       }
-      if (jm) {
-        jm_iteration<kTrans>(pl, tg, tgrid, s, a, bv, i, (int64_t)n, ncomp,
-                             st, w, x);
-        continue;
-      }
       halo(pl, s, {{bv.r, ncomp}, {bv.p[par], ncomp}});
       if (tiled)
         launch_tiled<kTrans, 0>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w,
@@ -2102,9 +1926,6 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     for (int q = 0; q < ncomp; ++q) lock = std::max(lock, (int)hs.c[q].iter);
     pl.bi_hint[kTrans ? 1 : 0] = lock;
   }
-  if (jm)
-    jm_finish<kTrans>(pl, tg, tgrid, s, a, bv, launched, (int64_t)n, ncomp,
-                      st, w, x);
   if (nm) {
     // the last iteration's x/r update (a merged pass whose pv part goes
     // unused; it returns at once when a poll already saw convergence)
@@ -2484,61 +2305,7 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
       for (int k = 1; k <= iters && !rc; ++k) rc = one(k, true);
       if (rc) return rc;
     }
-    // tiled Jacobi: the merged passes (as bi_core runs them)
-    const bool jm = tiled && !nm && getenv("PF_NO_MERGE") == nullptr;
-    if (jm) {
-      bv.rb[0] = bv.r;
-      bv.rb[1] = w.vecs + 11 * len;
-      auto one = [&](int k, bool timed) -> int {
-        const int par = k & 1;
-        if (timed) PF_CUDA(cudaEventRecord(ev[0], s));
-        if (k == 0) {
-          halo(pl, s, {{bv.rb[0], ncomp}, {bv.p[par], ncomp}});
-          if (transpose)
-            launch_tiled<true, 0>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w,
-                                  nullptr, nullptr, 0, 1);
-          else
-            launch_tiled<false, 0>(tg, tgrid, s, a, bv, par, (int64_t)n, st,
-                                   w, nullptr, nullptr, 0, 1);
-        } else {
-          const int rp = (k - 1) & 1;
-          halo(pl, s, {{bv.rb[rp], ncomp}, {bv.p[par], ncomp}, {bv.t, ncomp}});
-          if (transpose)
-            launch_tiled<true, 5>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w,
-                                  nullptr, nullptr, 0, 0, x, bv.rb[rp],
-                                  bv.rb[rp ^ 1]);
-          else
-            launch_tiled<false, 5>(tg, tgrid, s, a, bv, par, (int64_t)n, st,
-                                   w, nullptr, nullptr, 0, 0, x, bv.rb[rp],
-                                   bv.rb[rp ^ 1]);
-        }
-        if (timed) PF_CUDA(cudaEventRecord(ev[1], s));
-        halo(pl, s, {{bv.v[par ^ 1], ncomp}, {bv.rb[par], ncomp}});
-        if (transpose)
-          launch_tiled<true, 6>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w,
-                                nullptr, nullptr, 0, 0, nullptr, bv.rb[par]);
-        else
-          launch_tiled<false, 6>(tg, tgrid, s, a, bv, par, (int64_t)n, st, w,
-                                 nullptr, nullptr, 0, 0, nullptr, bv.rb[par]);
-        if (!timed) return PF_OK;
-        PF_CUDA(cudaEventRecord(ev[2], s));
-        PF_CUDA(cudaEventRecord(ev[3], s));
-        PF_CUDA(cudaEventSynchronize(ev[3]));
-        for (int j = 0; j < 3; ++j) {
-          float ms = 0.f;
-          PF_CUDA(cudaEventElapsedTime(&ms, ev[j], ev[j + 1]));
-          tot[j] += ms;
-        }
-        float ms = 0.f;
-        PF_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[3]));
-        tot[3] += ms;
-        return PF_OK;
-      };
-      int rc = one(0, false);
-      for (int k = 1; k <= iters && !rc; ++k) rc = one(k, true);
-      if (rc) return rc;
-    }
-    for (int k = 0; k < iters && !nm && !jm; ++k) {
+    for (int k = 0; k < iters && !nm; ++k) {
       const int par = k & 1;
       halo(pl, s, {{bv.r, ncomp}, {bv.p[par], ncomp}});
       PF_CUDA(cudaEventRecord(ev[0], s));
@@ -2588,7 +2355,7 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
       return PF_ERR_ARG;
     }
     for (int j = 0; j < 4; ++j) ms_host[j] = tot[j] / iters;
-    ms_host[4] = nm ? kPrecondNeumann2 : jm ? 5 : 1;
+    ms_host[4] = nm ? kPrecondNeumann2 : 1;
     return PF_OK;
   });
 }
