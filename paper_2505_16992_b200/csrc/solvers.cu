@@ -826,6 +826,11 @@ __device__ __forceinline__ void cp_async_commit() {
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
+// all but the N most recent committed groups have landed
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 // Shared memory of the tiled passes: the raw inputs of two planes (tile +
 // halo, filled by cp.async one plane ahead) and the preconditioned values
@@ -837,6 +842,20 @@ struct TileSmem {
   double g[2][3][kTY + 2][kTZ + 2];
 };
 constexpr size_t kTileSmem = sizeof(TileSmem);
+
+// Per-pass layout of the raw buffers: the pv pass stages 10 arrays two
+// planes deep (71 KB, two CTAs per SM: a larger buffer shrinks the L1 the
+// transposed neighbour gathers use and was measured slower); the lighter
+// passes stage fewer arrays three planes deep, so a plane's loads have two
+// plane steps to land
+template <int MODE>
+struct TileLayout {
+  static constexpr int kStages = MODE == 0 ? 2 : 3;
+  static constexpr int kArr = MODE == 0 ? 10 : MODE == 1 ? 7 : MODE == 4 ? 4 : 3;
+  static constexpr int kDinv = MODE == 0 ? 9 : MODE == 1 ? 6 : 3;  // 1/A slot
+  static constexpr size_t kBytes =
+      sizeof(double) * (size_t)(kStages * kArr + 6) * kTP;
+};
 
 // MODE 0 (pass pv): g = (r + beta (p0 - omega v0)) / A, outputs p' (the
 //                   undivided value), v' = A g, sums r^.v'.  `first` (the
@@ -867,7 +886,15 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
   constexpr bool kX = MODE >= 2;  // the input is the iterate x (or z) itself
   constexpr bool kZ = MODE == 4;  // ... divided by A (the close pass)
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  TileSmem &sm = *reinterpret_cast<TileSmem *>(smem_raw);
+  using TL = TileLayout<MODE>;
+  constexpr int kStages = TL::kStages, kDs = TL::kDinv;
+  using RawPlane = double[TL::kArr][kTY + 2][kTZ + 2];
+  using GPlane = double[3][kTY + 2][kTZ + 2];
+  RawPlane *raw = reinterpret_cast<RawPlane *>(smem_raw);
+  GPlane *gbuf = reinterpret_cast<GPlane *>(
+      smem_raw + sizeof(double) * (size_t)kStages * TL::kArr * kTP);
+  // raw slot of plane x (x >= -1)
+  auto slot = [](int32_t x) { return (x + kStages) % kStages; };
   const int nc = MODE == 3 ? nverify : st->ncomp;
   const int pc_on = st->precond;
   int act[3];
@@ -910,36 +937,36 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
       const int64_t o = q * n + j;
       if (kX) {
         if (ok)
-          cp_async8(&sm.raw[b][q][sy][sz], xin + o);
+          cp_async8(&raw[b][q][sy][sz], xin + o);
         else
-          sm.raw[b][q][sy][sz] = 0.0;
+          raw[b][q][sy][sz] = 0.0;
         continue;
       }
       if (ok) {
-        cp_async8(&sm.raw[b][q][sy][sz], r + o);
+        cp_async8(&raw[b][q][sy][sz], r + o);
         if (!fresh) {
-          cp_async8(&sm.raw[b][3 + q][sy][sz], vin + o);
-          if (MODE == 0) cp_async8(&sm.raw[b][6 + q][sy][sz], pin + o);
+          cp_async8(&raw[b][3 + q][sy][sz], vin + o);
+          if (MODE == 0) cp_async8(&raw[b][6 + q][sy][sz], pin + o);
         }
       } else {
-        sm.raw[b][q][sy][sz] = 0.0;
-        sm.raw[b][3 + q][sy][sz] = 0.0;
-        if (MODE == 0) sm.raw[b][6 + q][sy][sz] = 0.0;
+        raw[b][q][sy][sz] = 0.0;
+        raw[b][3 + q][sy][sz] = 0.0;
+        if (MODE == 0) raw[b][6 + q][sy][sz] = 0.0;
       }
     }
     if (kX && !kZ) return;
     if (ok)
-      cp_async8(&sm.raw[b][9][sy][sz], dinv + j);
+      cp_async8(&raw[b][kDs][sy][sz], dinv + j);
     else
-      sm.raw[b][9][sy][sz] = 0.0;
+      raw[b][kDs][sy][sz] = 0.0;
   };
   // g (and the undivided value) of slot (sy, sz) of raw buffer b
   auto G = [&](int b, int sy, int sz, double (&g)[3], double (&pv)[3]) {
     if (kZ) {
-      const double dj = sm.raw[b][9][sy][sz];
+      const double dj = raw[b][kDs][sy][sz];
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        pv[q] = (q < nc && act[q]) ? sm.raw[b][q][sy][sz] : 0.0;
+        pv[q] = (q < nc && act[q]) ? raw[b][q][sy][sz] : 0.0;
         g[q] = pv[q] * dj;
       }
       return;
@@ -947,23 +974,23 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
     if (kX) {
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        g[q] = pv[q] = (q < nc && act[q]) ? sm.raw[b][q][sy][sz] : 0.0;
+        g[q] = pv[q] = (q < nc && act[q]) ? raw[b][q][sy][sz] : 0.0;
       }
       return;
     }
-    const double dj = sm.raw[b][9][sy][sz];
+    const double dj = raw[b][kDs][sy][sz];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
       g[q] = pv[q] = 0.0;
       if (q >= nc || !act[q]) continue;
-      const double rr = sm.raw[b][q][sy][sz];
+      const double rr = raw[b][q][sy][sz];
       double val;
       if (fresh) {
         val = rr;  // r + beta (0 - omega 0)
       } else {
-        const double vv = sm.raw[b][3 + q][sy][sz];
+        const double vv = raw[b][3 + q][sy][sz];
         val = MODE == 0
-                  ? rr + c0[q] * (sm.raw[b][6 + q][sy][sz] - c1[q] * vv)
+                  ? rr + c0[q] * (raw[b][6 + q][sy][sz] - c1[q] * vv)
                   : rr - c0[q] * vv;
       }
       pv[q] = val;
@@ -1003,35 +1030,40 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
       halo_cell = false;
     }
     auto issue_plane = [&](int32_t x) {
-      const int b = x & 1;
+      const int b = slot(x);
       issue(b, x, y, z, ty + 1, tz + 1);
       if (halo_cell) issue(b, x, hy, hz, sy_, sz_);
       cp_async_commit();
     };
     // g of plane x (tile + halo) from its raw buffer into g buffer x & 1
     auto convert = [&](int32_t x, double (&gcen)[3], double (&pcen)[3]) {
-      const int b = x & 1;
+      const int b = slot(x);
+      const int gb2 = x & 1;
       G(b, ty + 1, tz + 1, gcen, pcen);
 #pragma unroll
-      for (int q = 0; q < 3; ++q) sm.g[b][q][ty + 1][tz + 1] = gcen[q];
+      for (int q = 0; q < 3; ++q) gbuf[gb2][q][ty + 1][tz + 1] = gcen[q];
       if (halo_cell) {
         double hg[3], tmp[3];
         G(b, sy_, sz_, hg, tmp);
 #pragma unroll
-        for (int q = 0; q < 3; ++q) sm.g[b][q][sy_][sz_] = hg[q];
+        for (int q = 0; q < 3; ++q) gbuf[gb2][q][sy_][sz_] = hg[q];
       }
     };
 
     double gm[3], gc[3], gn[3], pc[3], pn[3], tmp[3];
-    __syncthreads();  // the previous tile is done with both buffers
-    issue_plane(xs - 1);
-    issue_plane(xs);
-    cp_async_wait_all();
+    __syncthreads();  // the previous tile is done with every buffer
+    // planes xs - 1 .. xs + kStages - 2 in flight; wait for the first two
+    for (int k = 0; k < kStages; ++k) {
+      if (xs - 1 + k <= xe) issue_plane(xs - 1 + k);
+      else cp_async_commit();
+    }
+    cp_async_wait<kStages - 2>();
     __syncthreads();
-    G((xs - 1) & 1, ty + 1, tz + 1, gm, tmp);
+    G(slot(xs - 1), ty + 1, tz + 1, gm, tmp);
     convert(xs, gc, pc);
-    __syncthreads();  // raw buffer (xs - 1) & 1 is free again
-    issue_plane(xs + 1);
+    __syncthreads();  // raw slot of plane xs - 1 is free again
+    if (xs + kStages - 1 <= xe) issue_plane(xs + kStages - 1);
+    else cp_async_commit();
     for (int32_t x = xs; x < xe; ++x) {
       const int64_t i = (int64_t)x * sX + (int64_t)y * sY + z;
       // this plane's coefficients (and r^): plain loads, consumed after the
@@ -1063,10 +1095,11 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
         rh[q] = (MODE == 0 && q < nc && act[q]) ? w.rhat[q * n + i]
                 : (kX && !kZ && q < nc && act[q]) ? bin[q * n + i]
                                                   : 0.0;
-      cp_async_wait_all();  // my copies of plane x + 1 have landed
-      __syncthreads();      // everyone's have; g of plane x is complete
+      cp_async_wait<kStages - 2>();  // my copies of plane x + 1 have landed
+      __syncthreads();  // everyone's have; g of plane x is complete
       convert(x + 1, gn, pn);
-      if (x + 2 <= xe) issue_plane(x + 2);
+      if (x + kStages <= xe) issue_plane(x + kStages);
+      else cp_async_commit();
       const int gb = x & 1;
       if (kZ) {
         const double di = w.dinv[i];
@@ -1074,10 +1107,10 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
         for (int q = 0; q < 3; ++q) {
           if (q >= nc || !act[q]) continue;
           const double off = cf[0] * gm[q] + cf[1] * gn[q] +
-                             cf[2] * sm.g[gb][q][ty][tz + 1] +
-                             cf[3] * sm.g[gb][q][ty + 2][tz + 1] +
-                             cf[4] * sm.g[gb][q][ty + 1][tz] +
-                             cf[5] * sm.g[gb][q][ty + 1][tz + 2];
+                             cf[2] * gbuf[gb][q][ty][tz + 1] +
+                             cf[3] * gbuf[gb][q][ty + 2][tz + 1] +
+                             cf[4] * gbuf[gb][q][ty + 1][tz] +
+                             cf[5] * gbuf[gb][q][ty + 1][tz + 2];
           xout[q * n + i] += gc[q] - di * off;
         }
       }
@@ -1085,10 +1118,10 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
       for (int q = 0; q < 3; ++q) {
         if (kZ || q >= nc || !act[q]) continue;
         const double yv = aii * gc[q] + cf[0] * gm[q] + cf[1] * gn[q] +
-                          cf[2] * sm.g[gb][q][ty][tz + 1] +
-                          cf[3] * sm.g[gb][q][ty + 2][tz + 1] +
-                          cf[4] * sm.g[gb][q][ty + 1][tz] +
-                          cf[5] * sm.g[gb][q][ty + 1][tz + 2];
+                          cf[2] * gbuf[gb][q][ty][tz + 1] +
+                          cf[3] * gbuf[gb][q][ty + 2][tz + 1] +
+                          cf[4] * gbuf[gb][q][ty + 1][tz] +
+                          cf[5] * gbuf[gb][q][ty + 1][tz + 2];
         const int64_t o = q * n + i;
         if (MODE == 0) {
           vout[o] = yv;
@@ -1577,10 +1610,10 @@ void launch_tiled(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
       if (done.insert(reinterpret_cast<const void *>(kernel)).second)
         cudaFuncSetAttribute(kernel,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kTileSmem);
+                             (int)TileLayout<MODE>::kBytes);
     }
     count_launch();
-    kernel<<<grid, kTileThreads, kTileSmem, s>>>(tg, a, bv, par, n, st,
+    kernel<<<grid, kTileThreads, TileLayout<MODE>::kBytes, s>>>(tg, a, bv, par, n, st,
                                                  w.partials, w.counters, xin,
                                                  bin, nverify, xout);
   };
@@ -1860,11 +1893,18 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     bv.z = z;
   }
   launch(k_bi_reset, 1, 1, s, st, ncomp, maxiter, precond, tol, fresh, mask);
+  // init / verification on the tiled passes, or the per-cell gather kernels
+  // (PF_TILED_SETUP=0)
+  static const bool tsetup = [] {
+    const char *e = getenv("PF_TILED_SETUP");
+    return !(e && atoi(e) == 0);
+  }();
+  const bool tinit = tiled && tsetup;
   // the tiled init pass forms |b| itself
-  if (fresh && !tiled)
+  if (fresh && !tinit)
     launch(k_bi_bnorm, gr, kBlock, s, b, n, rg, st, w.partials, w.counters);
   halo(pl, s, {{x, ncomp}});
-  if (tiled)
+  if (tinit)
     launch_tiled<kTrans, 2>(tg, tgrid, s, a, bv, 0, (int64_t)n, st, w, x, b, 0);
   else
     launch(k_bi_init<V, kTrans>, gr, kBlock, s, v, a, b, x, bv, st,
@@ -1938,7 +1978,7 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   }
   launch(k_bi_finish, ge, kBlock, s, x, n, rg, st);
   halo(pl, s, {{x, ncomp}});
-  if (tiled)
+  if (tinit)
     launch_tiled<kTrans, 3>(tg, tgrid, s, a, bv, 0, (int64_t)n, st, w, x, b,
                             ncomp);
   else
