@@ -434,6 +434,7 @@ class ClockSampler:
 KERNEL_BYTES = {
     "k_cg_spmv_faces": 40,        # 3 face weights + p + q
     "k_cg_spmv": 40,              # survey SpMV_P minimum (stencil form moves 72)
+    "k_cg_spmv_pt": 56,           # tiled: z, p, 3 faces in; p', q out
     "k_cg_update": 48,            # x, p, r, q read; x, r written
     # damped block-Jacobi Y-line smoother (Thomas factors precomputed)
     "k_mg_smooth0 (level 0)": 40,         # r, 1/den, w_y, c' read; x written
@@ -478,6 +479,8 @@ def kernel_bytes(nm, d):
         return bi[nm]
     co = 8.0 / 2 ** d
     dep = {"k_cg_spmv_faces": 8 * (d + 2),
+           # tiled direction update + SpMV: z, p, d faces in; p', q out
+           "k_cg_spmv_pt": 8 * (d + 2) + 16,
            # stencil form (Jacobi plans: multi-block grids): rows + p + q
            "k_cg_spmv": 8 * rows + 16,
            "k_mg_resid_restrict (level 0)": 8 * (2 + d) + co,
@@ -522,13 +525,15 @@ def measure_roofline(args, dom, plan, state, nu, dt, dev, per_step):
     mg = plan.has_mg
     if mg:
         plan.mg_prepare(k)
-    ms = (ctypes.c_double * 11)()
+    ms = (ctypes.c_double * 12)()
     _lib.call("pf_cg_profile", plan.handle, _lib.ptr(k), _lib.ptr(b),
               args.profile_iters, 2 if mg else 1, _lib.ptr(plan.workspace),
               _lib.ptr(plan.mg_workspace if mg else None), ms, plan.stream)
-    names = (["k_cg_spmv_faces" if mg else "k_cg_spmv", "k_cg_update"]
+    cgt = ms[11] == 1.0   # the direction update rides in the tiled SpMV
+    names = (["k_cg_spmv_pt" if cgt else
+              "k_cg_spmv_faces" if mg else "k_cg_spmv", "k_cg_update"]
              + ((SPEC_NAMES if plan.geom_kind == "spectral" else MG_NAMES)
-                if mg else [None] * 6) + ["k_cg_pupdate"])
+                if mg else [None] * 6) + [None if cgt else "k_cg_pupdate"])
     cg = {}
     for j, nm in enumerate(names):
         if nm is not None and nm in KERNEL_BYTES and ms[j] > 0:
@@ -627,7 +632,7 @@ def whole_step_bytes(d, per_step, n, peak, nm_bi):
     fwd = 16 * s + (2 * d + 2) * s + n_corr * ((q + 3 * d + 1) * s
                                                 + (2 * d + 2) * s)
     adj = n_corr * (4 * q + 6 * d + 8) * s + (3 * q + 4 * d + 4) * s
-    cg_it = (d + 2) * s + 6 * s + 11 * s + 3 * s
+    cg_it = (d + 2) * s + 6 * s + 11 * s + 3 * s   # (tiled: 2 s less)
     b = (fwd + adj + bi_it * (per_step["bi_fwd"] + per_step["bi_adj"])
          + 2 * bi_solve + cg_it * per_step["cg"] + 4 * n_corr * 12 * s / 2)
     gbs = b * n / (per_step["ms"] * 1e-3) / 1e9

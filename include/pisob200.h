@@ -265,7 +265,9 @@ PF_API int pf_bicgstab_solve(const pf_plan *plan, const double *a, int32_t trans
  *          spectral: Z transform | X transform | Y solve | inverse X |
  *          inverse Z (precond == PF_PRECOND_MG; zero otherwise)
  *   [7] z sums   [8] direction update   [9] whole iteration
- *   [10] whole iteration replayed from the cached CUDA graph (MG only).
+ *   [10] whole iteration replayed from the cached CUDA graph (MG only)
+ *   [11] 1 when the direction update rides in a tiled SpMV (slot [0] then
+ *        times k_cg_spmv_pt, slot [8] is empty).
  * Used by bench.py for the roofline figure. */
 PF_API int pf_cg_profile(const pf_plan *plan, const double *a,
                          const double *b, int32_t iters, int32_t precond,

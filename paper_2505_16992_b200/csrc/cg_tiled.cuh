@@ -1,0 +1,168 @@
+// cg_tiled.cuh -- the pressure CG's direction update fused into its SpMV on
+// 2.5D tiles (3D single-device boxes with whole 8 x 32 Y/Z tiles).
+// Included by solvers.cu inside namespace pf (uses TileGeo, wrap, cp_async8,
+// MgLevel).
+//
+// The reference's CG iteration (S/linalg.py:136-170) updates the direction
+// p = z + beta p (after zero-mean projection) and then applies the
+// operator.  Here one pass forms p' = beta p + (z - zbar) at every stencil
+// point from z and the previous direction, stores p' at its own cells and
+// applies the level-0 face form of K (q = sum_f w_f (p'_i - p'_nb), the
+// operator k_cg_spmv_faces applies): 56 B/cell (z, p, 3 face weights in;
+// p', q out) instead of the 24 + 40 of the separate direction update and
+// gather SpMV, and tiled, so every array is read once per cell.  The
+// directions ping-pong by iteration parity: iteration it (c.iter before this
+// pass) reads P[(it & 1) ^ 1] and writes P[it & 1]; the first iteration
+// forms p' = z - zbar (the reference's initial direction) and reads no p.
+
+constexpr int kCgArr = 4;  // z, p, wy, wz
+struct CgTileSmem {
+  double raw[2][kCgArr][kTY + 2][kTZ + 2];
+  double g[2][kTY + 2][kTZ + 2];  // p' of planes x & 1
+};
+constexpr size_t kCgTileSmem = sizeof(CgTileSmem);
+
+__global__ void __launch_bounds__(kTileThreads, 2)
+    k_cg_spmv_pt(TileGeo tg, MgLevel L, const double *__restrict__ z,
+                 double *P0, double *P1, double *__restrict__ q,
+                 SolverState *st, double *partials, unsigned *counter) {
+  if (st->all_done) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CgTileSmem &sm = *reinterpret_cast<CgTileSmem *>(smem_raw);
+  const CompState &cs = st->c[0];
+  const int it = cs.iter;
+  const bool first = it == 0;
+  const double beta = first ? 0.0 : cs.beta, zbar = cs.zbar;
+  const double *__restrict__ pold = (it & 1) ? P0 : P1;
+  double *__restrict__ pnew = (it & 1) ? P1 : P0;
+  const double *__restrict__ wx = L.wx;
+  const double *__restrict__ wy = L.wy;
+  const double *__restrict__ wz = L.wz;
+  const int64_t sX = (int64_t)tg.Y * tg.Z, sY = tg.Z;
+  const int tz = threadIdx.x % kTZ, ty = threadIdx.x / kTZ;
+
+  auto issue = [&](int b, int32_t x, int32_t y, int32_t zc, int sy, int sz) {
+    bool okx, oky, okz;
+    x = wrap(x, tg.X, tg.px, okx);
+    y = wrap(y, tg.Y, tg.py, oky);
+    zc = wrap(zc, tg.Z, tg.pz, okz);
+    const int64_t j = (int64_t)x * sX + (int64_t)y * sY + zc;
+    if (okx && oky && okz) {
+      cp_async8(&sm.raw[b][0][sy][sz], z + j);
+      if (!first) cp_async8(&sm.raw[b][1][sy][sz], pold + j);
+      cp_async8(&sm.raw[b][2][sy][sz], wy + j);
+      cp_async8(&sm.raw[b][3][sy][sz], wz + j);
+    } else {
+      // outside a walled box: its face weights are zero (any finite p)
+      sm.raw[b][0][sy][sz] = 0.0;
+      sm.raw[b][1][sy][sz] = 0.0;
+      sm.raw[b][2][sy][sz] = 0.0;
+      sm.raw[b][3][sy][sz] = 0.0;
+    }
+  };
+  auto pval = [&](int b, int sy, int sz) {
+    const double zz = sm.raw[b][0][sy][sz] - zbar;
+    return first ? zz : beta * sm.raw[b][1][sy][sz] + zz;
+  };
+
+  double acc[1] = {0.0};
+  for (int tile = blockIdx.x; tile < tg.ntiles; tile += gridDim.x) {
+    const int tzt = tile % tg.tz_tiles;
+    const int rest = tile / tg.tz_tiles;
+    const int tyt = rest % tg.ty_tiles;
+    const int ch = rest / tg.ty_tiles;
+    const int32_t y = tyt * kTY + ty, zc = tzt * kTZ + tz;
+    const int32_t xs = tg.x0 + ch * tg.xc;
+    const int32_t xe = min(xs + tg.xc, tg.x1);
+    bool halo_cell = true;
+    int hy = 0, hz = 0, sy_ = 0, sz_ = 0;
+    if (threadIdx.x < 2 * kTZ) {
+      const int side = threadIdx.x / kTZ;
+      hy = tyt * kTY + (side ? kTY : -1);
+      hz = zc;
+      sy_ = side ? kTY + 1 : 0;
+      sz_ = tz + 1;
+    } else if (threadIdx.x < 2 * kTZ + 2 * kTY) {
+      const int k = threadIdx.x - 2 * kTZ;
+      const int side = k / kTY;
+      hy = tyt * kTY + (k % kTY);
+      hz = tzt * kTZ + (side ? kTZ : -1);
+      sy_ = (k % kTY) + 1;
+      sz_ = side ? kTZ + 1 : 0;
+    } else {
+      halo_cell = false;
+    }
+    auto issue_plane = [&](int32_t x) {
+      const int b = x & 1;
+      issue(b, x, y, zc, ty + 1, tz + 1);
+      if (halo_cell) issue(b, x, hy, hz, sy_, sz_);
+      cp_async_commit();
+    };
+    // p' of plane x (tile + halo) into g buffer x & 1; own value returned
+    auto convert = [&](int32_t x) {
+      const int b = x & 1;
+      const double pc = pval(b, ty + 1, tz + 1);
+      sm.g[b][ty + 1][tz + 1] = pc;
+      if (halo_cell) sm.g[b][sy_][sz_] = pval(b, sy_, sz_);
+      return pc;
+    };
+    // X face weight of plane x at the own column (0 outside a walled box)
+    auto wx_at = [&](int32_t x) {
+      bool ok;
+      const int32_t gx = wrap(x, tg.X, tg.px, ok);
+      return ok ? __ldg(wx + (int64_t)gx * sX + (int64_t)y * sY + zc) : 0.0;
+    };
+
+    __syncthreads();  // the previous tile is done with both buffers
+    double wxm = wx_at(xs - 1);
+    issue_plane(xs - 1);
+    issue_plane(xs);
+    cp_async_wait_all();
+    __syncthreads();
+    double pm = pval((xs - 1) & 1, ty + 1, tz + 1);
+    double pc = convert(xs);
+    __syncthreads();  // raw buffer (xs - 1) & 1 is free again
+    issue_plane(xs + 1);
+    for (int32_t x = xs; x < xe; ++x) {
+      const int64_t i = (int64_t)x * sX + (int64_t)y * sY + zc;
+      const double wxc = __ldg(wx + i);
+      const int gb = x & 1;
+      // this plane's Y / Z weights of the own cell and its -y / -z
+      // neighbours: plane x landed before the previous barrier, and its raw
+      // slot is refilled (plane x + 2) only after the next one
+      const double wyp = sm.raw[gb][2][ty + 1][tz + 1];
+      const double wym = sm.raw[gb][2][ty][tz + 1];
+      const double wzp = sm.raw[gb][3][ty + 1][tz + 1];
+      const double wzm = sm.raw[gb][3][ty + 1][tz];
+      cp_async_wait_all();  // my copies of plane x + 1 have landed
+      __syncthreads();      // everyone's have; p' of plane x is complete
+      const double pn = convert(x + 1);
+      if (x + 2 <= xe) issue_plane(x + 2);
+      const double qi = wxc * (pc - pn) + wxm * (pc - pm) +
+                        wyp * (pc - sm.g[gb][ty + 2][tz + 1]) +
+                        wym * (pc - sm.g[gb][ty][tz + 1]) +
+                        wzp * (pc - sm.g[gb][ty + 1][tz + 2]) +
+                        wzm * (pc - sm.g[gb][ty + 1][tz]);
+      pnew[i] = pc;
+      q[i] = qi;
+      acc[0] += pc * qi;
+      pm = pc;
+      pc = pn;
+      wxm = wxc;
+    }
+    cp_async_wait_all();
+  }
+  double tot[1];
+  if (grid_reduce<1>(acc, partials, counter, tot)) {
+    CompState &c = st->c[0];
+    c.iter += 1;
+    const double pap = tot[0];
+    if (!finite(pap) || fabs(pap) < DBL_MIN) {
+      c.fail = 1;
+      c.done = 1;
+      st->all_done = 1;
+      return;
+    }
+    c.alpha = c.rz / pap;
+  }
+}

@@ -316,6 +316,39 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// k_cg_update for the fused direction update (cg_tiled.cuh): p is the
+// direction the last k_cg_spmv_pt wrote, P[(c.iter - 1) & 1]
+__global__ void __launch_bounds__(kBlock)
+    k_cg_update_pt(const double *__restrict__ p0, const double *__restrict__ p1,
+                   const double *__restrict__ q, double *__restrict__ x,
+                   double *__restrict__ r, Rng rg, SolverState *st,
+                   double *partials, unsigned *counter) {
+  if (st->all_done) return;
+  const double *__restrict__ p = ((st->c[0].iter - 1) & 1) ? p1 : p0;
+  const double alpha = st->c[0].alpha;
+  double acc[2] = {0.0, 0.0};
+  RANGE_LOOP(i, rg) {
+    const double xi = x[i] + alpha * p[i];
+    const double ri = r[i] - alpha * q[i];
+    x[i] = xi;
+    r[i] = ri;
+    acc[0] += ri * ri;
+    acc[1] += xi;
+  }
+  double tot[2];
+  if (grid_reduce<2>(acc, partials, counter, tot)) {
+    CompState &c = st->c[0];
+    c.res = sqrt(tot[0]);
+    if (c.res <= c.tol_abs) {
+      c.converged = 1;
+      c.done = 1;
+      c.project_x = st->zero_mean;
+      c.xmean = st->zero_mean ? tot[1] / rg.ng : 0.0;
+      st->all_done = 1;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kBlock)
     k_cg_pupdate(const double *__restrict__ a, const double *__restrict__ r,
                  const double *__restrict__ z, double *__restrict__ p,
@@ -1238,6 +1271,7 @@ __global__ void __launch_bounds__(kBlock)
 }
 
 #include "bicg_nm.cuh"
+#include "cg_tiled.cuh"
 
 }  // namespace pf
 
@@ -1270,6 +1304,34 @@ int next_batch(int done_iters, int hint) {
   return b;
 }
 
+bool tile_geo_dim(const Plan &pl, int dim, TileGeo &tg);
+
+// The fused direction update + SpMV on tiles (cg_tiled.cuh) applies on
+// single-device 3D boxes whose level-0 face form is laid out as the box
+// (PF_NO_TILED_CG=1: the per-cell gather SpMV and a separate update)
+bool cg_tiled(const Plan &pl, const MgHierarchy *mg, TileGeo &tg) {
+  static const bool off = getenv("PF_NO_TILED_CG") != nullptr;
+  if (off || pl.slab || !mg || !tile_geo_dim(pl, pl.d.dim, tg)) return false;
+  const MgLevel &L = mg->lv[0];
+  return L.sx == tg.X && L.sy == tg.Y && L.sz == tg.Z && L.px == tg.px &&
+         L.pz == tg.pz && !tg.py;
+}
+
+void launch_cg_spmv_pt(const TileGeo &tg, const Plan &pl, const MgLevel &L,
+                       const double *z, double *p0, double *p1, double *q,
+                       SolverState *st, Workspace &w, cudaStream_t s) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(k_cg_spmv_pt,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kCgTileSmem);
+  });
+  count_launch();
+  k_cg_spmv_pt<<<std::min(tg.ntiles, pl.red_blocks), kTileThreads,
+                 kCgTileSmem, s>>>(tg, L, z, p0, p1, q, st, w.partials,
+                                   w.counters);
+}
+
 // one multigrid-preconditioned CG iteration on workspace buffers only
 void mg_iteration(const Plan &pl, Workspace &w, SolverState *st,
                   const MgHierarchy *mg, double *x, cudaStream_t s) {
@@ -1278,6 +1340,17 @@ void mg_iteration(const Plan &pl, Workspace &w, SolverState *st,
   double *z = w.vecs + 4 * (int64_t)n;
   const int ge = grid_for(pl.i1 - pl.i0), gr = std::min(ge, pl.red_blocks);
   const Rng rg = plan_range(pl);
+  TileGeo tg;
+  if (cg_tiled(pl, mg, tg)) {
+    double *p1 = w.vecs + 6 * (int64_t)n;
+    launch_cg_spmv_pt(tg, pl, mg->lv[0], z, p, p1, q, st, w, s);
+    launch(k_cg_update_pt, gr, kBlock, s, (const double *)p,
+           (const double *)p1, (const double *)q, x, r, rg, st, w.partials,
+           w.counters);
+    const CgFuse fuse{st, w.partials, w.counters, 0};
+    mg_apply(*mg, r, z, s, &st->all_done, nullptr, &fuse, pl.red_blocks, &pl);
+    return;
+  }
   halo(pl, s, {{p, 1}});
   launch(k_cg_spmv_faces, gr, kBlock, s, mg->lv[0], rg, (const double *)p, q, st,
          w.partials, w.counters);
@@ -1387,8 +1460,11 @@ int cg_core_mg(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   const CgFuse fuse{st, w.partials, w.counters, 1};
   int rc = mg_apply(*mg, r, z, s, done, nullptr, &fuse, pl.red_blocks, &pl);
   if (rc) return rc;
-  launch(k_cg_pinit, ge, kBlock, s, (const double *)nullptr, r,
-         (const double *)z, p, rg, st);
+  // the tiled iteration forms the first direction itself (p = z - zbar)
+  TileGeo tgc;
+  if (!cg_tiled(pl, mg, tgc))
+    launch(k_cg_pinit, ge, kBlock, s, (const double *)nullptr, r,
+           (const double *)z, p, rg, st);
   PF_LAUNCH_CHECK("mg-cg setup");
   // PF_NO_GRAPHS=1: launch the iterations directly (the in-process slab
   // tests: instantiating a graph may wait for the whole device while other
@@ -1634,10 +1710,14 @@ void launch_tiled(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
 }
 
 // tiled stencil passes apply to 3D boxes whose Y / Z extents are whole tiles
+bool tile_geo_dim(const Plan &pl, int dim, TileGeo &tg);
 template <class V>
 bool tile_geo(const Plan &pl, const V &v, TileGeo &tg) {
   (void)v;
-  if (V::kDim != 3 || pl.d.topo != PF_TOPO_BOX) return false;
+  return tile_geo_dim(pl, V::kDim, tg);
+}
+bool tile_geo_dim(const Plan &pl, int dim, TileGeo &tg) {
+  if (dim != 3 || pl.d.topo != PF_TOPO_BOX) return false;
   if (getenv("PF_NO_TILED")) return false;
   tg.X = (int32_t)pl.d.box_shape[0];
   tg.Y = (int32_t)pl.d.box_shape[1];
@@ -2118,24 +2198,36 @@ extern "C" int pf_cg_profile(const pf_plan *plan, const double *a,
       int rc = mg_apply(mg, r, z, s, done, nullptr, &fuse, pl.red_blocks, &pl);
       if (rc) return rc;
     }
-    launch(k_cg_pinit, ge, kBlock, s, a, r, (const double *)z, p, rg, st);
+    // the tiled fused direction update + SpMV where production runs it
+    TileGeo tgc;
+    const bool cgt = precond == 2 && cg_tiled(pl, &mg, tgc);
+    double *p1 = w.vecs + 6 * (int64_t)n;
+    if (!cgt)
+      launch(k_cg_pinit, ge, kBlock, s, a, r, (const double *)z, p, rg, st);
     // events: 0 start | 1 spmv | 2 update | 3..8 mg level-0 marks | 9 zsum |
-    // 10 pupdate
+    // 10 pupdate (tiled: folded into the spmv)
     cudaEvent_t ev[11];
     for (auto &e : ev) PF_CUDA(cudaEventCreate(&e));
     double tot[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     for (int k = 0; k < iters; ++k) {
-      halo(pl, s, {{p, 1}});
+      if (!cgt) halo(pl, s, {{p, 1}});
       PF_CUDA(cudaEventRecord(ev[0], s));
-      if (precond == 2)
+      if (cgt)
+        launch_cg_spmv_pt(tgc, pl, mg.lv[0], z, p, p1, q, st, w, s);
+      else if (precond == 2)
         launch(k_cg_spmv_faces, gr, kBlock, s, mg.lv[0], rg, (const double *)p,
                q, st, w.partials, w.counters);
       else
         launch(k_cg_spmv<V>, gr, kBlock, s, v, a, p, q, st, w.partials,
                w.counters);
       PF_CUDA(cudaEventRecord(ev[1], s));
-      launch(k_cg_update, gr, kBlock, s, a, p, q, x, r, rg, st, w.partials,
-             w.counters);
+      if (cgt)
+        launch(k_cg_update_pt, gr, kBlock, s, (const double *)p,
+               (const double *)p1, (const double *)q, x, r, rg, st,
+               w.partials, w.counters);
+      else
+        launch(k_cg_update, gr, kBlock, s, a, p, q, x, r, rg, st, w.partials,
+               w.counters);
       PF_CUDA(cudaEventRecord(ev[2], s));
       if (precond == 2) {
         // as in production: the z-sums ride in the last smoothing pass, so
@@ -2147,7 +2239,8 @@ extern "C" int pf_cg_profile(const pf_plan *plan, const double *a,
         for (int j = 3; j < 9; ++j) PF_CUDA(cudaEventRecord(ev[j], s));
       }
       PF_CUDA(cudaEventRecord(ev[9], s));
-      launch(k_cg_pupdate, ge, kBlock, s, a, r, (const double *)z, p, rg, st);
+      if (!cgt)
+        launch(k_cg_pupdate, ge, kBlock, s, a, r, (const double *)z, p, rg, st);
       PF_CUDA(cudaEventRecord(ev[10], s));
       PF_CUDA(cudaEventSynchronize(ev[10]));
       // spmv, update, [mg: smooth0, restrict, coarse, prolong, smooth2],
@@ -2194,6 +2287,7 @@ extern "C" int pf_cg_profile(const pf_plan *plan, const double *a,
     }
     for (int j = 0; j < 10; ++j) ms_host[j] = tot[j] / iters;
     ms_host[10] = graph_ms;
+    ms_host[11] = cgt ? 1.0 : 0.0;
     return PF_OK;
   });
 }

@@ -15,6 +15,6 @@ k = torch.empty_like(c)
 _lib.call("pf_assemble_pressure", plan.handle, _lib.ptr(c), 0, _lib.ptr(k), plan.stream)
 plan.mg_prepare(k)
 b = torch.randn(dom.n, dtype=torch.float64, device=dev)
-ms = (ctypes.c_double * 11)()
+ms = (ctypes.c_double * 12)()
 _lib.call("pf_cg_profile", plan.handle, _lib.ptr(k), _lib.ptr(b), 4, 2, _lib.ptr(plan.workspace), _lib.ptr(plan.mg_workspace), ms, plan.stream)
 print([round(v, 4) for v in ms])
