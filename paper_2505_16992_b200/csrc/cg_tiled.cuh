@@ -15,14 +15,16 @@
 // pass) reads P[(it & 1) ^ 1] and writes P[it & 1]; the first iteration
 // forms p' = z - zbar (the reference's initial direction) and reads no p.
 
-constexpr int kCgArr = 4;  // z, p, wy, wz
+constexpr int kCgArr = 4;     // z, p, wy, wz
+constexpr int kCgStages = 3;  // raw planes in flight (a light pass)
 struct CgTileSmem {
-  double raw[2][kCgArr][kTY + 2][kTZ + 2];
+  double raw[kCgStages][kCgArr][kTY + 2][kTZ + 2];
   double g[2][kTY + 2][kTZ + 2];  // p' of planes x & 1
 };
 constexpr size_t kCgTileSmem = sizeof(CgTileSmem);
+constexpr int kCgMinB = 4;    // CTAs per SM (36 KB of shared memory each)
 
-__global__ void __launch_bounds__(kTileThreads, 2)
+__global__ void __launch_bounds__(kTileThreads, kCgMinB)
     k_cg_spmv_pt(TileGeo tg, MgLevel L, const double *__restrict__ z,
                  double *P0, double *P1, double *__restrict__ q,
                  SolverState *st, double *partials, unsigned *counter) {
@@ -92,18 +94,19 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     } else {
       halo_cell = false;
     }
+    auto rslot = [](int32_t x) { return (x + kCgStages) % kCgStages; };
     auto issue_plane = [&](int32_t x) {
-      const int b = x & 1;
+      const int b = rslot(x);
       issue(b, x, y, zc, ty + 1, tz + 1);
       if (halo_cell) issue(b, x, hy, hz, sy_, sz_);
       cp_async_commit();
     };
     // p' of plane x (tile + halo) into g buffer x & 1; own value returned
     auto convert = [&](int32_t x) {
-      const int b = x & 1;
+      const int b = rslot(x), gb2 = x & 1;
       const double pc = pval(b, ty + 1, tz + 1);
-      sm.g[b][ty + 1][tz + 1] = pc;
-      if (halo_cell) sm.g[b][sy_][sz_] = pval(b, sy_, sz_);
+      sm.g[gb2][ty + 1][tz + 1] = pc;
+      if (halo_cell) sm.g[gb2][sy_][sz_] = pval(b, sy_, sz_);
       return pc;
     };
     // X face weight of plane x at the own column (0 outside a walled box)
@@ -113,31 +116,35 @@ __global__ void __launch_bounds__(kTileThreads, 2)
       return ok ? __ldg(wx + (int64_t)gx * sX + (int64_t)y * sY + zc) : 0.0;
     };
 
-    __syncthreads();  // the previous tile is done with both buffers
+    __syncthreads();  // the previous tile is done with every buffer
     double wxm = wx_at(xs - 1);
-    issue_plane(xs - 1);
-    issue_plane(xs);
-    cp_async_wait_all();
+    for (int k = 0; k < kCgStages; ++k) {
+      if (xs - 1 + k <= xe) issue_plane(xs - 1 + k);
+      else cp_async_commit();
+    }
+    cp_async_wait<kCgStages - 2>();
     __syncthreads();
-    double pm = pval((xs - 1) & 1, ty + 1, tz + 1);
+    double pm = pval(rslot(xs - 1), ty + 1, tz + 1);
     double pc = convert(xs);
-    __syncthreads();  // raw buffer (xs - 1) & 1 is free again
-    issue_plane(xs + 1);
+    __syncthreads();  // raw slot of plane xs - 1 is free again
+    if (xs + kCgStages - 1 <= xe) issue_plane(xs + kCgStages - 1);
+    else cp_async_commit();
     for (int32_t x = xs; x < xe; ++x) {
       const int64_t i = (int64_t)x * sX + (int64_t)y * sY + zc;
       const double wxc = __ldg(wx + i);
-      const int gb = x & 1;
+      const int gb = x & 1, rb = rslot(x);
       // this plane's Y / Z weights of the own cell and its -y / -z
       // neighbours: plane x landed before the previous barrier, and its raw
-      // slot is refilled (plane x + 2) only after the next one
-      const double wyp = sm.raw[gb][2][ty + 1][tz + 1];
-      const double wym = sm.raw[gb][2][ty][tz + 1];
-      const double wzp = sm.raw[gb][3][ty + 1][tz + 1];
-      const double wzm = sm.raw[gb][3][ty + 1][tz];
-      cp_async_wait_all();  // my copies of plane x + 1 have landed
-      __syncthreads();      // everyone's have; p' of plane x is complete
+      // slot is refilled only after the next one
+      const double wyp = sm.raw[rb][2][ty + 1][tz + 1];
+      const double wym = sm.raw[rb][2][ty][tz + 1];
+      const double wzp = sm.raw[rb][3][ty + 1][tz + 1];
+      const double wzm = sm.raw[rb][3][ty + 1][tz];
+      cp_async_wait<kCgStages - 2>();  // my copies of plane x + 1 landed
+      __syncthreads();  // everyone's have; p' of plane x is complete
       const double pn = convert(x + 1);
-      if (x + 2 <= xe) issue_plane(x + 2);
+      if (x + kCgStages <= xe) issue_plane(x + kCgStages);
+      else cp_async_commit();
       const double qi = wxc * (pc - pn) + wxm * (pc - pm) +
                         wyp * (pc - sm.g[gb][ty + 2][tz + 1]) +
                         wym * (pc - sm.g[gb][ty][tz + 1]) +

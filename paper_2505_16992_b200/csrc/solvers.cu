@@ -1313,8 +1313,25 @@ bool cg_tiled(const Plan &pl, const MgHierarchy *mg, TileGeo &tg) {
   static const bool off = getenv("PF_NO_TILED_CG") != nullptr;
   if (off || pl.slab || !mg || !tile_geo_dim(pl, pl.d.dim, tg)) return false;
   const MgLevel &L = mg->lv[0];
-  return L.sx == tg.X && L.sy == tg.Y && L.sz == tg.Z && L.px == tg.px &&
-         L.pz == tg.pz && !tg.py;
+  if (!(L.sx == tg.X && L.sy == tg.Y && L.sz == tg.Z && L.px == tg.px &&
+        L.pz == tg.pz && !tg.py))
+    return false;
+  // X chunks for kCgMinB resident CTAs per SM (as tile_geo does for two)
+  const int32_t nx = tg.x1 - tg.x0;
+  const int64_t R = (int64_t)kCgMinB * pl.num_sms;
+  const int64_t ncols = (int64_t)tg.ty_tiles * tg.tz_tiles;
+  int64_t best = -1;
+  for (int32_t xc = 1; xc <= std::max(1, nx); ++xc) {
+    const int64_t tiles = ncols * ((nx + xc - 1) / xc);
+    const int64_t cost = (tiles + R - 1) / R * (xc + 2);
+    if (best < 0 || cost <= best) {
+      best = cost;
+      tg.xc = xc;
+    }
+  }
+  tg.chunks = (nx + tg.xc - 1) / tg.xc;
+  tg.ntiles = tg.ty_tiles * tg.tz_tiles * tg.chunks;
+  return true;
 }
 
 void launch_cg_spmv_pt(const TileGeo &tg, const Plan &pl, const MgLevel &L,
@@ -1327,9 +1344,10 @@ void launch_cg_spmv_pt(const TileGeo &tg, const Plan &pl, const MgLevel &L,
                          (int)kCgTileSmem);
   });
   count_launch();
-  k_cg_spmv_pt<<<std::min(tg.ntiles, pl.red_blocks), kTileThreads,
-                 kCgTileSmem, s>>>(tg, L, z, p0, p1, q, st, w.partials,
-                                   w.counters);
+  k_cg_spmv_pt<<<std::min(tg.ntiles, std::min(pl.red_blocks,
+                                              kCgMinB * pl.num_sms)),
+                 kTileThreads, kCgTileSmem, s>>>(tg, L, z, p0, p1, q, st,
+                                                 w.partials, w.counters);
 }
 
 // one multigrid-preconditioned CG iteration on workspace buffers only
