@@ -348,6 +348,28 @@ def workload_config(args):
 # clocks
 
 
+def wait_for_idle_gpu(index, timeout_s=60.0):
+    """Other processes on this GPU (e.g. a test run's stragglers) would share
+    its SMs and HBM during the timed region: wait up to timeout_s for them
+    to leave.  Returns the PIDs still there (reported on the line)."""
+    me = os.getpid()
+    t0 = time.time()
+    others = []
+    while True:
+        try:
+            out = subprocess.run(
+                ["nvidia-smi", "--query-compute-apps=pid", "--format=csv,noheader",
+                 "-i", str(index)], capture_output=True, text=True,
+                timeout=10).stdout
+            others = [int(x) for x in out.split() if x.strip().isdigit()
+                      and int(x) != me]
+        except (OSError, subprocess.SubprocessError, ValueError):
+            return []
+        if not others or time.time() - t0 > timeout_s:
+            return others
+        time.sleep(1.0)
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled every 250 ms by a reader
     thread.  start() returns once the first sample has arrived, so the
@@ -680,6 +702,7 @@ def run_c5train(args, world, rank, local, dev):
     for _ in range(args.warmup):
         tstep()
     lib = _lib.load()
+    busy = wait_for_idle_gpu(local) if world == 1 else []
     clocks = ClockSampler(local)
     clocks.start()
     if world > 1:
@@ -916,6 +939,7 @@ def main():
         stats[k] = 0
 
     lib = _lib.load()
+    busy = wait_for_idle_gpu(local) if world == 1 else []
     clocks = ClockSampler(local)
     clocks.start()
     if world > 1:
@@ -1115,6 +1139,8 @@ def main():
             "gpu_launches": int(launches),
             "iterations_per_step": it_per_step,
         }
+        if busy:
+            line["other_gpu_processes"] = busy
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
