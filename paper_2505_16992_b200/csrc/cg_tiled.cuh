@@ -24,17 +24,25 @@ struct CgTileSmem {
 constexpr size_t kCgTileSmem = sizeof(CgTileSmem);
 constexpr int kCgMinB = 4;    // CTAs per SM (36 KB of shared memory each)
 
+// MODE 0: the fused direction update + SpMV above.  The same tiled face
+// stencil also forms the CG setup residual (MODE 1: r = bp - K x, sum r ->
+// the zero-mean projection; k_cg_resid_faces) and the true-residual
+// verification (MODE 2: |bp - K x|, S/linalg.py:236-239;
+// k_cg_true_res_faces): z is then x, P0 / q are bp / r.
+template <int MODE>
 __global__ void __launch_bounds__(kTileThreads, kCgMinB)
-    k_cg_spmv_pt(TileGeo tg, MgLevel L, const double *__restrict__ z,
-                 double *P0, double *P1, double *__restrict__ q,
-                 SolverState *st, double *partials, unsigned *counter) {
-  if (st->all_done) return;
+    k_cg_tiled(TileGeo tg, MgLevel L, const double *__restrict__ z,
+               double *P0, double *P1, double *__restrict__ q,
+               SolverState *st, double *partials, unsigned *counter, Rng rg) {
+  if (MODE != 2 && st->all_done) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CgTileSmem &sm = *reinterpret_cast<CgTileSmem *>(smem_raw);
   const CompState &cs = st->c[0];
   const int it = cs.iter;
-  const bool first = it == 0;
-  const double beta = first ? 0.0 : cs.beta, zbar = cs.zbar;
+  const bool first = MODE != 0 || it == 0;
+  const double beta = first ? 0.0 : cs.beta;
+  const double zbar = MODE == 0 ? cs.zbar : 0.0;
+  const double *__restrict__ bp = P0;
   const double *__restrict__ pold = (it & 1) ? P0 : P1;
   double *__restrict__ pnew = (it & 1) ? P1 : P0;
   const double *__restrict__ wx = L.wx;
@@ -150,9 +158,19 @@ __global__ void __launch_bounds__(kTileThreads, kCgMinB)
                         wym * (pc - sm.g[gb][ty][tz + 1]) +
                         wzp * (pc - sm.g[gb][ty + 1][tz + 2]) +
                         wzm * (pc - sm.g[gb][ty + 1][tz]);
-      pnew[i] = pc;
-      q[i] = qi;
-      acc[0] += pc * qi;
+      if (MODE == 0) {
+        pnew[i] = pc;
+        q[i] = qi;
+        acc[0] += pc * qi;
+      } else {
+        const double ri = bp[i] - qi;
+        if (MODE == 1) {
+          q[i] = ri;
+          acc[0] += ri;
+        } else {
+          acc[0] += ri * ri;
+        }
+      }
       pm = pc;
       pc = pn;
       wxm = wxc;
@@ -160,7 +178,16 @@ __global__ void __launch_bounds__(kTileThreads, kCgMinB)
     cp_async_wait_all();
   }
   double tot[1];
-  if (grid_reduce<1>(acc, partials, counter, tot)) {
+  if (!grid_reduce<1>(acc, partials, counter, tot)) return;
+  if (MODE == 1) {
+    st->c[0].rmean = st->zero_mean ? tot[0] / rg.ng : 0.0;
+    return;
+  }
+  if (MODE == 2) {
+    st->c[0].true_res = sqrt(tot[0]);
+    return;
+  }
+  {
     CompState &c = st->c[0];
     c.iter += 1;
     const double pap = tot[0];

@@ -1334,20 +1334,26 @@ bool cg_tiled(const Plan &pl, const MgHierarchy *mg, TileGeo &tg) {
   return true;
 }
 
-void launch_cg_spmv_pt(const TileGeo &tg, const Plan &pl, const MgLevel &L,
-                       const double *z, double *p0, double *p1, double *q,
-                       SolverState *st, Workspace &w, cudaStream_t s) {
+template <int MODE>
+void launch_cg_tiled(const TileGeo &tg, const Plan &pl, const MgLevel &L,
+                     const double *z, double *p0, double *p1, double *q,
+                     SolverState *st, Workspace &w, cudaStream_t s) {
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(k_cg_spmv_pt,
+    cudaFuncSetAttribute(k_cg_tiled<MODE>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kCgTileSmem);
   });
   count_launch();
-  k_cg_spmv_pt<<<std::min(tg.ntiles, std::min(pl.red_blocks,
-                                              kCgMinB * pl.num_sms)),
-                 kTileThreads, kCgTileSmem, s>>>(tg, L, z, p0, p1, q, st,
-                                                 w.partials, w.counters);
+  k_cg_tiled<MODE><<<std::min(tg.ntiles, std::min(pl.red_blocks,
+                                                  kCgMinB * pl.num_sms)),
+                     kTileThreads, kCgTileSmem, s>>>(
+      tg, L, z, p0, p1, q, st, w.partials, w.counters, plan_range(pl));
+}
+void launch_cg_spmv_pt(const TileGeo &tg, const Plan &pl, const MgLevel &L,
+                       const double *z, double *p0, double *p1, double *q,
+                       SolverState *st, Workspace &w, cudaStream_t s) {
+  launch_cg_tiled<0>(tg, pl, L, z, p0, p1, q, st, w, s);
 }
 
 // one multigrid-preconditioned CG iteration on workspace buffers only
@@ -1471,8 +1477,13 @@ int cg_core_mg(const Plan &pl, const V &v, Workspace &w, SolverState *st,
   (void)a;
   launch(k_cg_reset, 1, 1, s, st, maxiter, 2, zero_mean, tol, 0);
   halo(pl, s, {{x, 1}});
-  launch(k_cg_resid_faces, gr, kBlock, s, mg->lv[0], rg, bp, (const double *)x,
-         r, st, w.partials, w.counters);
+  TileGeo tgr;
+  if (cg_tiled(pl, mg, tgr))
+    launch_cg_tiled<1>(tgr, pl, mg->lv[0], x, const_cast<double *>(bp), nullptr,
+                       r, st, w, s);
+  else
+    launch(k_cg_resid_faces, gr, kBlock, s, mg->lv[0], rg, bp,
+           (const double *)x, r, st, w.partials, w.counters);
   launch(k_cg_rproj, gr, kBlock, s, (const double *)nullptr, r, rg, st,
          w.partials, w.counters);
   const CgFuse fuse{st, w.partials, w.counters, 1};
@@ -1552,8 +1563,13 @@ int cg_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
                             cudaMemcpyDeviceToDevice, s));
     if (hs.c[0].converged && !hs.c[0].zero_rhs) {
       halo(pl, s, {{x, 1}});
-      launch(k_cg_true_res_faces, gr, kBlock, s, mg->lv[0], rg, bp,
-             (const double *)x, st, w.partials, w.counters);
+      TileGeo tgv;
+      if (cg_tiled(pl, mg, tgv))
+        launch_cg_tiled<2>(tgv, pl, mg->lv[0], x, const_cast<double *>(bp),
+                           nullptr, nullptr, st, w, s);
+      else
+        launch(k_cg_true_res_faces, gr, kBlock, s, mg->lv[0], rg, bp,
+               (const double *)x, st, w.partials, w.counters);
     }
     PF_LAUNCH_CHECK("mg-cg true residual");
     return read_state(pl, st, &hs, s);
