@@ -190,8 +190,7 @@ PF_API int pf_assemble_pressure(const pf_plan *plan, const double *c,
 PF_API int pf_h_stage(const pf_plan *plan, const double *c, const double *u_cur,
                const double *rhs, double *h_out, void *stream);
 
-/* b = divergence_rhs(h, bc), S/piso.py:415-428; the contravariant fluxes are
- * formed per face on the fly (flux_scratch: unused, may be null) */
+/* b = divergence_rhs(h, bc), S/piso.py:415-428 (flux_scratch (d, n)) */
 PF_API int pf_divergence_rhs(const pf_plan *plan, const double *h, const double *bc,
                       double *flux_scratch, double *b_out, void *stream);
 

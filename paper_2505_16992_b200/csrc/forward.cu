@@ -178,7 +178,6 @@ __global__ void __launch_bounds__(kBlock)
 // -------------------------------------------------------------------------
 // b = div_xi(h) with prescribed boundary fluxes  (S/piso.py:415-428)
 
-// `flux` is the velocity field u (d, n): U^a = J (T u)_a is formed per face
 template <class V>
 __device__ __forceinline__ double cell_divergence(const V &v,
                                                   int32_t i,
@@ -194,10 +193,8 @@ __device__ __forceinline__ double cell_divergence(const V &v,
     const double nsgn = (f & 1) ? 1.0 : -1.0;
     const Face fc = v.topo.face(cell, f);
     if (fc.nb >= 0) {
-      // the contravariant fluxes formed on the fly from the velocity (no
-      // separate flux pass; the same arithmetic as k_flux, so the same bits)
-      const double unb = v.flux(flux, fc.ax, fc.nb);
-      b += nsgn * (0.5 * (v.flux(flux, a, i) + (fc.neg ? -unb : unb)));
+      const double unb = flux[(int64_t)fc.ax * n + fc.nb];
+      b += nsgn * (0.5 * (flux[(int64_t)a * n + i] + (fc.neg ? -unb : unb)));
     }
   }
 #pragma unroll
@@ -419,13 +416,14 @@ extern "C" int pf_h_stage(const pf_plan *plan, const double *c,
 extern "C" int pf_divergence_rhs(const pf_plan *plan, const double *h,
                                  const double *bc, double *flux_scratch,
                                  double *b_out, void *stream) {
-  PF_REQUIRE(plan && h && b_out, "pf_divergence_rhs: null argument");
-  (void)flux_scratch;  // unused: the fluxes are formed on the fly
+  PF_REQUIRE(plan && h && flux_scratch && b_out,
+             "pf_divergence_rhs: null argument");
   PF_REQUIRE(bc || P(plan).d.m == 0, "pf_divergence_rhs: null bc");
   return dispatch(P(plan), [&](auto v) {
     halo(P(plan), S(stream), {{const_cast<double *>(h), decltype(v)::kDim}});
-    launch(k_divergence_rhs<decltype(v)>, grid_for(v.owned()), kBlock, S(stream),
-        v, h, bc, b_out);
+    launch(k_flux<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, h, flux_scratch);
+    launch(k_divergence_rhs<decltype(v)>, grid_for(v.owned()), kBlock, S(stream), 
+        v, flux_scratch, bc, b_out);
     PF_LAUNCH_CHECK("k_divergence_rhs");
     return PF_OK;
   });
@@ -453,15 +451,15 @@ extern "C" int pf_divergence_max(const pf_plan *plan, const double *u,
                                  const double *bc, double *flux_scratch,
                                  void *workspace, double *out_host,
                                  void *stream) {
-  PF_REQUIRE(plan && u && workspace && out_host,
+  PF_REQUIRE(plan && u && flux_scratch && workspace && out_host,
              "pf_divergence_max: null argument");
-  (void)flux_scratch;  // unused: the fluxes are formed on the fly
   const Plan &pl = P(plan);
   Workspace w = carve(workspace, pl.d.n, pl.d.dim);
   int rc = dispatch(pl, [&](auto v) {
     halo(pl, S(stream), {{const_cast<double *>(u), decltype(v)::kDim}});
+    launch(k_flux<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, u, flux_scratch);
     launch(k_divergence_max<decltype(v)>, red_grid(pl, v.owned()), kBlock,
-           S(stream), v, u, bc, w.partials, w.counters, w.scalars);
+           S(stream), v, flux_scratch, bc, w.partials, w.counters, w.scalars);
     PF_LAUNCH_CHECK("k_divergence_max");
     return PF_OK;
   });
