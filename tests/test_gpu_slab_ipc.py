@@ -20,9 +20,15 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out_path):
+def _worker(rank, world, port, out_path, production=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
                       CUDA_MODULE_LOADING="EAGER", PF_COMM_TIMEOUT_S="30")
+    if production:
+        # one process per GPU in production: the solver's CUDA graphs and
+        # unbounded batches between polls (conftest limits them for the
+        # in-process slab tests only)
+        os.environ.pop("PF_NO_GRAPHS", None)
+        os.environ.pop("PF_MAX_BATCH", None)
     import torch.distributed as dist
     from paper_2505_16992_b200 import adjoint, channel, mesh, piso, slab
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -69,12 +75,13 @@ def _worker(rank, world, port, out_path):
     dist.destroy_process_group()
 
 
-def test_slab_step_across_processes_ipc(tmp_path):
+@pytest.mark.parametrize("production", [False, True])
+def test_slab_step_across_processes_ipc(tmp_path, production):
     import torch.multiprocessing as mp
     out = str(tmp_path / "ipc.npz")
     ctx = mp.get_context("spawn")
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, out))
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, out, production))
              for r in range(2)]
     for p in procs:
         p.start()
