@@ -1282,6 +1282,16 @@ using namespace pf;
 
 static cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
 
+// PF_NO_SPECULATIVE=1: close a solve (finish, true residual) only after the
+// poll that saw it converge (an A/B switch for the speculative close)
+static bool speculative_close() {
+  static const bool on = [] {
+    const char *e = getenv("PF_NO_SPECULATIVE");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 static int read_state(const Plan &pl, SolverState *dev, SolverState *host,
                       cudaStream_t s) {
   return d2h(pl, host, dev, sizeof(SolverState), s);
@@ -1465,9 +1475,9 @@ template <class V>
 int cg_core_mg(const Plan &pl, const V &v, Workspace &w, SolverState *st,
                SolverState &hs, const double *a, const double *bp, double *x,
                double tol, int maxiter, int zero_mean, const MgHierarchy *mg,
-               cudaStream_t s) {
+               cudaStream_t s, double *xout) {
   // x is the workspace copy of the warm start (the graph's buffers are all
-  // workspace-resident)
+  // workspace-resident); xout the caller's solution buffer
   const int32_t n = v.n;
   double *r = w.vecs, *p = w.vecs + n;
   double *z = w.vecs + 4 * (int64_t)n;
@@ -1508,15 +1518,26 @@ int cg_core_mg(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     rc = mg_graph(pl, w, st, mg, x, &exec, &nk);
     if (rc) return rc;
   }
+  auto close = [&]() {
+    launch(k_cg_finish, ge, kBlock, s, x, rg, st);
+    PF_CUDA(cudaMemcpyAsync(xout, x, sizeof(double) * n,
+                            cudaMemcpyDeviceToDevice, s));
+    halo(pl, s, {{xout, 1}});
+    TileGeo tgv;
+    if (cg_tiled(pl, mg, tgv))
+      launch_cg_tiled<2>(tgv, pl, mg->lv[0], xout, const_cast<double *>(bp),
+                         nullptr, nullptr, st, w, s);
+    else
+      launch(k_cg_true_res_faces, gr, kBlock, s, mg->lv[0], rg, bp,
+             (const double *)xout, st, w.partials, w.counters);
+    PF_LAUNCH_CHECK("mg-cg close");
+    return PF_OK;
+  };
   // the first batch goes out without a poll (its kernels return at once
   // when the setup already converged): one host round trip per batch
   int launched = 0;
   for (;;) {
-    if (launched >= maxiter) {  // maxiter <= 0: no iteration at all
-      rc = read_state(pl, st, &hs, s);
-      if (rc) return rc;
-      break;
-    }
+    if (launched >= maxiter) break;  // maxiter <= 0: no iteration at all
     int b = std::min(next_batch(launched, 0), maxiter - launched);
     b = std::max(1, (b + kGraphIters - 1) / kGraphIters);
     for (int k = 0; k < b; ++k) {
@@ -1529,14 +1550,22 @@ int cg_core_mg(const Plan &pl, const V &v, Workspace &w, SolverState *st,
       }
     }
     launched += b * kGraphIters;
+    const bool spec = speculative_close();
+    // speculative close behind the batch (idempotent until a batch
+    // converges, and the loop stops at the first that does): the zero-mean
+    // projection of x, the copy out and the true-residual verification, so
+    // a solve whose first batch converges costs one host round trip
+    if (spec) close();
     rc = read_state(pl, st, &hs, s);
     if (!rc) rc = comm_check(pl, s);
     if (rc) return rc;
-    if (hs.all_done || launched >= maxiter) break;
+    if (hs.all_done || launched >= maxiter) {
+      if (spec) return PF_OK;
+      break;
+    }
   }
-  launch(k_cg_finish, ge, kBlock, s, x, rg, st);
-  PF_LAUNCH_CHECK("mg-cg finish");
-  return PF_OK;
+  close();
+  return read_state(pl, st, &hs, s);
 }
 
 template <class V>
@@ -1556,23 +1585,10 @@ int cg_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     double *xw = w.vecs + 5 * (int64_t)n;
     PF_CUDA(cudaMemcpyAsync(xw, x, sizeof(double) * n,
                             cudaMemcpyDeviceToDevice, s));
-    int rc = cg_core_mg(pl, v, w, st, hs, a, bp, xw, tol, maxiter, zero_mean,
-                        mg, s);
-    if (rc) return rc;
-    PF_CUDA(cudaMemcpyAsync(x, xw, sizeof(double) * n,
-                            cudaMemcpyDeviceToDevice, s));
-    if (hs.c[0].converged && !hs.c[0].zero_rhs) {
-      halo(pl, s, {{x, 1}});
-      TileGeo tgv;
-      if (cg_tiled(pl, mg, tgv))
-        launch_cg_tiled<2>(tgv, pl, mg->lv[0], x, const_cast<double *>(bp),
-                           nullptr, nullptr, st, w, s);
-      else
-        launch(k_cg_true_res_faces, gr, kBlock, s, mg->lv[0], rg, bp,
-               (const double *)x, st, w.partials, w.counters);
-    }
-    PF_LAUNCH_CHECK("mg-cg true residual");
-    return read_state(pl, st, &hs, s);
+    // the close (projection, copy back, true residual) rides behind each
+    // batch inside cg_core_mg; hs is read after it
+    return cg_core_mg(pl, v, w, st, hs, a, bp, xw, tol, maxiter, zero_mean,
+                      mg, s, x);
   }
   launch(k_cg_reset, 1, 1, s, st, maxiter, precond, zero_mean, tol, 0);
   halo(pl, s, {{x, 1}});
@@ -2070,6 +2086,20 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     }
     PF_LAUNCH_CHECK("bicgstab iterations");
     launched += bsz;
+    if (!nm && speculative_close()) {
+      // speculative close: the finish and the true-residual verification
+      // go out behind the batch (both idempotent), so a batch sized right
+      // by the hint costs one host round trip for the whole solve
+      launch(k_bi_finish, ge, kBlock, s, x, n, rg, st);
+      halo(pl, s, {{x, ncomp}});
+      if (tinit)
+        launch_tiled<kTrans, 3>(tg, tgrid, s, a, bv, 0, (int64_t)n, st, w, x,
+                                b, ncomp);
+      else
+        launch(k_true_res<V>, gr, kBlock, s, v, a, kTrans ? 1 : 0, ncomp, b,
+               x, st, w.partials, w.counters);
+      PF_LAUNCH_CHECK("bicgstab finish");
+    }
     int rc = read_state(pl, st, &hs, s);
     if (!rc) rc = comm_check(pl, s);
     if (rc) return rc;
@@ -2080,6 +2110,8 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     for (int q = 0; q < ncomp; ++q) lock = std::max(lock, (int)hs.c[q].iter);
     pl.bi_hint[kTrans ? 1 : 0] = lock;
   }
+  // the speculative close already ran behind the last batch
+  if (!nm && launched > 0 && speculative_close()) return PF_OK;
   if (nm) {
     // the last iteration's x/r update (a merged pass whose pv part goes
     // unused; it returns at once when a poll already saw convergence)
