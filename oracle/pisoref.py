@@ -252,9 +252,13 @@ def solve_pressure_exact(dom, k_st, b):
 
 
 def cg(dom, st, b, x0=None, tol=1e-8, maxiter=None, precond="jacobi",
-       zero_mean=True):
+       zero_mean=True, variant="classic"):
     """Restatement of cg_solve/_cg_core/_run_with_fallback
-    (S/linalg.py:136-170, 215-273).  Returns (x, converged, iterations)."""
+    (S/linalg.py:136-170, 215-273).  Returns (x, converged, iterations).
+    variant="single": the product's single-reduction form of the same
+    iteration (Chronopoulos & Gear: w = K z carried alongside, the step
+    length from r.z and z.w of one pass; same iterates in exact
+    arithmetic), checked against the classic loop."""
     n = dom.n
     if maxiter is None:
         maxiter = max(200, 40 * int(round(n ** 0.5)))
@@ -297,6 +301,51 @@ def cg(dom, st, b, x0=None, tol=1e-8, maxiter=None, precond="jacobi",
             rz = rzn
         return x, False, mi
 
+    def core_single(x, pc, mi):
+        def M(r):
+            z = r / st[0] if pc else r.copy()
+            return z - z.mean() if zero_mean else z
+
+        def K(v):
+            return stencil_matvec(dom, st, v)
+        r = b - K(x)
+        if zero_mean:
+            r -= r.mean()
+        if np.linalg.norm(r) <= tol_abs:
+            return x, True, 0
+        z = M(r)
+        w = K(z)
+        g, d = float(r @ z), float(z @ w)
+        if not np.isfinite(d) or abs(d) < np.finfo(float).tiny:
+            return x, False, 0
+        al, be = g / d, 0.0
+        p, s_ = np.zeros(n), np.zeros(n)
+        for it in range(1, mi + 1):
+            p = z + be * p
+            s_ = w + be * s_
+            x = x + al * p
+            r = r - al * s_
+            z = M(r)
+            w = K(z)
+            # one reduction: |r|, r.z, z.w
+            res, gn, d = np.linalg.norm(r), float(r @ z), float(z @ w)
+            if res <= tol_abs:
+                if zero_mean:
+                    x = x - x.mean()
+                return x, True, it
+            if it >= mi:
+                break
+            if not np.isfinite(gn) or g == 0.0:
+                return x, False, it
+            be = gn / g
+            pap = d - be * gn / al
+            if not np.isfinite(pap) or abs(pap) < np.finfo(float).tiny:
+                return x, False, it
+            al, g = gn / pap, gn
+        return x, False, mi
+
+    if variant == "single":
+        core = core_single
     x = np.zeros(n) if x0 is None else x0.copy()
     x, ok, it = core(x, precond is not None, maxiter)
     if ok:

@@ -59,6 +59,10 @@ struct CgFuse {
   double *partials;
   unsigned *counter;
   int initial;
+  // st null: a reduction of the caller's follows the application on the
+  // stream (k_cg1_spmv), which every rank reaches only after its inverse
+  // transposes' peer loads -- the spectral closing barrier is implied
+  int caller_closes = 0;
 };
 
 }  // namespace pf

@@ -1316,12 +1316,37 @@ int next_batch(int done_iters, int hint) {
 
 bool tile_geo_dim(const Plan &pl, int dim, TileGeo &tg);
 
+// Pressure CG variant (k_cg1_*): 0 the classic loop (three fused reductions
+// per iteration), 1 Chronopoulos-Gear with one reduction per iteration (the
+// residual norm rides with r.z and z.w, so convergence is seen one
+// preconditioner application late), 2 the same recurrence with the norm
+// reduced in the update pass (two reductions, no extra application).  Every
+// reduction is a cross-rank synchronisation on slab plans, which default to
+// 2 (measured: the warm-started solves converge in one or two iterations,
+// where variant 1's extra application outweighs the synchronisation it
+// saves).  PF_CG_VARIANT=classic|single|split overrides; non-classic on one
+// device is a test setting.
+int cg_variant(const Plan &pl) {
+  static const int env = [] {
+    const char *e = getenv("PF_CG_VARIANT");
+    if (!e) return -1;
+    if (!strcmp(e, "classic")) return 0;
+    if (!strcmp(e, "single")) return 1;
+    if (!strcmp(e, "split")) return 2;
+    return -1;
+  }();
+  return env >= 0 ? env : pl.slab ? 2 : 0;
+}
+bool cg_single(const Plan &pl) { return cg_variant(pl) != 0; }
+
 // The fused direction update + SpMV on tiles (cg_tiled.cuh) applies on
 // single-device 3D boxes whose level-0 face form is laid out as the box
 // (PF_NO_TILED_CG=1: the per-cell gather SpMV and a separate update)
 bool cg_tiled(const Plan &pl, const MgHierarchy *mg, TileGeo &tg) {
   static const bool off = getenv("PF_NO_TILED_CG") != nullptr;
-  if (off || pl.slab || !mg || !tile_geo_dim(pl, pl.d.dim, tg)) return false;
+  if (off || pl.slab || cg_single(pl) || !mg ||
+      !tile_geo_dim(pl, pl.d.dim, tg))
+    return false;
   const MgLevel &L = mg->lv[0];
   if (!(L.sx == tg.X && L.sy == tg.Y && L.sz == tg.Z && L.px == tg.px &&
         L.pz == tg.pz && !tg.py))
@@ -1367,6 +1392,151 @@ void launch_cg_spmv_pt(const TileGeo &tg, const Plan &pl, const MgLevel &L,
 }
 
 // one multigrid-preconditioned CG iteration on workspace buffers only
+// ---------------------------------------------------------------------------
+// Single-reduction CG (Chronopoulos & Gear 1989): the reference's iterates
+// (S/linalg.py:136-170) in exact arithmetic, with w = K z carried alongside
+// so that the next step length follows from sums of one pass:
+//
+//   p = (z - zbar) + beta p      s = w + beta s   (= K p by linearity)
+//   x += alpha p                 r -= alpha s
+//   z = M r                      w = K z
+//   gamma = r.(z - zbar)         delta = (z - zbar).w
+//   beta = gamma / gamma_old     alpha = gamma / (delta - beta gamma / alpha_old)
+//
+// (z - zbar).w uses K 1 = 0 (face form, any walls): K (z - zbar) = K z.  The
+// residual norm of the update rides in the same reduction, so convergence
+// is seen one preconditioner application late; x is already the converged
+// iterate then (the count reported is the reference's).
+
+__device__ __forceinline__ void cg1_fail(SolverState *st) {
+  CompState &c = st->c[0];
+  c.fail = 1;
+  c.done = 1;
+  st->all_done = 1;
+}
+
+// w = K z and the six sums: r.r, sum z, r.z, sum r, z.w, sum w.  check: the
+// residual test of the update before this pass happens here (variant 1);
+// otherwise the update pass made it (variant 2)
+__global__ void __launch_bounds__(kBlock)
+    k_cg1_spmv(MgLevel L, Rng rg, const double *__restrict__ z,
+               const double *__restrict__ r, double *__restrict__ w,
+               int initial, int check, SolverState *st, double *partials,
+               unsigned *counter) {
+  if (st->all_done) return;
+  double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  RANGE_LOOP(i, rg) {
+    const Cell3 c = decode(L, i);
+    const double wi = kx(nbhd(L, c), i, z);
+    const double zi = z[i], ri = r[i];
+    w[i] = wi;
+    acc[0] += ri * ri;
+    acc[1] += zi;
+    acc[2] += ri * zi;
+    acc[3] += ri;
+    acc[4] += zi * wi;
+    acc[5] += wi;
+  }
+  double tot[6];
+  if (!grid_reduce<6>(acc, partials, counter, tot)) return;
+  CompState &c = st->c[0];
+  if (!initial && check) {
+    // the update before this pass was iteration c.iter + 1
+    c.iter += 1;
+    c.res = sqrt(tot[0]);
+    if (c.res <= c.tol_abs) {
+      c.converged = 1;
+      c.done = 1;
+      c.project_x = st->zero_mean;  // xmean: k_cg1_xmean in the close
+      st->all_done = 1;
+      return;
+    }
+    if (c.iter >= c.maxiter) {
+      c.done = 1;
+      st->all_done = 1;
+      return;
+    }
+  }
+  c.zbar = st->zero_mean ? tot[1] / rg.ng : 0.0;
+  const double g = tot[2] - c.zbar * tot[3];
+  const double d = tot[4] - c.zbar * tot[5];
+  if (initial) {
+    if (!pf::finite(d) || fabs(d) < DBL_MIN) return cg1_fail(st);
+    c.rz = g;
+    c.beta = 0.0;
+    c.alpha = g / d;
+    return;
+  }
+  if (!pf::finite(g) || c.rz == 0.0) return cg1_fail(st);
+  const double beta = g / c.rz;
+  const double pap = d - beta * g / c.alpha;  // p.K p of the next direction
+  if (!pf::finite(pap) || fabs(pap) < DBL_MIN) return cg1_fail(st);
+  c.beta = beta;
+  c.rz = g;
+  c.alpha = g / pap;
+}
+
+// p = (z - zbar) + beta p; s = w + beta s; x += alpha p; r -= alpha s (the
+// first iteration reads no p / s).  kCheck (variant 2): |r| and sum x of
+// the update, the residual test and the x mean of the projection here
+template <bool kCheck>
+__global__ void __launch_bounds__(kBlock)
+    k_cg1_update(const double *__restrict__ z, const double *__restrict__ w,
+                 double *__restrict__ p, double *__restrict__ sv,
+                 double *__restrict__ x, double *__restrict__ r, Rng rg,
+                 SolverState *st, double *partials, unsigned *counter) {
+  if (st->all_done) return;
+  const CompState &cs = st->c[0];
+  const bool first = cs.iter == 0;
+  const double beta = cs.beta, alpha = cs.alpha, zbar = cs.zbar;
+  double acc[2] = {0.0, 0.0};
+  RANGE_LOOP(i, rg) {
+    double pi = z[i] - zbar, si = w[i];
+    if (!first) {
+      pi += beta * p[i];
+      si += beta * sv[i];
+    }
+    p[i] = pi;
+    sv[i] = si;
+    const double xi = x[i] + alpha * pi, ri = r[i] - alpha * si;
+    x[i] = xi;
+    r[i] = ri;
+    if (kCheck) {
+      acc[0] += ri * ri;
+      acc[1] += xi;
+    }
+  }
+  if (!kCheck) return;
+  double tot[2];
+  if (!grid_reduce<2>(acc, partials, counter, tot)) return;
+  CompState &c = st->c[0];
+  c.iter += 1;
+  c.res = sqrt(tot[0]);
+  if (c.res <= c.tol_abs) {
+    c.converged = 1;
+    c.done = 1;
+    c.project_x = st->zero_mean;
+    c.xmean = st->zero_mean ? tot[1] / rg.ng : 0.0;
+    st->all_done = 1;
+  } else if (c.iter >= c.maxiter) {
+    c.done = 1;
+    st->all_done = 1;
+  }
+}
+
+// mean of the converged x for the zero-mean projection (variant 1; the
+// others get it from their update pass's reduction)
+__global__ void __launch_bounds__(kBlock)
+    k_cg1_xmean(const double *__restrict__ x, Rng rg, SolverState *st,
+                double *partials, unsigned *counter) {
+  if (!st->c[0].project_x) return;
+  double acc[1] = {0.0};
+  RANGE_LOOP(i, rg) acc[0] += x[i];
+  double tot[1];
+  if (grid_reduce<1>(acc, partials, counter, tot))
+    st->c[0].xmean = tot[0] / rg.ng;
+}
+
 void mg_iteration(const Plan &pl, Workspace &w, SolverState *st,
                   const MgHierarchy *mg, double *x, cudaStream_t s) {
   const int32_t n = (int32_t)pl.d.n;
@@ -1374,6 +1544,23 @@ void mg_iteration(const Plan &pl, Workspace &w, SolverState *st,
   double *z = w.vecs + 4 * (int64_t)n;
   const int ge = grid_for(pl.i1 - pl.i0), gr = std::min(ge, pl.red_blocks);
   const Rng rg = plan_range(pl);
+  if (const int var = cg_variant(pl)) {
+    double *wv = w.vecs + 7 * (int64_t)n;
+    if (var == 2)
+      launch(k_cg1_update<true>, gr, kBlock, s, (const double *)z,
+             (const double *)wv, p, q, x, r, rg, st, w.partials, w.counters);
+    else
+      launch(k_cg1_update<false>, ge, kBlock, s, (const double *)z,
+             (const double *)wv, p, q, x, r, rg, st, w.partials, w.counters);
+    const CgFuse closes{nullptr, nullptr, nullptr, 0, 1};
+    mg_apply(*mg, r, z, s, &st->all_done, nullptr, &closes, pl.red_blocks,
+             &pl);
+    halo(pl, s, {{z, 1}});
+    launch(k_cg1_spmv, gr, kBlock, s, mg->lv[0], rg, (const double *)z,
+           (const double *)r, wv, 0, var == 1 ? 1 : 0, st, w.partials,
+           w.counters);
+    return;
+  }
   TileGeo tg;
   if (cg_tiled(pl, mg, tg)) {
     double *p1 = w.vecs + 6 * (int64_t)n;
@@ -1433,6 +1620,7 @@ __global__ void __launch_bounds__(kBlock)
   if (grid_reduce<1>(acc, partials, counter, tot))
     st->c[0].true_res = sqrt(tot[0]);
 }
+
 
 constexpr int kGraphIters = 4;  // MG-PCG iterations per graph launch
 
@@ -1496,12 +1684,22 @@ int cg_core_mg(const Plan &pl, const V &v, Workspace &w, SolverState *st,
            (const double *)x, r, st, w.partials, w.counters);
   launch(k_cg_rproj, gr, kBlock, s, (const double *)nullptr, r, rg, st,
          w.partials, w.counters);
+  const bool single = cg_single(pl);
   const CgFuse fuse{st, w.partials, w.counters, 1};
-  int rc = mg_apply(*mg, r, z, s, done, nullptr, &fuse, pl.red_blocks, &pl);
+  const CgFuse closes{nullptr, nullptr, nullptr, 0, 1};  // k_cg1_spmv follows
+  int rc = mg_apply(*mg, r, z, s, done, nullptr, single ? &closes : &fuse,
+                    pl.red_blocks, &pl);
   if (rc) return rc;
+  if (single) {
+    // w0 = K z0 and the first step length (the update forms p0 = z0 - zbar)
+    halo(pl, s, {{z, 1}});
+    launch(k_cg1_spmv, gr, kBlock, s, mg->lv[0], rg, (const double *)z,
+           (const double *)r, w.vecs + 7 * (int64_t)n, 1, 0, st, w.partials,
+           w.counters);
+  }
   // the tiled iteration forms the first direction itself (p = z - zbar)
   TileGeo tgc;
-  if (!cg_tiled(pl, mg, tgc))
+  if (!single && !cg_tiled(pl, mg, tgc))
     launch(k_cg_pinit, ge, kBlock, s, (const double *)nullptr, r,
            (const double *)z, p, rg, st);
   PF_LAUNCH_CHECK("mg-cg setup");
@@ -1519,6 +1717,9 @@ int cg_core_mg(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     if (rc) return rc;
   }
   auto close = [&]() {
+    if (cg_variant(pl) == 1)
+      launch(k_cg1_xmean, gr, kBlock, s, (const double *)x, rg, st,
+             w.partials, w.counters);
     launch(k_cg_finish, ge, kBlock, s, x, rg, st);
     PF_CUDA(cudaMemcpyAsync(xout, x, sizeof(double) * n,
                             cudaMemcpyDeviceToDevice, s));

@@ -916,7 +916,7 @@ int spec_apply(const MgLevel &l0, const SpecPlan &sp, const double *r,
     else
       launch_smem(k_spec_inv_z<false>, zt, kFftThreads, zsm, s, sp, r, z,
                   CgFuse{nullptr, nullptr, nullptr, 0}, done);
-    barrier();
+    if (!(fuse && fuse->caller_closes)) barrier();
   }
   mark(5);
   PF_LAUNCH_CHECK("spec_apply");

@@ -98,6 +98,24 @@ def test_oracle_krylov_restatement_converges_to_exact():
     assert G.rel(y, t.u_star[:, 0]) < 1e-10
 
 
+@pytest.mark.parametrize("case", ["channel", "cavity8", "obstacle"])
+def test_oracle_single_reduction_cg_matches_classic(case):
+    """The product's single-reduction (Chronopoulos-Gear) pressure CG, the
+    slab plans' variant, restated in the oracle: the same iterates as the
+    reference's loop (S/linalg.py:136-170) up to rounding -- same iteration
+    count within one, same solution to the solve's accuracy."""
+    g, dom, tapes, outs = _oracle_rollout(case)
+    t = tapes[0]
+    b = -O.divergence_rhs(dom, t.correctors[0][1], t.bc)
+    for pc in ("jacobi", None):
+        xc, okc, itc = O.cg(dom, t.K, b, tol=1e-10, precond=pc)
+        xs, oks, its = O.cg(dom, t.K, b, tol=1e-10, precond=pc,
+                            variant="single")
+        assert okc and oks and abs(itc - its) <= 1, (pc, itc, its)
+        assert G.rel(xs, xc) < 1e-7, (pc, G.rel(xs, xc))
+        assert abs(xs.mean()) < 1e-12 * max(1.0, np.abs(xs).max())
+
+
 @pytest.mark.parametrize("transpose", [False, True])
 def test_oracle_neumann2_restatement(transpose):
     """The two-sweep Jacobi polynomial preconditioner of the product's
