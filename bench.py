@@ -352,6 +352,8 @@ def wait_for_idle_gpu(index, timeout_s=60.0):
     """Other processes on this GPU (e.g. a test run's stragglers) would share
     its SMs and HBM during the timed region: wait up to timeout_s for them
     to leave.  Returns the PIDs still there (reported on the line)."""
+    if os.environ.get("PF_NO_IDLE_WAIT") == "1":  # diagnosis only
+        return []
     me = os.getpid()
     t0 = time.time()
     others = []
@@ -395,6 +397,8 @@ class ClockSampler:
             self.first.set()
 
     def start(self):
+        if os.environ.get("PF_NO_CLOCK_SAMPLER") == "1":  # diagnosis only
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}",
@@ -933,8 +937,12 @@ def main():
         return new, g
 
     state = state0
+    # the warm-up holds the previous step's gradient as the timed loop does,
+    # so the caching allocator reaches its high-water mark here (a first
+    # cudaMalloc inside the timed loop stalled its first steps 30-140 ms)
+    grad = None
     for _ in range(args.warmup):
-        state, _ = step(state)
+        state, grad = step(state)
     for k in stats:
         stats[k] = 0
 
@@ -949,11 +957,43 @@ def main():
     l0 = lib.pf_launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    # per-step events (no synchronisation) and the host's issue times: a
+    # step that stalls shows whether the device or the host held it up
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    host_t = []
+    trace = os.environ.get("PF_TRACE_STEPS") == "1" and rank == 0
+    if trace:  # diagnosis only: per-call events (not a bench number)
+        _lib.TRACE = []
+        mem0 = torch.cuda.memory_stats(dev)
     e0.record()
-    for _ in range(args.steps):
+    t_host0 = time.perf_counter()
+    for k in range(args.steps):
         state, grad = step(state)
+        marks[k].record()
+        host_t.append(time.perf_counter())
     e1.record()
     torch.cuda.synchronize()
+    if trace:
+        rows = [(nm, 1e3 * (a - t_host0), 1e3 * (b - t_host0),
+                 e0.elapsed_time(x), e0.elapsed_time(y))
+                for nm, a, b, x, y in _lib.TRACE]
+        _lib.TRACE = None
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        with open(os.path.join(ROOT, "gpurun_out",
+                               f"trace_{os.getpid()}.json"), "w") as f:
+            mem1 = torch.cuda.memory_stats(dev)
+            json.dump({"rows": rows,
+                       "steps": [e0.elapsed_time(m) for m in marks],
+                       "mem": {k: [mem0.get(k), mem1.get(k)] for k in (
+                           "num_device_alloc", "num_device_free",
+                           "num_alloc_retries",
+                           "reserved_bytes.all.current")}}, f)
+    prev = e0
+    step_ms = []
+    for mk in marks:
+        step_ms.append(prev.elapsed_time(mk))
+        prev = mk
+    host_ms = [1e3 * (b - a) for a, b in zip([t_host0] + host_t[:-1], host_t)]
     launches = lib.pf_launch_count() - l0
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
@@ -987,7 +1027,12 @@ def main():
         return (st_ if st_.is_contiguous() else st_.contiguous()).reshape(-1)
 
     def pinned(m):
-        return torch.empty(m, dtype=torch.float64, pin_memory=True)
+        # touched once here: on the GPU boxes (virtual machines) a page's
+        # first touch faults through the hypervisor, which inside the timed
+        # loop stalled first steps by up to half a second
+        t = torch.empty(m, dtype=torch.float64, pin_memory=True)
+        t.zero_()
+        return t
 
     u_host = [pinned(nU) for _ in range(2)]
     p_host = [pinned(nP) for _ in range(2)]
@@ -1024,6 +1069,7 @@ def main():
         p_in = p_host[0].to(dev, non_blocking=True)
     bc_in, ev = bcs_in(0)
     t_state, n_state = state.t, state.step
+    e2e_marks = []
     for k in range(args.steps):
         main.wait_event(ev)
         for t in [u_in, p_in] + bc_in:
@@ -1069,8 +1115,9 @@ def main():
             bc_in, ev = bcs_in(slot)
         g = adj(tape)
         count(dg, g)
-        done_a = torch.cuda.Event()
+        done_a = torch.cuda.Event(enable_timing=True)
         done_a.record(main)
+        e2e_marks.append(done_a)
         s_out.wait_event(done_a)
         with torch.cuda.stream(s_out):
             gf = flat(g.u)
@@ -1081,6 +1128,10 @@ def main():
     e3.record(main)
     torch.cuda.synchronize()
     ms_e2e = e2.elapsed_time(e3)
+    e2e_step_ms, prev = [], e2
+    for mk in e2e_marks:
+        e2e_step_ms.append(round(prev.elapsed_time(mk), 3))
+        prev = mk
     if world > 1:
         t = torch.tensor([ms_e2e], device="cpu" if share_dev() else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -1139,6 +1190,10 @@ def main():
             "gpu_launches": int(launches),
             "iterations_per_step": it_per_step,
         }
+        line["step_ms"] = {
+            "device": [round(x, 3) for x in step_ms],
+            "host_issue": [round(x, 3) for x in host_ms],
+            "e2e_device": e2e_step_ms}
         if busy:
             line["other_gpu_processes"] = busy
         print(json.dumps(line))

@@ -204,6 +204,13 @@ PF_API int pf_correct_velocity(const pf_plan *plan, const double *h, const doubl
 PF_API int pf_divergence_max(const pf_plan *plan, const double *u, const double *bc,
                       double *flux_scratch, void *workspace, double *out_host,
                       void *stream);
+/* The same maximum written to the device scalar *out_dev without waiting
+ * (the step's diagnostics read it lazily: no host round trip between the
+ * forward step and the adjoint). */
+PF_API int pf_divergence_max_dev(const pf_plan *plan, const double *u,
+                                 const double *bc, double *flux_scratch,
+                                 void *workspace, double *out_dev,
+                                 void *stream);
 
 /* y = A x (transpose != 0: y = A^t x) for a stencil A, ncomp right-hand
  * sides of length n each -- SystemPattern.matvec, S/linalg.py:80-83 and

@@ -7,6 +7,7 @@ tensors; the stream is torch's current stream on the tensors' device.
 
 import ctypes
 import threading
+import time
 import os
 
 import torch
@@ -69,6 +70,8 @@ _SIGS = {
     "pf_correct_velocity": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr],
     "pf_divergence_max": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
                           ctypes.POINTER(c_dbl), c_ptr],
+    "pf_divergence_max_dev": [c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr,
+                              c_ptr],
     "pf_stencil_matvec": [c_ptr, c_ptr, c_int, c_int, c_ptr, c_ptr, c_ptr],
     "pf_cg_solve": [c_ptr, c_ptr, c_ptr, c_dbl, c_ptr, c_int, c_dbl, c_int,
                     c_int, c_int, c_ptr, c_ptr, ctypes.POINTER(SolverReportC),
@@ -167,6 +170,11 @@ def load(path=LIB_PATH):
     return lib
 
 
+# diagnosis: a list here collects (entry point, host start, host end,
+# device start event, device end event) of every call (tools/dev/trace.py)
+TRACE = None
+
+
 def call(name, *args):
     """Invoke an entry point; non-zero status raises LibraryError.  The
     tensors whose pointers were taken for this call (ptr) stay referenced
@@ -175,10 +183,19 @@ def call(name, *args):
     call, and the next temporary of the same argument list could reuse
     (and overwrite) it ahead of the kernel in stream order."""
     lib = load()
+    tr = TRACE
+    if tr is not None:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        h0 = time.perf_counter()
     try:
         rc = getattr(lib, name)(*args)
     finally:
         _keep.refs = []
+    if tr is not None:
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        tr.append((name, h0, time.perf_counter(), e0, e1))
     if rc != 0:
         msg = lib.pf_last_error().decode(errors="replace")
         raise LibraryError(f"{name} failed (status {rc}): {msg}")

@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double *const sm = reinterpret_cast<double *>(smem_raw);
   const int nc = st->ncomp;
-  bool act[3], pend[3];
+  bool act[3], pend[3], appl[3];
   // the iteration scalars live in shared memory (read where y is formed):
   // pv: beta, omega | st: alpha | x/r + pv: alpha, omega, beta
   double *const c0 = sm + kNmCo, *const c1 = sm + kNmCo + 3,
@@ -194,7 +194,9 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
                                   st->c[q].iter > 0 && !st->c[q].fail)
                                : !st->c[q].done);
     // x/r + pv: components that converged at s only take z += alpha p
-    pend[q] = kRpv && q < nc && st->c[q].pending;
+    // ... unless the light pass (k_nm_xr) behind the last poll made it
+    appl[q] = kRpv && q < nc && st->c[q].xr_applied;
+    pend[q] = kRpv && q < nc && st->c[q].pending && !appl[q];
   }
   if (threadIdx.x < 3) {
     const int q = threadIdx.x;
@@ -354,7 +356,7 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
             iq = nm_pbase(g, q) + own.off;
 #pragma unroll
             for (int c = 0; c < 3; ++c)
-              if (on(c) || pend[c]) zq[c] = g.zio[c][iq];
+              if ((on(c) && !appl[c]) || pend[c]) zq[c] = g.zio[c][iq];
           }
         }
         if (ghost1) {
@@ -404,7 +406,7 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
                 const double sv = rw[c * kNP] - al * rw[(3 + c) * kNP];
                 const double rn = sv - om * rw[(9 + c) * kNP];
                 g.rout[c][io] = rn;
-                g.zio[c][io] = zq[c] + (al * pp + om * sv);
+                if (!appl[c]) g.zio[c][io] = zq[c] + (al * pp + om * sv);
                 acc[3 + c] += rn * rn;
               } else {
                 g.zio[c][io] = zq[c] + al * pp;
@@ -539,7 +541,8 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
     int all = 1;
     for (int q = 0; q < nc; ++q) {
       CompState &c = st->c[q];
-      if (pend[q]) c.pending = 0;
+      c.pending = 0;  // applied here or by the light pass
+      c.xr_applied = 0;
       if (act[q]) {
         c.res = sqrt(tot[3 + q]);
         if (c.res <= c.tol_abs) {

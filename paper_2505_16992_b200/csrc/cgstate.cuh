@@ -14,7 +14,9 @@ struct CompState {
   int32_t iter, maxiter, done, converged, fail, zero_rhs, pending, active;
   // brk_next: rho_next or omega vanished -- a breakdown unless the update
   // that follows converges
-  int32_t project_x, brk_next, pad2[6];
+  // xr_applied: the Neumann-2 light pass (k_nm_xr) already made the x/r
+  // update the next merged pass would make
+  int32_t project_x, brk_next, xr_applied, pad2[5];
 };
 
 struct SolverState {

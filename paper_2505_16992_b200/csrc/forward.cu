@@ -467,6 +467,31 @@ extern "C" int pf_divergence_max(const pf_plan *plan, const double *u,
   return d2h(pl, out_host, w.scalars, sizeof(double), S(stream));
 }
 
+// the same into a device scalar, without waiting: the step's diagnostics
+// read it when asked, so no host round trip sits between the forward step
+// and the adjoint
+extern "C" int pf_divergence_max_dev(const pf_plan *plan, const double *u,
+                                     const double *bc, double *flux_scratch,
+                                     void *workspace, double *out_dev,
+                                     void *stream) {
+  PF_REQUIRE(plan && u && flux_scratch && workspace && out_dev,
+             "pf_divergence_max_dev: null argument");
+  const Plan &pl = P(plan);
+  Workspace w = carve(workspace, pl.d.n, pl.d.dim);
+  int rc = dispatch(pl, [&](auto v) {
+    halo(pl, S(stream), {{const_cast<double *>(u), decltype(v)::kDim}});
+    launch(k_flux<decltype(v)>, grid_for(v.n), kBlock, S(stream), v, u, flux_scratch);
+    launch(k_divergence_max<decltype(v)>, red_grid(pl, v.owned()), kBlock,
+           S(stream), v, flux_scratch, bc, w.partials, w.counters, w.scalars);
+    PF_LAUNCH_CHECK("k_divergence_max");
+    return PF_OK;
+  });
+  if (rc) return rc;
+  PF_CUDA(cudaMemcpyAsync(out_dev, w.scalars, sizeof(double),
+                          cudaMemcpyDeviceToDevice, S(stream)));
+  return PF_OK;
+}
+
 // ---------------------------------------------------------------------------
 // channel drivers (S/piso.py:512-546): adaptive_dt's CFL peak and the
 // per-step wall forcing, each one fused reduction

@@ -438,6 +438,7 @@ __global__ void k_bi_reset(SolverState *st, int ncomp, int maxiter,
     c.converged = c.active && c.zero_rhs;
     c.fail = 0;
     c.pending = 0;
+    c.xr_applied = 0;
     c.res = 0.0;
     c.true_res = 0.0;
     if (!c.done) all = 0;
@@ -913,6 +914,8 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
                const double *__restrict__ bin = nullptr, int nverify = 0,
                double *__restrict__ xout = nullptr) {
   if (MODE != 3 && MODE != 4 && st->all_done) return;
+  // the speculative close (nverify = 1) runs only once the solve ended
+  if (MODE == 4 && nverify && !st->all_done) return;
   // compile-time: a runtime branch here slows the transposed pass ~15 %
   constexpr bool fresh = MODE == 0 && kFirst;
   constexpr int K = MODE == 1 ? 9 : MODE == 2 ? 6 : 3;
@@ -1272,6 +1275,69 @@ __global__ void __launch_bounds__(kBlock)
 
 #include "bicg_nm.cuh"
 #include "cg_tiled.cuh"
+
+// Neumann-2 BiCGStab, behind a batch's last st pass: that iteration's x/r
+// update (z += alpha p + omega s, r' = s - omega t with s = r - alpha v;
+// converged-at-s components z += alpha p) and the residual test on r' --
+// the pointwise part of the merged pass that would follow (168 B/cell for
+// three components instead of the merged pass's stencil), so a batch sized
+// by the hint ends converged.  The next merged pass, if the solve goes on,
+// skips the update it would make (xr_applied) and repeats the same test.
+__global__ void __launch_bounds__(kBlock)
+    k_nm_xr(const double *__restrict__ r, const double *__restrict__ v,
+            const double *__restrict__ p, const double *__restrict__ t,
+            double *__restrict__ z, double *__restrict__ rout, int64_t n,
+            Rng rg, SolverState *st, double *partials, unsigned *counter) {
+  if (st->all_done) return;
+  const int nc = st->ncomp;
+  bool on[3], pend[3];
+  double al[3], om[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    on[q] = q < nc && !st->c[q].done;
+    pend[q] = q < nc && st->c[q].pending;
+    al[q] = q < nc ? st->c[q].alpha : 0.0;
+    om[q] = q < nc ? st->c[q].omega : 0.0;
+  }
+  double acc[3] = {0.0, 0.0, 0.0};
+  RANGE_LOOP(i, rg) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int64_t j = q * n + i;
+      if (on[q]) {
+        const double sv = r[j] - al[q] * v[j];
+        const double rn = sv - om[q] * t[j];
+        rout[j] = rn;
+        z[j] += al[q] * p[j] + om[q] * sv;
+        acc[q] += rn * rn;
+      } else if (pend[q]) {
+        z[j] += al[q] * p[j];
+      }
+    }
+  }
+  double tot[3];
+  if (!grid_reduce<3>(acc, partials, counter, tot)) return;
+  int all = 1;
+  for (int q = 0; q < nc; ++q) {
+    CompState &c = st->c[q];
+    if (on[q]) {
+      // the merged pass's terminal decisions (bicg_nm.cuh epilogue)
+      c.res = sqrt(tot[q]);
+      if (c.res <= c.tol_abs) {
+        c.converged = 1;
+        c.done = 1;
+      } else if (c.iter >= c.maxiter) {
+        c.done = 1;
+      } else if (c.brk_next) {
+        c.fail = 1;
+        c.done = 1;
+      }
+    }
+    if (on[q] || pend[q]) c.xr_applied = 1;
+    if (!c.done) all = 0;
+  }
+  st->all_done = all;
+}
 
 }  // namespace pf
 
@@ -2169,24 +2235,6 @@ void nm_iteration(const Plan &pl, const TileGeo &tgn, const TileGeo &tge,
                        nullptr, qg, nullptr, par);
 }
 
-// after `launched` iterations: the x/r update of the last one
-template <bool kTrans>
-void nm_finish(const Plan &pl, const TileGeo &tgn, const TileGeo &tge,
-               int ngrid, int egrid, cudaStream_t s, const double *a,
-               const BiVecs &bv, int launched, int64_t n, int ncomp,
-               SolverState *st, Workspace &w, double *qg) {
-  if (launched < 1) return;
-  const int i = launched, par = i & 1, rp = (i - 1) & 1;
-  halo(pl, s, {{bv.rb[rp], ncomp}, {bv.p[par], ncomp}, {bv.t, ncomp}});
-  if (qg) {
-    launch_nm<kTrans, 3>(tge, egrid, s, a, bv, par, n, st, w, 0, nullptr,
-                         nullptr, nullptr, qg, rp);
-    halo(pl, s, {{qg, ncomp}});
-  }
-  launch_nm<kTrans, 3>(tgn, ngrid, s, a, bv, par, n, st, w, 0, nullptr,
-                       nullptr, qg, nullptr, rp);
-}
-
 template <class V, bool kTrans>
 int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
             SolverState &hs, const double *a, const double *b, double *x,
@@ -2287,7 +2335,22 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     }
     PF_LAUNCH_CHECK("bicgstab iterations");
     launched += bsz;
-    if (!nm && speculative_close()) {
+    if (nm) {
+      // the last iteration's x/r update and residual test (k_nm_xr), then
+      // the speculative close x = x0 + M^-1 z (a one-stage stencil on the
+      // single-halo tiled pass, which skips itself unless the solve ended)
+      const int par = launched & 1, rp = (launched - 1) & 1;
+      launch(k_nm_xr, gr, kBlock, s, (const double *)bv.rb[rp],
+             (const double *)bv.v[par], (const double *)bv.p[par],
+             (const double *)bv.t, z, bv.rb[par], (int64_t)n, rg, st,
+             w.partials, w.counters);
+      if (speculative_close()) {
+        halo(pl, s, {{z, ncomp}});
+        launch_tiled<kTrans, 4>(tg, tgrid, s, a, bv, 0, (int64_t)n, st, w, z,
+                                nullptr, 1, 0, x);
+      }
+    }
+    if (speculative_close()) {
       // speculative close: the finish and the true-residual verification
       // go out behind the batch (both idempotent), so a batch sized right
       // by the hint costs one host round trip for the whole solve
@@ -2311,13 +2374,10 @@ int bi_core(const Plan &pl, const V &v, Workspace &w, SolverState *st,
     for (int q = 0; q < ncomp; ++q) lock = std::max(lock, (int)hs.c[q].iter);
     pl.bi_hint[kTrans ? 1 : 0] = lock;
   }
-  // the speculative close already ran behind the last batch
-  if (!nm && launched > 0 && speculative_close()) return PF_OK;
-  if (nm) {
-    // the last iteration's x/r update (a merged pass whose pv part goes
-    // unused; it returns at once when a poll already saw convergence)
-    nm_finish<kTrans>(pl, tgn, tge, ngrid, egrid, s, a, bv, launched,
-                      (int64_t)n, ncomp, st, w, qg);
+  // the speculative close already ran behind the last batch (a solve
+  // stopped by maxiter before its state said done closes here)
+  if (launched > 0 && speculative_close() && hs.all_done) return PF_OK;
+  if (nm && launched > 0) {
     // x = x0 + M^-1 z: a one-stage stencil, on the single-halo tiled pass
     halo(pl, s, {{z, ncomp}});
     launch_tiled<kTrans, 4>(tg, tgrid, s, a, bv, 0, (int64_t)n, st, w, z,

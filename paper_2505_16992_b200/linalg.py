@@ -63,7 +63,7 @@ def _global_n(plan):
 
 
 PRECOND_NONE, PRECOND_JACOBI, PRECOND_MG, PRECOND_NEUMANN2 = 0, 1, 2, 3
-_DEFAULT_MOM_PRECOND = os.environ.get("PF_MOMENTUM_PRECOND", "jacobi")
+_DEFAULT_MOM_PRECOND = os.environ.get("PF_MOMENTUM_PRECOND", "neumann2")
 
 
 def _precond_flag(precond):
@@ -144,10 +144,11 @@ def bicgstab_solve(plan, data, b, x0=None, tol=None, maxiter=None,
         x.copy_(x0.reshape(k, n))
     reps = (_lib.SolverReportC * k)()
     pc = _precond_flag(precond)
-    # auto / "ilu0": Jacobi, unless PF_MOMENTUM_PRECOND=neumann2.  The fused
-    # two-sweep polynomial halves the iterations (C4: 15 -> 8 per step) but
-    # its passes are latency-bound: same-box A/B, C4 step 34.8 ms vs 34.0
-    # ms with Jacobi (profiles/r2_ab_c4.txt); it stays selectable
+    # auto / "ilu0": the fused two-sweep Jacobi polynomial (Neumann-2) on
+    # tiled boxes (the library degrades it to Jacobi elsewhere): C4
+    # lock-step iterations 15 -> 8 per step; same-box A/B 31.0 ms vs 32.0
+    # ms with Jacobi (profiles/r2_nm_light.txt).  PF_MOMENTUM_PRECOND=jacobi
+    # selects Jacobi
     if pc == -1:
         pc = PRECOND_NEUMANN2 if _DEFAULT_MOM_PRECOND == "neumann2" \
             else PRECOND_JACOBI

@@ -124,8 +124,21 @@ class StepDiagnostics:
     momentum_iterations: int = 0
     pressure_iterations: int = 0
     div_contract: float = 0.0
-    div_wide_max: float = 0.0
+    # a float, or the device scalar pf_divergence_max_dev wrote (read on
+    # first access, so the step itself never waits for it)
+    _div_wide_max: object = 0.0
     reports: list = field(default_factory=list)
+
+    @property
+    def div_wide_max(self) -> float:
+        v = self._div_wide_max
+        if torch.is_tensor(v):
+            v = self._div_wide_max = float(v.item())
+        return v
+
+    @div_wide_max.setter
+    def div_wide_max(self, value):
+        self._div_wide_max = value
 
 
 @dataclass
@@ -576,11 +589,11 @@ def piso_step(domain, state, cfg, workspace=None, tape=None):
         u_cur = u_new
 
     diag.div_contract = last_resid
-    dmax = _lib.c_dbl()
-    _lib.call("pf_divergence_max", plan.handle, _lib.ptr(u_cur),
+    dmax = torch.empty((), dtype=F64, device=dev)
+    _lib.call("pf_divergence_max_dev", plan.handle, _lib.ptr(u_cur),
               _lib.ptr(bc), _lib.ptr(flux), _lib.ptr(plan.workspace),
-              _lib.ctypes.byref(dmax), hstream)
-    diag.div_wide_max = float(dmax.value)
+              _lib.ptr(dmax), hstream)
+    diag.div_wide_max = dmax
 
     bc_list = bc_views(plan, bc)
     if tape is not None:
