@@ -2167,10 +2167,14 @@ void launch_nm(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
     static std::set<const void *> done;
     {
       std::lock_guard<std::mutex> lock(mu);
-      if (done.insert(reinterpret_cast<const void *>(kernel)).second)
+      if (done.insert(reinterpret_cast<const void *>(kernel)).second) {
         cudaFuncSetAttribute(kernel,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)kNmSmem);
+        cudaFuncSetAttribute(kernel,
+                             cudaFuncAttributePreferredSharedMemoryCarveout,
+                             100);
+      }
     }
     count_launch();
     kernel<<<grid, kTileThreads, kNmSmem, s>>>(tg, g, st, w.partials,
@@ -2661,11 +2665,11 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
     TileGeo tg, tgn;
     const bool tiled = tile_geo(pl, v, tg);
     const int tgrid = tiled ? std::min(tg.ntiles, pl.red_blocks) : 0;
-    // the production preconditioner: Jacobi, or Neumann-2 where it runs
-    // when PF_MOMENTUM_PRECOND=neumann2 (the Python default follows it)
+    // the production preconditioner, as linalg.py picks it: Neumann-2 where
+    // its tiled passes run, Jacobi when PF_MOMENTUM_PRECOND=jacobi
     TileGeo tge;
     const char *mp = getenv("PF_MOMENTUM_PRECOND");
-    const bool nm = mp && std::string(mp) == "neumann2" &&
+    const bool nm = (!mp || std::string(mp) == "neumann2") &&
                     nm_geo(pl, v, tgn, &tge);
     const int ngrid = nm ? std::min(tgn.ntiles, nm_minb() * pl.num_sms) : 0;
     const int egrid = nm ? std::min(tge.ntiles, nm_minb() * pl.num_sms) : 0;
