@@ -54,16 +54,22 @@ constexpr int kNY = kTY + 4, kNZ = kTZ + 4;           // tile + 2-cell halo
 constexpr int kNP = kNY * kNZ;                         // 432 cells per plane
 constexpr int kNPairs = kNP / 2;                       // 216 Z-pairs
 constexpr int kNRing1 = (kTY + 2) * (kTZ + 2) - kTY * kTZ;  // 84 halo-1 cells
+constexpr int kNZ1 = kTZ + 2;                          // q1 row (halo 1)
+constexpr int kNP1 = (kTY + 2) * kNZ1;                 // 340 q1 cells
 static_assert(kNZ % 2 == 0 && kNPairs <= kTileThreads, "pair layout");
 
 // shared memory, in doubles: raw[13][kNP] (r, v, p, t x 3, 1/A) |
-// g1[3 slots][3][kNP] | q1[4 slots][3][kNP] | iteration scalars [3][3]
+// g1[3 slots][3][kNP] | q1[4 slots][3][kNP1] | iteration scalars [3][3]
+// (q1 lives on the tile + 1-cell halo only, 340 cells per plane: measured
+// C4 x/r + pv pass 1114 -> 937 us against the 432-cell layout.  A
+// three-slot q1 ring and per-pass raw buffers (100.6 / 90.2 / 79.8 KB)
+// were measured 1 % slower again.)
 // (q1 keeps four planes: stage 2 of plane q-3 reads q-4, q-3, q-2 while
 // stage 1 writes q-1, and reads its X neighbours from the ring)
 constexpr int kNmRawN = 13, kNmDi = 12;  // raw arrays; 1/A's slot
 constexpr int kNmRaw = 0, kNmG1 = kNmRawN * kNP, kNmQ1 = kNmG1 + 9 * kNP,
-              kNmCo = kNmQ1 + 12 * kNP, kNmEnd = kNmCo + 10;
-constexpr size_t kNmSmem = sizeof(double) * kNmEnd;   // 117,584 B
+              kNmCo = kNmQ1 + 12 * kNP1, kNmEnd = kNmCo + 10;
+constexpr size_t kNmSmem = sizeof(double) * kNmEnd;   // 108,752 B
 
 // halo-1 ring cell k (0..83) in plane coordinates
 __device__ __forceinline__ void nm_ring1(int k, int &sy, int &sz) {
@@ -209,6 +215,7 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
   const int tid = threadIdx.x;
   const int tz = tid % kTZ, ty = tid / kTZ;
   const int eo = (ty + 2) * kNZ + tz + 2;  // own cell's plane element
+  const int eo1 = (ty + 1) * kNZ1 + tz + 1;  // ... in the q1 layout
   // the Z-pair this thread loads and converts, the halo-1 cell it smooths
   const bool has_pair = tid < kNPairs;
   const int psy = tid / (kNZ / 2), psz = 2 * (tid % (kNZ / 2));
@@ -217,6 +224,7 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
   int r1y = 0, r1z = 0;
   if (has_r1) nm_ring1(tid, r1y, r1z);
   const int er = r1y * kNZ + r1z;
+  const int er1 = (r1y - 1) * kNZ1 + r1z - 1;
 
   double acc[K];
 #pragma unroll
@@ -289,8 +297,8 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
       // ring slots: g1 of planes q-3 / q-2 / q-1 and q1 of planes q-5 /
       // q-4 / q-3 / q-2 at the start of step q; rotated every step
       int g1a = kNmG1, g1b = g1a + 3 * kNP, g1c = g1b + 3 * kNP;
-      int q1a = kNmQ1, q1b = q1a + 3 * kNP, q1c = q1b + 3 * kNP,
-          q1d = q1c + 3 * kNP;
+      int q1a = kNmQ1, q1b = q1a + 3 * kNP1, q1c = q1b + 3 * kNP1,
+          q1d = q1c + 3 * kNP1;
       // own-cell y of planes q-3, q-2, q-1, q
       double ya[3] = {0, 0, 0}, yb[3] = {0, 0, 0}, yc[3] = {0, 0, 0},
              yd[3] = {0, 0, 0};
@@ -365,7 +373,7 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
           const int32_t ig = nm_pbase(g, x1) + own.off;
 #pragma unroll
           for (int c = 0; c < 3; ++c)
-            sm[q1a + c * kNP + eo] = on(c) ? __ldg(g.qghost[c] + ig) : 0.0;
+            sm[q1a + c * kNP1 + eo1] = on(c) ? __ldg(g.qghost[c] + ig) : 0.0;
         }
         cp_async_wait_all();
         __syncthreads();  // B_a: plane q's raw inputs have landed
@@ -419,10 +427,10 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             if (!on(c)) continue;
-            const double *qq = sm + q1c + c * kNP + eo;
-            const double off = cA[0] * sm[q1b + c * kNP + eo] +
-                               cA[1] * sm[q1d + c * kNP + eo] +
-                               cA[2] * qq[-kNZ] + cA[3] * qq[kNZ] +
+            const double *qq = sm + q1c + c * kNP1 + eo1;
+            const double off = cA[0] * sm[q1b + c * kNP1 + eo1] +
+                               cA[1] * sm[q1d + c * kNP1 + eo1] +
+                               cA[2] * qq[-kNZ1] + cA[3] * qq[kNZ1] +
                                cA[4] * qq[-1] + cA[5] * qq[1];
             const double out = ya[c] - off;
             g.out2[c][i3] = out;
@@ -469,14 +477,14 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
               if (on(c)) g.out1[c][i1] = qo[c];
           } else {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) qn[c * kNP + eo] = qo[c];
+            for (int c = 0; c < 3; ++c) qn[c * kNP1 + eo1] = qo[c];
             if (has_r1) {
               const bool okr = in1 && ring.ok;
 #pragma unroll
               for (int c = 0; c < 3; ++c) {
                 if (!on(c)) continue;
                 const int o = c * kNP + er;
-                qn[o] = okr ? djr * (cR[0] * gm[o] + cR[1] * gp[o] +
+                qn[c * kNP1 + er1] = okr ? djr * (cR[0] * gm[o] + cR[1] * gp[o] +
                                      cR[2] * gc[o - kNZ] +
                                      cR[3] * gc[o + kNZ] +
                                      cR[4] * gc[o - 1] + cR[5] * gc[o + 1])
