@@ -97,6 +97,7 @@ struct MgHierarchy {
   int ax_of[3];  // physical axis of canonical X, Y, Z (-1: absent)
   MgLevel lv[kMgMaxLevels];
   double omega;   // damping of the block-Jacobi line smoother
+  double corr;    // coarse-correction scale (restricted residual x corr)
   int spectral;   // level 0 only, preconditioned by the spectral solve
   SpecPlan sp;
 };

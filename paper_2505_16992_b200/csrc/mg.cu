@@ -219,7 +219,7 @@ __device__ __forceinline__ void resid_restrict_at(const MgLevel &F,
                                                   const double *r,
                                                   const double *x,
                                                   const MgLevel &C,
-                                                  int32_t I) {
+                                                  int32_t I, double corr) {
   const Cell3 cc = decode(C, I);
   double acc = 0.0;
   for (int dx = 0; dx < F.fx; ++dx)
@@ -233,17 +233,17 @@ __device__ __forceinline__ void resid_restrict_at(const MgLevel &F,
         const Nbhd b = nbhd(F, c);
         acc += r[c.i] - kx(b, c.i, x);
       }
-  C.r[I] = acc;
+  C.r[I] = corr * acc;
 }
 
 __global__ void __launch_bounds__(kBlock)
     k_mg_resid_restrict(MgLevel F, const double *__restrict__ r,
                         const double *__restrict__ x, MgLevel C,
-                        const int *done) {
+                        double corr, const int *done) {
   MG_DONE_RETURN;
   const int32_t I = blockIdx.x * blockDim.x + threadIdx.x;
   if (I >= C.n) return;
-  resid_restrict_at(F, r, x, C, I);
+  resid_restrict_at(F, r, x, C, I, corr);
 }
 
 // res = r - K (x + P x_c) at fine cell i: prolongation fused into the
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(1024)
       line_solve<0>(L, ln / L.sz, ln % L.sz, L.r, L.x, L.x, om);
     __syncthreads();
     for (int32_t I = tid; I < C.n; I += nt)
-      resid_restrict_at(L, L.r, L.x, C, I);
+      resid_restrict_at(L, L.r, L.x, C, I, h.corr);
     __syncthreads();
   }
   const MgLevel &E = h.lv[last];
@@ -383,6 +383,8 @@ static int64_t spec_level0_bytes(int64_t n) {
 bool mg_plan(const Plan &p, MgHierarchy &h, int64_t *bytes) {
   h.nlev = 0;
   h.omega = 0.85;
+  h.corr = 1.0;
+  if (const char *e = getenv("PF_MG_CORR")) h.corr = atof(e);
   h.spectral = 0;
   *bytes = 0;
   if (p.d.topo != PF_TOPO_BOX) return false;
@@ -546,7 +548,7 @@ static void vcycle(const MgHierarchy &h, int l, const double *r, double *x,
   launch(k_mg_smooth0, lines_grid(L), kLineBlock, s, L, r, x, h.omega, done);
   mark(1);
   launch(k_mg_resid_restrict, grid_for(C.n), kBlock, s, L, r,
-         (const double *)x, C, done);
+         (const double *)x, C, h.corr, done);
   mark(2);
   vcycle(h, l + 1, C.r, C.x, s, done, nullptr, nullptr, red_blocks,
          fused_from);

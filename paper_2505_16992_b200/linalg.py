@@ -64,6 +64,9 @@ def _global_n(plan):
 
 PRECOND_NONE, PRECOND_JACOBI, PRECOND_MG, PRECOND_NEUMANN2 = 0, 1, 2, 3
 _DEFAULT_MOM_PRECOND = os.environ.get("PF_MOMENTUM_PRECOND", "neumann2")
+# PF_PRESSURE_PRECOND=jacobi: Jacobi-PCG for the pressure even where the
+# plan has a spectral / multigrid preconditioner (A/B and debugging)
+_DEFAULT_P_PRECOND = os.environ.get("PF_PRESSURE_PRECOND", "auto")
 
 
 def _precond_flag(precond):
@@ -105,7 +108,8 @@ def cg_solve(plan, data, b, x0=None, tol=None, maxiter=None,
     if pc == -1:
         # multigrid is built for the zero-mean pressure operator (symmetric
         # face form with zero row sums); everything else gets Jacobi
-        pc = PRECOND_MG if (zero_mean and plan.has_mg) else PRECOND_JACOBI
+        pc = PRECOND_MG if (zero_mean and plan.has_mg and
+                            _DEFAULT_P_PRECOND != "jacobi") else PRECOND_JACOBI
     mgw = None
     if pc == PRECOND_MG:
         if not plan.mg_prepare(data):
