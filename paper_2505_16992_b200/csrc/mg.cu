@@ -4,6 +4,7 @@
 // Y lines of the smoother are strided by sz and threads of a warp take
 // consecutive z -- every line-solve load is coalesced across the warp.
 #include <algorithm>
+#include <mutex>
 
 #include "cgstate.cuh"
 #include "mg.cuh"
@@ -355,6 +356,119 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
+// The same V-cycle with every array of levels l0 .. last staged in shared
+// memory (small hierarchies: C1's coarse levels are ~22 KB): the serial
+// Thomas sweeps and the restrictions then chain on shared-memory latency
+// instead of L2 latency.  In: the coefficient arrays and level l0's rhs;
+// out: level l0's solution.  The level descriptors live in shared memory
+// too, their array pointers redirected to the staged copies.
+constexpr int kStagedThreads = 512;  // 128 registers: line_solve's chunks
+                                     // stay in registers (1024: spills)
+__global__ void __launch_bounds__(kStagedThreads)
+    k_mg_coarse_staged(MgHierarchy h, int l0, const int *done) {
+  MG_DONE_RETURN;
+  extern __shared__ __align__(16) double shm[];
+  __shared__ MgLevel slv[kMgMaxLevels];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int last = h.nlev - 1;
+  const double om = h.omega;
+  if (tid == 0) {
+    double *p = shm;
+    for (int l = l0; l <= last; ++l) {
+      MgLevel L = h.lv[l];
+      double **arr[8] = {&L.wx, &L.wy, &L.wz, &L.cp, &L.ivd,
+                         &L.r, &L.x, &L.t};
+      for (int k = 0; k < 8; ++k)
+        if (*arr[k]) {
+          *arr[k] = p;
+          p += L.n;
+        }
+      slv[l] = L;
+    }
+  }
+  __syncthreads();
+  for (int l = l0; l <= last; ++l) {
+    const MgLevel &G = h.lv[l], &S = slv[l];
+    const double *src[6] = {G.wx, G.wy, G.wz, G.cp, G.ivd,
+                            l == l0 ? G.r : nullptr};
+    double *dst[6] = {S.wx, S.wy, S.wz, S.cp, S.ivd, S.r};
+    for (int k = 0; k < 6; ++k)
+      if (src[k])
+        for (int32_t i = tid; i < G.n; i += nt) dst[k][i] = src[k][i];
+  }
+  __syncthreads();
+  for (int l = l0; l < last; ++l) {
+    const MgLevel &L = slv[l], &C = slv[l + 1];
+    for (int32_t ln = tid; ln < L.sx * L.sz; ln += nt)
+      line_solve<0>(L, ln / L.sz, ln % L.sz, L.r, L.x, L.x, om);
+    __syncthreads();
+    for (int32_t I = tid; I < C.n; I += nt)
+      resid_restrict_at(L, L.r, L.x, C, I, h.corr);
+    __syncthreads();
+  }
+  const MgLevel &E = slv[last];
+  if (E.pinned) {
+    coarsest_block(E);
+  } else {
+    for (int32_t ln = tid; ln < E.sx * E.sz; ln += nt)
+      line_solve<0>(E, ln / E.sz, ln % E.sz, E.r, E.x, E.x, om);
+    __syncthreads();
+    for (int it = 0; it < 4; ++it) {
+      for (int32_t i = tid; i < E.n; i += nt)
+        E.t[i] = E.r[i] - kx(nbhd(E, decode(E, i)), i, E.x);
+      __syncthreads();
+      for (int32_t ln = tid; ln < E.sx * E.sz; ln += nt)
+        line_solve<0>(E, ln / E.sz, ln % E.sz, E.t, E.t, E.t, om);
+      __syncthreads();
+      for (int32_t i = tid; i < E.n; i += nt) E.x[i] += E.t[i];
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  for (int l = last - 1; l >= l0; --l) {
+    const MgLevel &L = slv[l], &C = slv[l + 1];
+    for (int32_t i = tid; i < L.n; i += nt)
+      prolong_resid_at(L, L.r, L.x, L.t, C, i);
+    __syncthreads();
+    for (int32_t ln = tid; ln < L.sx * L.sz; ln += nt)
+      line_solve<2>(L, ln / L.sz, ln % L.sz, L.t, L.t, L.x, om, &C);
+    __syncthreads();
+  }
+  const double *xs = slv[l0].x;
+  double *xg = h.lv[l0].x;
+  for (int32_t i = tid; i < h.lv[l0].n; i += nt) xg[i] = xs[i];
+}
+
+// shared-memory bytes k_mg_coarse_staged needs for levels l0 .. last
+static size_t coarse_staged_bytes(const MgHierarchy &h, int l0) {
+  size_t b = 0;
+  for (int l = l0; l < h.nlev; ++l) {
+    const MgLevel &L = h.lv[l];
+    const double *arr[8] = {L.wx, L.wy, L.wz, L.cp, L.ivd, L.r, L.x, L.t};
+    for (int k = 0; k < 8; ++k)
+      if (arr[k]) b += sizeof(double) * (size_t)L.n;
+  }
+  return b;
+}
+constexpr size_t kCoarseStagedMax = 160 * 1024;
+
+static void launch_coarse(const MgHierarchy &h, int l0, cudaStream_t s,
+                          const int *done) {
+  const size_t b = coarse_staged_bytes(h, l0);
+  if (b > kCoarseStagedMax || getenv("PF_MG_NO_STAGE")) {
+    launch(k_mg_coarse_fused, 1, 1024, s, h, l0, done);
+    return;
+  }
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(k_mg_coarse_staged,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kCoarseStagedMax);
+  });
+  count_launch();
+  k_mg_coarse_staged<<<1, kStagedThreads, b, s>>>(h, l0, done);
+}
+
 // CG z-sums for the rare single-level hierarchy (no final smoother to fuse)
 __global__ void __launch_bounds__(kBlock)
     k_mg_zsum(const double *__restrict__ r, const double *__restrict__ z,
@@ -536,7 +650,7 @@ static void vcycle(const MgHierarchy &h, int l, const double *r, double *x,
   };
   const MgLevel &L = h.lv[l];
   if (l > 0 && (l >= fused_from || (l == h.nlev - 1 && !L.pinned))) {
-    launch(k_mg_coarse_fused, 1, 1024, s, h, l, done);
+    launch_coarse(h, l, s, done);
     return;
   }
   if (l == h.nlev - 1) {

@@ -220,6 +220,38 @@ def test_multigrid_pcg_converges_to_exact_solution(name):
     assert torch.equal(x, x2) and rep2.iterations == rep.iterations
 
 
+@pytest.mark.parametrize("shape", [(32, 32), (64, 48)])
+def test_multigrid_staged_coarse_cycle_matches_global(shape, monkeypatch):
+    """Small hierarchies run their coarse V-cycle from shared memory
+    (k_mg_coarse_staged); PF_MG_NO_STAGE=1 runs the same cycle on global
+    memory (k_mg_coarse_fused).  Same arithmetic per line and cell, so the
+    solves agree to rounding (the coarsest mean is reduced over a different
+    block size) with the same iteration counts, and both land on the exact
+    solution."""
+    from paper_2505_16992_b200 import linalg, mesh
+    dom = mesh.make_cavity(shape)
+    plan = _plan(dom, "multigrid")
+    assert plan.has_mg and plan.mg_levels >= 3
+    K = _pressure_operator(dom)
+    b = np.random.default_rng(3).standard_normal(dom.n)
+    Kt = torch.as_tensor(K, device="cuda:0")
+    bt = torch.as_tensor(b, device="cuda:0")
+    x_exact = O.solve_pressure_exact(dom, K, b)
+    out = {}
+    for staged in (True, False):
+        if staged:
+            monkeypatch.delenv("PF_MG_NO_STAGE", raising=False)
+        else:
+            monkeypatch.setenv("PF_MG_NO_STAGE", "1")
+        x, rep = linalg.cg_solve(plan, Kt, bt, tol=1e-11, zero_mean=True,
+                                 precond="mg")
+        assert rep.converged and not rep.fallback_used
+        assert G.rel(_np(x), x_exact) < 1e-8
+        out[staged] = (_np(x), rep.iterations)
+    assert abs(out[True][1] - out[False][1]) <= 1
+    assert G.rel(out[True][0], out[False][0]) < 1e-9
+
+
 SPECTRAL_DOMAINS = {
     "channel8": MG_DOMAINS["channel8"],
     "channel16": MG_DOMAINS["channel16"],
