@@ -361,11 +361,15 @@ __global__ void __launch_bounds__(1024)
 // Thomas sweeps and the restrictions then chain on shared-memory latency
 // instead of L2 latency.  In: the coefficient arrays and level l0's rhs;
 // out: level l0's solution.  The level descriptors live in shared memory
-// too, their array pointers redirected to the staged copies.
-constexpr int kStagedThreads = 512;  // 128 registers: line_solve's chunks
-                                     // stay in registers (1024: spills)
+// too, their array pointers redirected to the staged copies.  From l0 = 0
+// (a whole small hierarchy: C1's 1,024-cell cavity) it is the entire
+// V-cycle in one launch instead of five, and with `fz.st` its last
+// smoothing sweep also forms the CG z-sums and beta (k_mg_smooth2_cg's
+// fusion, reduced over the block).
+constexpr int kStagedThreads = 256;  // 255 registers: line_solve's chunks
+                                     // stay in registers (512: spills)
 __global__ void __launch_bounds__(kStagedThreads)
-    k_mg_coarse_staged(MgHierarchy h, int l0, const int *done) {
+    k_mg_coarse_staged(MgHierarchy h, int l0, CgFuse fz, const int *done) {
   MG_DONE_RETURN;
   extern __shared__ __align__(16) double shm[];
   __shared__ MgLevel slv[kMgMaxLevels];
@@ -425,14 +429,27 @@ __global__ void __launch_bounds__(kStagedThreads)
     }
   }
   __syncthreads();
+  const bool sums_on = l0 == 0 && fz.st;
+  double sums[3] = {0.0, 0.0, 0.0};
   for (int l = last - 1; l >= l0; --l) {
     const MgLevel &L = slv[l], &C = slv[l + 1];
     for (int32_t i = tid; i < L.n; i += nt)
       prolong_resid_at(L, L.r, L.x, L.t, C, i);
     __syncthreads();
-    for (int32_t ln = tid; ln < L.sx * L.sz; ln += nt)
-      line_solve<2>(L, ln / L.sz, ln % L.sz, L.t, L.t, L.x, om, &C);
+    for (int32_t ln = tid; ln < L.sx * L.sz; ln += nt) {
+      if (l == 0 && sums_on)
+        line_solve<2, true>(L, ln / L.sz, ln % L.sz, L.t, L.t, L.x, om, &C,
+                            sums);
+      else
+        line_solve<2>(L, ln / L.sz, ln % L.sz, L.t, L.t, L.x, om, &C);
+    }
     __syncthreads();
+  }
+  if (sums_on) {
+    block_reduce<3>(sums);
+    if (tid == 0)
+      cg_fin_z(fz.st, sums[0], sums[1], sums[2], (int32_t)slv[0].n,
+               fz.initial != 0);
   }
   const double *xs = slv[l0].x;
   double *xg = h.lv[l0].x;
@@ -452,10 +469,16 @@ static size_t coarse_staged_bytes(const MgHierarchy &h, int l0) {
 }
 constexpr size_t kCoarseStagedMax = 160 * 1024;
 
+static bool staged_ok(const MgHierarchy &h, int l0) {
+  return coarse_staged_bytes(h, l0) <= kCoarseStagedMax &&
+         !getenv("PF_MG_NO_STAGE");
+}
+
 static void launch_coarse(const MgHierarchy &h, int l0, cudaStream_t s,
-                          const int *done) {
+                          const int *done,
+                          CgFuse fz = CgFuse{nullptr, nullptr, nullptr, 0}) {
   const size_t b = coarse_staged_bytes(h, l0);
-  if (b > kCoarseStagedMax || getenv("PF_MG_NO_STAGE")) {
+  if (!staged_ok(h, l0)) {
     launch(k_mg_coarse_fused, 1, 1024, s, h, l0, done);
     return;
   }
@@ -466,7 +489,7 @@ static void launch_coarse(const MgHierarchy &h, int l0, cudaStream_t s,
                          (int)kCoarseStagedMax);
   });
   count_launch();
-  k_mg_coarse_staged<<<1, kStagedThreads, b, s>>>(h, l0, done);
+  k_mg_coarse_staged<<<1, kStagedThreads, b, s>>>(h, l0, fz, done);
 }
 
 // CG z-sums for the rare single-level hierarchy (no final smoother to fuse)
@@ -704,6 +727,12 @@ int mg_apply(const MgHierarchy &h, const double *r, double *z, cudaStream_t s,
       launch(k_mg_zsum, std::min(grid_for(hh.lv[0].n), red_blocks), kBlock,
              s, (const double *)r, (const double *)z, (int32_t)hh.lv[0].n,
              *fuse, done);
+  } else if (!ev && hh.lv[0].n <= kFusedCoarseMax && staged_ok(hh, 0) &&
+             (!fuse || fuse->st)) {
+    // a whole small hierarchy: one staged single-CTA V-cycle (the level-0
+    // passes are latency, not bandwidth, at a few thousand cells)
+    launch_coarse(hh, 0, s, done,
+                  fuse ? *fuse : CgFuse{nullptr, nullptr, nullptr, 0});
   } else {
     vcycle(hh, 0, r, z, s, done, ev, fuse, red_blocks, fused_from);
   }

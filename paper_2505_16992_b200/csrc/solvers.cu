@@ -2167,14 +2167,10 @@ void launch_nm(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
     static std::set<const void *> done;
     {
       std::lock_guard<std::mutex> lock(mu);
-      if (done.insert(reinterpret_cast<const void *>(kernel)).second) {
+      if (done.insert(reinterpret_cast<const void *>(kernel)).second)
         cudaFuncSetAttribute(kernel,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)kNmSmem);
-        cudaFuncSetAttribute(kernel,
-                             cudaFuncAttributePreferredSharedMemoryCarveout,
-                             100);
-      }
     }
     count_launch();
     kernel<<<grid, kTileThreads, kNmSmem, s>>>(tg, g, st, w.partials,
