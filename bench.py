@@ -1,7 +1,7 @@
 """Benchmark: forward + adjoint PISO steps on the 3D turbulent channel.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c4|c5|c5train|slab8] [--no-cpu-baseline]
+                    [--config c1|c2|c3|c4|c5|c5train|slab8] [--no-cpu-baseline]
 
 --gpus N > 1 without torchrun starts the N ranks itself.
 
