@@ -2662,10 +2662,12 @@ extern "C" int pf_bicgstab_profile(const pf_plan *plan, const double *a,
     const bool tiled = tile_geo(pl, v, tg);
     const int tgrid = tiled ? std::min(tg.ntiles, pl.red_blocks) : 0;
     // the production preconditioner, as linalg.py picks it: Neumann-2 where
-    // its tiled passes run, Jacobi when PF_MOMENTUM_PRECOND=jacobi
+    // its tiled passes run (slab plans of several ranks: only when
+    // PF_MOMENTUM_PRECOND=neumann2), Jacobi when PF_MOMENTUM_PRECOND=jacobi
     TileGeo tge;
     const char *mp = getenv("PF_MOMENTUM_PRECOND");
-    const bool nm = (!mp || std::string(mp) == "neumann2") &&
+    const bool multi = pl.slab && pl.d.slab_world > 1;
+    const bool nm = (mp ? std::string(mp) == "neumann2" : !multi) &&
                     nm_geo(pl, v, tgn, &tge);
     const int ngrid = nm ? std::min(tgn.ntiles, nm_minb() * pl.num_sms) : 0;
     const int egrid = nm ? std::min(tge.ntiles, nm_minb() * pl.num_sms) : 0;

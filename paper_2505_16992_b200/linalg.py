@@ -64,6 +64,12 @@ def _global_n(plan):
 
 PRECOND_NONE, PRECOND_JACOBI, PRECOND_MG, PRECOND_NEUMANN2 = 0, 1, 2, 3
 _DEFAULT_MOM_PRECOND = os.environ.get("PF_MOMENTUM_PRECOND", "neumann2")
+# slab plans of more than one rank: Jacobi unless PF_MOMENTUM_PRECOND names
+# the polynomial explicitly -- its edge passes and the extra exchanges of
+# their stage-1 planes cost more than the halved iteration count saves
+# (profiles/r2_s4/slab_overhead_*: C4 as 2 / 8 slabs 37.6 / 51.8 ms per step
+# with Jacobi against 39.4 / 54.0 with Neumann-2)
+_SLAB_MOM_PRECOND = os.environ.get("PF_MOMENTUM_PRECOND", "jacobi")
 # PF_PRESSURE_PRECOND=jacobi: Jacobi-PCG for the pressure even where the
 # plan has a spectral / multigrid preconditioner (A/B and debugging)
 _DEFAULT_P_PRECOND = os.environ.get("PF_PRESSURE_PRECOND", "auto")
@@ -82,6 +88,16 @@ def _precond_flag(precond):
     if precond in ("neumann2", "poly2"):
         return PRECOND_NEUMANN2
     return -1        # auto
+
+
+def auto_momentum_precond(plan):
+    """The momentum BiCGStab preconditioner "ilu0" / "auto" resolves to:
+    Neumann-2 on one domain, Jacobi on slab plans of several ranks (the
+    library degrades Neumann-2 to Jacobi where its tiled passes do not
+    run); PF_MOMENTUM_PRECOND overrides both."""
+    multi = getattr(plan.domain, "world", 1) > 1
+    pick = _SLAB_MOM_PRECOND if multi else _DEFAULT_MOM_PRECOND
+    return PRECOND_NEUMANN2 if pick == "neumann2" else PRECOND_JACOBI
 
 
 def _report(c, stage):
@@ -154,8 +170,7 @@ def bicgstab_solve(plan, data, b, x0=None, tol=None, maxiter=None,
     # ms with Jacobi (profiles/r2_nm_light.txt).  PF_MOMENTUM_PRECOND=jacobi
     # selects Jacobi
     if pc == -1:
-        pc = PRECOND_NEUMANN2 if _DEFAULT_MOM_PRECOND == "neumann2" \
-            else PRECOND_JACOBI
+        pc = auto_momentum_precond(plan)
     elif pc == PRECOND_MG:
         pc = PRECOND_JACOBI
     with _lib.nvtx(stages[0] if stages else stage):

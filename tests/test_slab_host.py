@@ -146,3 +146,25 @@ def test_owned_cells_tile_the_mesh_world2(tmp_path):
     dom = mesh.make_channel((8, 6, 4), ratio=1.1)
     assert torch.equal(res["rows"], torch.arange(dom.n))
     assert res["counts"].tolist() == [float(f.m) for f in dom.bfaces]
+
+
+def test_auto_momentum_preconditioner_per_plan(monkeypatch):
+    """precond="ilu0" resolves to Neumann-2 on one domain and to Jacobi on a
+    slab plan of several ranks (measured cheaper there); a one-rank slab
+    keeps Neumann-2; PF_MOMENTUM_PRECOND (read at import) overrides both."""
+    from types import SimpleNamespace
+    from paper_2505_16992_b200 import linalg
+    dom = mesh.make_channel((8, 16, 32), ratio=1.05)
+    plans = {w: SimpleNamespace(domain=slab.SlabDomain(dom, 0, w))
+             for w in (1, 2, 8)}
+    single = SimpleNamespace(domain=dom)
+    monkeypatch.setattr(linalg, "_DEFAULT_MOM_PRECOND", "neumann2")
+    monkeypatch.setattr(linalg, "_SLAB_MOM_PRECOND", "jacobi")
+    assert linalg.auto_momentum_precond(single) == linalg.PRECOND_NEUMANN2
+    assert linalg.auto_momentum_precond(plans[1]) == linalg.PRECOND_NEUMANN2
+    for w in (2, 8):
+        assert linalg.auto_momentum_precond(plans[w]) == linalg.PRECOND_JACOBI
+    monkeypatch.setattr(linalg, "_SLAB_MOM_PRECOND", "neumann2")
+    assert linalg.auto_momentum_precond(plans[8]) == linalg.PRECOND_NEUMANN2
+    monkeypatch.setattr(linalg, "_DEFAULT_MOM_PRECOND", "jacobi")
+    assert linalg.auto_momentum_precond(single) == linalg.PRECOND_JACOBI
