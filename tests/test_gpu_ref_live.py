@@ -151,7 +151,9 @@ def _cots(rng, n, d, steps):
 
 
 def test_channel_tiled_spectral_path_matches_reference(R):
-    """C4 recipe at 64x48x64: tiled BiCGStab + spectral PCG vs reference."""
+    """C4 recipe at 64x48x64: the production path -- Neumann-2 tiled
+    BiCGStab passes (Y = 48, Z = 64 are whole 8 x 32 tiles) + spectral PCG
+    -- vs the reference."""
     from paper_2505_16992_b200 import mesh, plan as _plan  # noqa: F401
     shape = (64, 48, 64)
     rdom = RL.channel(R["mesh"], shape)
@@ -166,6 +168,9 @@ def test_channel_tiled_spectral_path_matches_reference(R):
     # the timed kernels really ran: spectral preconditioner, tiled passes
     plan = odom.device_plan(torch.device("cuda:0"))
     assert plan.geom_kind == "spectral"
+    from paper_2505_16992_b200 import linalg
+    assert linalg.auto_momentum_precond(plan) == linalg.PRECOND_NEUMANN2
+    assert shape[1] % 8 == 0 and shape[2] % 32 == 0
     ref = _run_reference(R, rdom, u0, None, dt, nu, steps, cots,
                          forcing=True)
     _compare("channel 64x48x64", ref, ours)
