@@ -1048,7 +1048,11 @@ def main():
     main = torch.cuda.current_stream(dev)
     s_out = torch.cuda.Stream(dev)
     s_in = torch.cuda.Stream(dev)
-    n_chunks = 8
+    # large fields move in 8 chunks so the next step's upload starts behind
+    # the first chunk's download; small ones (C1, C5) in one copy each --
+    # every chunk is a few host-side calls and stream events, which at a
+    # few ms per step cost more than the overlap gains
+    n_chunks = 8 if nU * 8 >= (64 << 20) else 1
 
     def bcs_in(slot):
         with torch.cuda.stream(s_in):
@@ -1057,81 +1061,93 @@ def main():
             ev.record(s_in)
         return bcs, ev
 
+    def e2e_loop(nsteps, s0, t_state, n_state):
+        """nsteps end-to-end steps from host slot s0; returns the device
+        time, the per-step marks and where the trajectory continues."""
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e2 = torch.cuda.Event(enable_timing=True)
+        e3 = torch.cuda.Event(enable_timing=True)
+        e2.record(main)
+        with torch.cuda.stream(s_in):
+            u_in = u_host[s0].to(dev, non_blocking=True)
+            p_in = p_host[s0].to(dev, non_blocking=True)
+        bc_in, ev = bcs_in(s0)
+        e2e_marks = []
+        for k in range(nsteps):
+            main.wait_event(ev)
+            for t in [u_in, p_in] + bc_in:
+                t.record_stream(main)
+            st = piso.FlowState(u=u_in.view(d_loc, n_loc).t(), p=p_in, bc=bc_in,
+                                t=t_state, step=n_state)
+            new, dg, tape = fwd(st)
+            t_state, n_state = new.t, new.step
+            done_f = torch.cuda.Event()
+            done_f.record(main)
+            slot = (s0 + k + 1) % 2
+            last = k + 1 == nsteps
+            u_nx = None if last else torch.empty(nU, dtype=torch.float64,
+                                                 device=dev)
+            p_nx = None if last else torch.empty(nP, dtype=torch.float64,
+                                                 device=dev)
+            s_out.wait_event(done_f)
+            for src, hst, dst in ((flat(new.u), u_host[slot], u_nx),
+                                  (flat(new.p), p_host[slot], p_nx)):
+                src.record_stream(s_out)
+                m = src.numel()
+                for c in range(n_chunks):
+                    a, b = m * c // n_chunks, m * (c + 1) // n_chunks
+                    with torch.cuda.stream(s_out):
+                        hst[a:b].copy_(src[a:b], non_blocking=True)
+                        e_c = torch.cuda.Event()
+                        e_c.record(s_out)
+                    if dst is not None:
+                        s_in.wait_event(e_c)
+                        with torch.cuda.stream(s_in):
+                            dst[a:b].copy_(hst[a:b], non_blocking=True)
+            with torch.cuda.stream(s_out):
+                for hb, nb in zip(bc_host[slot], new.bc):
+                    hb.copy_(nb, non_blocking=True)
+                    nb.record_stream(s_out)
+                e_bc = torch.cuda.Event()
+                e_bc.record(s_out)
+            if not last:
+                u_nx.record_stream(s_in)
+                p_nx.record_stream(s_in)
+                u_in, p_in = u_nx, p_nx
+                s_in.wait_event(e_bc)
+                bc_in, ev = bcs_in(slot)
+            g = adj(tape)
+            count(dg, g)
+            done_a = torch.cuda.Event(enable_timing=True)
+            done_a.record(main)
+            e2e_marks.append(done_a)
+            s_out.wait_event(done_a)
+            with torch.cuda.stream(s_out):
+                gf = flat(g.u)
+                g_host[k % 2].copy_(gf, non_blocking=True)
+            gf.record_stream(s_out)
+        main.wait_stream(s_out)
+        main.wait_stream(s_in)
+        e3.record(main)
+        torch.cuda.synchronize()
+        ms_e2e = e2.elapsed_time(e3)
+        e2e_step_ms, prev = [], e2
+        for mk in e2e_marks:
+            e2e_step_ms.append(round(prev.elapsed_time(mk), 3))
+            prev = mk
+        return ms_e2e, e2e_step_ms, (s0 + nsteps) % 2, t_state, n_state
+
+    # untimed warm-up of the same loop (allocator blocks, first pinned
+    # transfers), then the timed run continuing the trajectory
+    s0, t_state, n_state = 0, state.t, state.step
+    if args.warmup > 0:
+        _, _, s0, t_state, n_state = e2e_loop(args.warmup, s0, t_state,
+                                              n_state)
     e2e_stats0 = dict(stats)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e2 = torch.cuda.Event(enable_timing=True)
-    e3 = torch.cuda.Event(enable_timing=True)
-    e2.record(main)
-    with torch.cuda.stream(s_in):
-        u_in = u_host[0].to(dev, non_blocking=True)
-        p_in = p_host[0].to(dev, non_blocking=True)
-    bc_in, ev = bcs_in(0)
-    t_state, n_state = state.t, state.step
-    e2e_marks = []
-    for k in range(args.steps):
-        main.wait_event(ev)
-        for t in [u_in, p_in] + bc_in:
-            t.record_stream(main)
-        st = piso.FlowState(u=u_in.view(d_loc, n_loc).t(), p=p_in, bc=bc_in,
-                            t=t_state, step=n_state)
-        new, dg, tape = fwd(st)
-        t_state, n_state = new.t, new.step
-        done_f = torch.cuda.Event()
-        done_f.record(main)
-        slot = (k + 1) % 2
-        last = k + 1 == args.steps
-        u_nx = None if last else torch.empty(nU, dtype=torch.float64,
-                                             device=dev)
-        p_nx = None if last else torch.empty(nP, dtype=torch.float64,
-                                             device=dev)
-        s_out.wait_event(done_f)
-        for src, hst, dst in ((flat(new.u), u_host[slot], u_nx),
-                              (flat(new.p), p_host[slot], p_nx)):
-            src.record_stream(s_out)
-            m = src.numel()
-            for c in range(n_chunks):
-                a, b = m * c // n_chunks, m * (c + 1) // n_chunks
-                with torch.cuda.stream(s_out):
-                    hst[a:b].copy_(src[a:b], non_blocking=True)
-                    e_c = torch.cuda.Event()
-                    e_c.record(s_out)
-                if dst is not None:
-                    s_in.wait_event(e_c)
-                    with torch.cuda.stream(s_in):
-                        dst[a:b].copy_(hst[a:b], non_blocking=True)
-        with torch.cuda.stream(s_out):
-            for hb, nb in zip(bc_host[slot], new.bc):
-                hb.copy_(nb, non_blocking=True)
-                nb.record_stream(s_out)
-            e_bc = torch.cuda.Event()
-            e_bc.record(s_out)
-        if not last:
-            u_nx.record_stream(s_in)
-            p_nx.record_stream(s_in)
-            u_in, p_in = u_nx, p_nx
-            s_in.wait_event(e_bc)
-            bc_in, ev = bcs_in(slot)
-        g = adj(tape)
-        count(dg, g)
-        done_a = torch.cuda.Event(enable_timing=True)
-        done_a.record(main)
-        e2e_marks.append(done_a)
-        s_out.wait_event(done_a)
-        with torch.cuda.stream(s_out):
-            gf = flat(g.u)
-            g_host[k % 2].copy_(gf, non_blocking=True)
-        gf.record_stream(s_out)
-    main.wait_stream(s_out)
-    main.wait_stream(s_in)
-    e3.record(main)
-    torch.cuda.synchronize()
-    ms_e2e = e2.elapsed_time(e3)
-    e2e_step_ms, prev = [], e2
-    for mk in e2e_marks:
-        e2e_step_ms.append(round(prev.elapsed_time(mk), 3))
-        prev = mk
+    ms_e2e, e2e_step_ms, _, _, _ = e2e_loop(args.steps, s0, t_state,
+                                            n_state)
     if world > 1:
         t = torch.tensor([ms_e2e], device="cpu" if share_dev() else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
