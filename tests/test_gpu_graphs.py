@@ -42,19 +42,49 @@ print(json.dumps({"hash": h.hexdigest(), "it": [dg.momentum_iterations, dg.press
 '''
 
 
-def _run(env_updates, drop):
+def _run(env_updates, drop, script=SCRIPT):
     env = dict(os.environ)
     env.update(env_updates)
     for k in drop:
         env.pop(k, None)
-    out = subprocess.run([sys.executable, "-c", SCRIPT, ROOT], env=env,
+    out = subprocess.run([sys.executable, "-c", script, ROOT], env=env,
                          capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stderr[-2000:]
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
-def test_graphs_and_batches_match_test_settings():
-    prod = _run({}, ["PF_NO_GRAPHS", "PF_MAX_BATCH"])
-    test = _run({"PF_NO_GRAPHS": "1", "PF_MAX_BATCH": "4"}, [])
+# C1 (32^2 cavity): the whole multigrid V-cycle is one staged single-CTA
+# kernel with the CG z-sums folded in (mg.cu k_mg_coarse_staged)
+SCRIPT_C1 = r'''
+import hashlib, json, sys
+import numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2505_16992_b200 import adjoint, mesh, piso
+dev = torch.device("cuda:0")
+dom = mesh.make_cavity((32, 32))
+plan = dom.device_plan(dev)
+assert plan.geom_kind == "multigrid"
+g = torch.Generator(device="cpu").manual_seed(1)
+w = torch.randn((dom.n, 2), generator=g, dtype=torch.float64).to(dev)
+ws = piso.PisoWorkspace(dom)
+st = piso.make_state(dom, u0=np.zeros((dom.n, 2)), device=dev)
+for k in range(5):
+    cfg = piso.StepConfig(dt=0.02, nu=0.01, tol=1e-10)
+    tape = piso.StepTape()
+    st, dg = piso.piso_step(dom, st, cfg, ws, tape)
+    gr = adjoint.backward_step(dom, tape, adjoint.GradState(u=w, p=None), tol=1e-10)
+torch.cuda.synchronize()
+h = hashlib.sha256()
+for t in (st.u, st.p, gr.u):
+    h.update(t.contiguous().cpu().numpy().tobytes())
+print(json.dumps({"hash": h.hexdigest(), "it": [dg.momentum_iterations, dg.pressure_iterations, gr.solve_iterations]}))
+'''
+
+
+@pytest.mark.parametrize("script", ["channel", "cavity_c1"])
+def test_graphs_and_batches_match_test_settings(script):
+    src = SCRIPT if script == "channel" else SCRIPT_C1
+    prod = _run({}, ["PF_NO_GRAPHS", "PF_MAX_BATCH"], src)
+    test = _run({"PF_NO_GRAPHS": "1", "PF_MAX_BATCH": "4"}, [], src)
     assert prod["it"] == test["it"]
     assert prod["hash"] == test["hash"], "graph replay changed the result"
