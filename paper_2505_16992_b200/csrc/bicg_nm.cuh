@@ -68,8 +68,16 @@ static_assert(kNZ % 2 == 0 && kNPairs <= kTileThreads, "pair layout");
 // stage 1 writes q-1, and reads its X neighbours from the ring)
 constexpr int kNmRawN = 13, kNmDi = 12;  // raw arrays; 1/A's slot
 constexpr int kNmRaw = 0, kNmG1 = kNmRawN * kNP, kNmQ1 = kNmG1 + 9 * kNP,
-              kNmCo = kNmQ1 + 12 * kNP1, kNmEnd = kNmCo + 10;
-constexpr size_t kNmSmem = sizeof(double) * kNmEnd;   // 108,752 B
+              kNmCo = kNmQ1 + 12 * kNP1, kNmCf = kNmCo + 10,
+              kNmEnd = kNmCf + 12 * kTileThreads;
+// The transposed passes park each plane's own (gathered) row for its stage 2
+// two plane steps later (two slots x 6 rows x 256 cells): adjoint st 763 ->
+// 739 us; the forward passes, whose own row is one coalesced load per face,
+// measured 1.7 % slower with it and keep the smaller buffer (more L1)
+template <bool kTrans>
+constexpr size_t nm_smem() {
+  return sizeof(double) * (kTrans ? kNmEnd : kNmCf);  // 133,328 / 108,752 B
+}
 
 // halo-1 ring cell k (0..83) in plane coordinates
 __device__ __forceinline__ void nm_ring1(int k, int &sy, int &sz) {
@@ -346,9 +354,7 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
         if (S2) {
           const int32_t b3 = nm_pbase(g, x3);
           i3 = b3 + own.off;
-          const int32_t bm = kTrans ? nm_pbase(g, x3 - 1) : 0;
-          const int32_t bp = kTrans ? nm_pbase(g, x3 + 1) : 0;
-          nm_coefs<kTrans>(g, b3, bm, bp, own, cA);
+          if (!kTrans) nm_coefs<false>(g, b3, 0, 0, own, cA);
           {
 #pragma unroll
             for (int c = 0; c < 3; ++c)
@@ -423,6 +429,13 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
           }
         }
         if (S2) {
+          // the own row of plane x3: stage 1 loaded it two steps ago and
+          // parked it in shared memory (own cell only, no barrier needed)
+          if (kTrans) {
+            const double *cf = sm + kNmCf + (x3 & 1) * 6 * kTileThreads + tid;
+#pragma unroll
+            for (int f = 0; f < 6; ++f) cA[f] = cf[f * kTileThreads];
+          }
           // q1 of planes x3 - 1, x3, x3 + 1: slots q1b, q1c, q1d
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
@@ -464,6 +477,12 @@ __global__ void __launch_bounds__(kTileThreads, kMinB)
             qo[c] = djo * (cB[0] * gm[o] + cB[1] * gp[o] +
                            cB[2] * gc[o - kNZ] + cB[3] * gc[o + kNZ] +
                            cB[4] * gc[o - 1] + cB[5] * gc[o + 1]);
+          }
+          if (kTrans && !one && in1) {
+            // stage 2 of plane x1 (two steps on) reuses this own row
+            double *cf = sm + kNmCf + (x1 & 1) * 6 * kTileThreads + tid;
+#pragma unroll
+            for (int f = 0; f < 6; ++f) cf[f * kTileThreads] = cB[f];
           }
           if (kClose) {
             const int32_t i1 = b1 + own.off;

@@ -2170,11 +2170,11 @@ void launch_nm(const TileGeo &tg, int grid, cudaStream_t s, const double *a,
       if (done.insert(reinterpret_cast<const void *>(kernel)).second)
         cudaFuncSetAttribute(kernel,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kNmSmem);
+                             (int)nm_smem<kTrans>());
     }
     count_launch();
-    kernel<<<grid, kTileThreads, kNmSmem, s>>>(tg, g, st, w.partials,
-                                               w.counters, edge);
+    kernel<<<grid, kTileThreads, nm_smem<kTrans>(), s>>>(tg, g, st, w.partials,
+                                                         w.counters, edge);
   };
   if (nm_minb() == 1) {
     if constexpr (MODE == 0) {
